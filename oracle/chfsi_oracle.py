@@ -1,0 +1,336 @@
+"""CPU oracle for the ChFSI hot path — TEST INFRASTRUCTURE ONLY.
+
+This module is a numpy restatement of the reference `spectral_chain` solver
+path. Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s
+`cpu_baseline` / `--impl reference` legs may import it, and only as the
+checker or the timed CPU baseline — never as the thing measured or shipped.
+The product path (`paper_1206_3768_b200`) never imports it.
+
+Pinning: `tests/golden/make_golden.py` runs the unmodified reference
+(imported read-only from `/root/reference/pkg/src`) on seeded inputs and
+commits the results under `tests/golden/`; `tests/test_oracle_golden.py`
+checks every function below against those vectors (counts exactly, values
+bitwise or to 1e-12).
+
+Each function cites the reference file:line it restates (paths relative to
+`/root/reference/pkg/src/spectral_chain/`).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.linalg
+
+RANK_TOL = 1e-13          # linalg.py:173 (|R_ii| < 1e-13 ||Y||_F)
+LANCZOS_BREAKDOWN = 1e-14  # chfsi.py:152
+RANK_RETRIES = 3           # chfsi.py:242
+
+
+class OracleRankDeficient(ValueError):
+    def __init__(self, indices):
+        self.indices = tuple(int(i) for i in indices)
+        super().__init__(f"rank-deficient columns {self.indices}")
+
+
+# ----------------------------------------------------------------- config ---
+
+def resolve(n, nev, blk=None, deg=25, tol=1e-10, lanczos_steps=None, max_repeats=50):
+    """Size-dependent defaults; restates chfsi.py:53-69."""
+    width = nev + 40 if blk is None else blk
+    width = min(width, n)
+    if not 1 <= nev <= width <= n:
+        raise ValueError("need 1 <= nev <= blk <= n")
+    if deg < 1 or tol <= 0:
+        raise ValueError("bad degree or tolerance")
+    if lanczos_steps is None:
+        k = max(min(3 * width, max(10, n // 10)), min(10, 3 * width))
+    else:
+        k = lanczos_steps
+    return width, deg, tol, max(2, min(k, n)), max_repeats
+
+
+def safe_window(scale_ref, a, b):
+    """Window clamp; restates chfsi.py:264-271. Returns (a, b, scale_ref)."""
+    finite = np.isfinite(scale_ref) and np.isfinite(a) and np.isfinite(b)
+    if not finite or not scale_ref < b:
+        return scale_ref + 0.5, scale_ref + 1.0, scale_ref
+    if not (scale_ref < a and a < b):
+        a = scale_ref + 0.5 * (b - scale_ref)
+    return a, b, scale_ref
+
+
+def filter_coefficients(deg, a, b, scale_ref):
+    """Per-step (alpha_j, beta_j) and the shift c of chfsi.py:198-207.
+
+    Step j computes ``Y_j = alpha_j (H Y_{j-1} - c Y_{j-1}) - beta_j Y_{j-2}``
+    (beta_1 = 0).
+    """
+    e = (b - a) / 2
+    c = (b + a) / 2
+    sigma = e / (scale_ref - c)
+    tau = 2.0 / sigma
+    alphas, betas = [sigma / e], [0.0]
+    for _ in range(deg - 1):
+        sn = 1.0 / (tau - sigma)
+        alphas.append(2 * sn / e)
+        betas.append(sigma * sn)
+        sigma = sn
+    return c, alphas, betas
+
+
+# ---------------------------------------------------------------- kernels ---
+
+def chebyshev_filter(h, y, deg, a, b, scale_ref):
+    """Degree-``deg`` scaled Chebyshev filter; restates chfsi.py:179-208."""
+    if deg < 1:
+        raise ValueError("polynomial degree must be >= 1")
+    y0 = np.asarray(y, dtype=np.complex128)
+    if y0.shape[0] != h.shape[0]:
+        raise ValueError("shape mismatch")
+    c, alphas, betas = filter_coefficients(deg, a, b, scale_ref)
+    older, cur = y0, alphas[0] * (h @ y0 - c * y0)
+    for j in range(1, deg):
+        nxt = alphas[j] * (h @ cur - c * cur) - betas[j] * older
+        older, cur = cur, nxt
+    return cur
+
+
+def chebyshev_response(lam, deg, a, b, scale_ref):
+    """Scalar twin of the filter; restates chfsi.py:211-225."""
+    x = np.asarray(lam, dtype=float)
+    c, alphas, betas = filter_coefficients(deg, a, b, scale_ref)
+    older, cur = np.ones_like(x), alphas[0] * (x - c)
+    for j in range(1, deg):
+        older, cur = cur, alphas[j] * (x - c) * cur - betas[j] * older
+    return cur
+
+
+def lanczos(h, k, rng):
+    """Lanczos with full reorthogonalization; restates chfsi.py:125-162.
+
+    Returns (ritz values ascending, final residual norm, steps taken).
+    """
+    n = h.shape[0]
+    k = min(k, n)
+    v = np.zeros((n, k), dtype=np.complex128)
+    al = np.zeros(k)
+    be = np.zeros(max(k - 1, 0))
+    q = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    q = q / np.linalg.norm(q)
+    last = 0.0
+    taken = 0
+    for i in range(k):
+        v[:, i] = q
+        taken = i + 1
+        u = h @ q
+        al[i] = np.real(np.vdot(q, u))
+        r = u - al[i] * q
+        if i:
+            r = r - be[i - 1] * v[:, i - 1]
+        basis = v[:, :taken]
+        r = r - basis @ (basis.conj().T @ r)
+        last = float(np.linalg.norm(r))
+        if last < LANCZOS_BREAKDOWN or i == k - 1:
+            break
+        be[i] = last
+        q = r / last
+    t = np.diag(al[:taken]) + np.diag(be[: taken - 1], 1) + np.diag(be[: taken - 1], -1)
+    return np.linalg.eigvalsh(t), last, taken
+
+
+def qr_orthonormalize(y):
+    """Householder QR with positive-real R diagonal; restates linalg.py:152-178."""
+    m = np.asarray(y, dtype=np.complex128)
+    if m.ndim == 1:
+        m = m[:, None]
+    if m.shape[0] < m.shape[1]:
+        raise ValueError("need rows >= cols")
+    q, r = np.linalg.qr(m)
+    dg = np.diagonal(r)
+    dead = np.flatnonzero(np.abs(dg) < RANK_TOL * np.linalg.norm(m))
+    if dead.size:
+        raise OracleRankDeficient(dead)
+    return np.asfortranarray(q * (dg / np.abs(dg)).conj())
+
+
+def random_block(rng, n, cols):
+    """Complex Gaussian block, real then imaginary draw; restates _util.py:15-18."""
+    re = rng.standard_normal((n, cols))
+    return np.asfortranarray(re + 1j * rng.standard_normal((n, cols)))
+
+
+def orthonormalize_panel(panel, locked, rng):
+    """Two CGS passes vs locked, QR, rank repair; restates chfsi.py:242-261."""
+    work = panel
+    for attempt in range(RANK_RETRIES + 1):
+        if locked.shape[1]:
+            for _ in range(2):
+                work = work - locked @ (locked.conj().T @ work)
+        try:
+            return qr_orthonormalize(work)
+        except OracleRankDeficient as err:
+            if attempt == RANK_RETRIES:
+                raise
+            work = np.array(work, copy=True)
+            work[:, list(err.indices)] = random_block(rng, work.shape[0], len(err.indices))
+    raise AssertionError("unreachable")
+
+
+def hermitian_eig(g):
+    """Dense Hermitian eigensolver; restates linalg.py:181-206 (zheevd)."""
+    vals, vecs = np.linalg.eigh(np.asarray(g, dtype=np.complex128))
+    return vals, np.asfortranarray(vecs)
+
+
+# ----------------------------------------------------------------- solver ---
+
+@dataclass
+class OracleReport:
+    """Mirror of SolveReport (chfsi.py:101-122) plus the chained-mode tail (G2)."""
+
+    inner_loops: int = 0
+    filtered_vectors: int = 0
+    matvecs: int = 0
+    lanczos_matvecs: int = 0
+    residual_check_matvecs: int = 0
+    locked_per_loop: list = field(default_factory=list)
+    final_residuals: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    wall_time: float = 0.0
+    converged: bool = False
+    operator_norm_estimate: float = 0.0
+    filter_time: float = 0.0
+    tail_vectors: np.ndarray | None = None
+    lambda_blk_plus_1: float = float("nan")
+
+
+def chfsi_solve(h, nev, blk=None, deg=25, tol=1e-10, lanczos_steps=None, max_repeats=50,
+                guess=None, rng=None):
+    """ChFSI with locking; restates chfsi.py:274-384.
+
+    ``guess`` is ``(vectors n x blk, lambda1, lambda_blk_plus_1)`` or None.
+    Returns ``(values, vectors, report)``. Additive extension:
+    ``report.tail_vectors`` is the full final block ``[locked | unlocked
+    panel]`` (exactly ``blk`` columns at the break) and
+    ``report.lambda_blk_plus_1`` the largest final Ritz value, which is what
+    the chained sequence driver hands to the next problem.
+    """
+    t0 = time.perf_counter()
+    rng = rng if isinstance(rng, np.random.Generator) else np.random.default_rng(rng)
+    n = h.shape[0]
+    width, deg, tol, k, max_rep = resolve(n, nev, blk, deg, tol, lanczos_steps, max_repeats)
+    rep = OracleReport()
+    if guess is not None:
+        vecs = np.asarray(guess[0], dtype=np.complex128)
+        if vecs.shape != (n, width):
+            raise ValueError("guess block has the wrong shape")
+        ritz, last, steps = lanczos(h, min(10, n), rng)
+        win = safe_window(guess[1], guess[2], float(ritz[-1] + last))
+        panel = vecs.copy()
+    else:
+        ritz, last, steps = lanczos(h, k, rng)
+        upper = float(ritz[-1] + last)
+        lower = float(ritz[width]) if ritz.size > width else float(ritz[-1] - 0.10 * (ritz[-1] - ritz[0]))
+        win = safe_window(float(ritz[0]), lower, upper)
+        panel = qr_orthonormalize(random_block(rng, n, width))
+    rep.lanczos_matvecs = steps
+    rep.matvecs = steps
+    rep.operator_norm_estimate = float(max(abs(ritz[0]), abs(ritz[-1])) + last)
+
+    vals, res_l = [], []
+    locked = np.zeros((n, 0), dtype=np.complex128)
+    ritz_vals = np.zeros(0)
+    for _ in range(max_rep):
+        rep.inner_loops += 1
+        w = panel.shape[1]
+        tf = time.perf_counter()
+        panel = chebyshev_filter(h, panel, deg, *win)
+        rep.filter_time += time.perf_counter() - tf
+        rep.filtered_vectors += w
+        rep.matvecs += deg * w
+        panel = orthonormalize_panel(panel, locked, rng)
+        hp = h @ panel
+        rep.residual_check_matvecs += w
+        rep.matvecs += w
+        g = panel.conj().T @ hp
+        g = (g + g.conj().T) / 2
+        ritz_vals, rot = hermitian_eig(g)
+        panel = panel @ rot
+        hp = hp @ rot
+        res = np.linalg.norm(hp - panel * ritz_vals, axis=0)
+        nl = 0
+        while nl < w and len(vals) + nl < nev and res[nl] < tol:
+            nl += 1
+        if nl:
+            vals.extend(float(x) for x in ritz_vals[:nl])
+            res_l.extend(float(x) for x in res[:nl])
+            locked = np.hstack([locked, panel[:, :nl]])
+        rep.locked_per_loop.append(nl)
+        if len(vals) >= nev:
+            rep.converged = True
+            rep.tail_vectors = np.hstack([locked, panel[:, nl:]])
+            break
+        panel = panel[:, nl:]
+        win = safe_window(float(ritz_vals[nl]), float(ritz_vals[-1]), win[1])
+    else:
+        rep.tail_vectors = np.hstack([locked, panel])
+    rep.lambda_blk_plus_1 = float(ritz_vals[-1]) if ritz_vals.size else float("nan")
+    order = np.argsort(vals, kind="stable")
+    rep.final_residuals = np.asarray(res_l)[order]
+    rep.wall_time = time.perf_counter() - t0
+    return np.asarray(vals)[order], locked[:, order], rep
+
+
+# -------------------------------------------------------------- reduction ---
+
+def to_standard(a, b):
+    """H = L^-1 A L^-H with B = L L^H; restates reduction.py:102-113."""
+    l = np.linalg.cholesky(np.asarray(b, dtype=np.complex128))
+    z = scipy.linalg.solve_triangular(l, np.asarray(a, dtype=np.complex128), lower=True,
+                                      check_finite=False)
+    hm = scipy.linalg.solve_triangular(l, z.conj().T, lower=True, check_finite=False)
+    return (hm + hm.conj().T) / 2, l
+
+
+def back_transform(l, y):
+    """x = L^-H y; restates reduction.py:122-134."""
+    return scipy.linalg.solve_triangular(l, y, lower=True, trans="C", check_finite=False)
+
+
+# --------------------------------------------------------- sequence driver ---
+
+def run_sequence(pencils, nev, nex, deg, tol=1e-10, seed=0, mode="chained",
+                 max_repeats=50):
+    """Solve a correlated sequence; restates harness.py:188-289 (parity mode).
+
+    ``pencils`` yields ``(label, A, B)``. ``mode="harness"`` warm-starts from
+    the dense eigendecomposition of the previous problem (harness.py:235-251,
+    rng seeds ``(seed, label, 1)``); ``mode="chained"`` warm-starts from the
+    previous ChFSI tail block. Problem 1 is a cold start with rng
+    ``(seed, 1, 0)``. Returns a list of per-problem dicts.
+    """
+    blk = nev + nex
+    out = []
+    prev = None
+    for label, a, b in pencils:
+        t0 = time.perf_counter()
+        h, l = to_standard(a, b)
+        if prev is None:
+            guess, rng = None, np.random.default_rng((seed, label, 0))
+        else:
+            guess, rng = prev, np.random.default_rng((seed, label, 1))
+        vals, vecs, rep = chfsi_solve(h, nev, blk, deg, tol, guess=guess, rng=rng,
+                                      max_repeats=max_repeats)
+        x = back_transform(l, vecs)
+        wall = time.perf_counter() - t0
+        if mode == "harness":
+            dv, dvec = hermitian_eig(h)
+            prev = (dvec[:, :blk], float(dv[0]), float(dv[blk]))
+        else:
+            prev = (rep.tail_vectors, float(vals[0]) if vals.size else float("nan"),
+                    rep.lambda_blk_plus_1)
+        out.append(dict(label=label, values=vals, vectors=vecs, x=x, report=rep, wall=wall,
+                        filter_flops=8.0 * h.shape[0] ** 2 * deg * rep.filtered_vectors))
+    return out

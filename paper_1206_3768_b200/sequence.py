@@ -1,0 +1,129 @@
+"""Synthetic correlated pencil sequences (the BASELINE.json generator).
+
+The reference's own generator (`spectral_chain/sequence.py:137-178`) draws a
+Gaussian Hermitian A and a log-spaced SPD B; BASELINE.json prescribes a
+different recipe, restated here with a pinned draw order
+so the CPU oracle and the device path see the SAME bytes:
+
+* ``rng = numpy.random.default_rng(seed)``;
+* complex standard Gaussian ``z = (N(0,1) + i N(0,1)) / sqrt(2)`` — the real
+  block is drawn first, then the imaginary block;
+* draw 1: ``C`` (n x n);   ``B1 = I + C C^H / (4n)``, re-symmetrized;
+* draw 2: ``G`` (n x n);   ``Q, R = qr(G)``;  ``U = Q diag(conj(r_ii / |r_ii|))``
+  (the phase fix of the reference test fixture `pkg/tests/conftest.py:19-22`);
+* ``d_i = -1 + 11 (i/n)^1.5`` for ``i = 0..n-1``;  ``A1 = U diag(d) U^H``,
+  re-symmetrized;
+* for ``l = 1..N-1``: draw ``E_l`` then ``F_l``, each ``(G + G^H)/2`` of a fresh
+  complex Gaussian rescaled to ``||.||_F = sqrt(n)``;
+  ``eps_l = 1e-2 * 0.5**l``;  ``A_{l+1} = A_l + eps_l E_l``;
+  ``B_{l+1} = B_l + (eps_l / 10) F_l``.
+
+Problems are yielded lazily (``iter_baseline_sequence``) so that n=20000
+sequences never hold more than one (A, B) pair plus the running sums.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = [
+    "BaselineConfig",
+    "BASELINE_CONFIGS",
+    "complex_gaussian",
+    "hermitian_unit_frobenius",
+    "iter_baseline_sequence",
+    "generate_baseline_sequence",
+]
+
+
+@dataclass(frozen=True)
+class BaselineConfig:
+    """One row of BASELINE.json ``configs`` (SURVEY.md §8 shape table)."""
+
+    name: str
+    n: int
+    length: int
+    nev: int
+    nex: int
+    deg: int
+    tol: float = 1e-10
+    adaptive_degree: bool = False
+
+    @property
+    def blk(self) -> int:
+        return self.nev + self.nex
+
+
+BASELINE_CONFIGS = {
+    "C1": BaselineConfig("C1", 512, 6, 32, 16, 12),
+    "C2": BaselineConfig("C2", 2048, 10, 128, 32, 16),
+    "C3": BaselineConfig("C3", 5000, 12, 500, 100, 20),
+    "C4": BaselineConfig("C4", 12000, 8, 1200, 200, 20),
+    "C5": BaselineConfig("C5", 20000, 6, 3000, 400, 36, adaptive_degree=True),
+}
+
+
+def complex_gaussian(rng, n, m):
+    """i.i.d. complex standard Gaussian block (unit variance per entry)."""
+    re = rng.standard_normal((n, m))
+    im = rng.standard_normal((n, m))
+    z = np.empty((n, m), dtype=np.complex128)
+    z.real = re
+    z.imag = im
+    z *= 1.0 / np.sqrt(2.0)
+    return z
+
+
+def _symmetrize(m):
+    return (m + m.conj().T) * 0.5
+
+
+def hermitian_unit_frobenius(rng, n):
+    """Hermitian Gaussian perturbation with ``||E||_F = sqrt(n)``."""
+    g = complex_gaussian(rng, n, n)
+    e = _symmetrize(g)
+    e *= np.sqrt(n) / np.linalg.norm(e)
+    return e
+
+
+def iter_baseline_sequence(n, length, seed=0):
+    """Yield ``(label, A_l, B_l)`` for l = 1..length (complex128, C-ordered).
+
+    The yielded arrays are fresh copies; the generator keeps its own running
+    ``A``/``B``.
+    """
+    if n < 2 or length < 1:
+        raise ValueError("need n >= 2 and length >= 1")
+    rng = np.random.default_rng(seed)
+    c = complex_gaussian(rng, n, n)
+    b = c @ c.conj().T
+    b *= 1.0 / (4.0 * n)
+    b[np.diag_indices(n)] += 1.0
+    b = _symmetrize(b)
+    del c
+    g = complex_gaussian(rng, n, n)
+    q, r = np.linalg.qr(g)
+    del g
+    rd = np.diagonal(r)
+    u = q * (rd / np.abs(rd)).conj()
+    del q, r
+    d = -1.0 + 11.0 * (np.arange(n, dtype=np.float64) / n) ** 1.5
+    a = (u * d) @ u.conj().T
+    a = _symmetrize(a)
+    del u
+    yield 1, a.copy(), b.copy()
+    for ell in range(1, length):
+        eps = 1e-2 * 0.5**ell
+        e = hermitian_unit_frobenius(rng, n)
+        f = hermitian_unit_frobenius(rng, n)
+        a += eps * e
+        b += (eps / 10.0) * f
+        del e, f
+        yield ell + 1, a.copy(), b.copy()
+
+
+def generate_baseline_sequence(n, length, seed=0):
+    """Materialize the whole sequence as a list of ``(label, A, B)``."""
+    return list(iter_baseline_sequence(n, length, seed))
