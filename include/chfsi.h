@@ -1,0 +1,152 @@
+/*
+ * libchfsi — C-ABI of the B200-native ChFSI hot path (sm_100a).
+ *
+ * The reference (`spectral_chain`, pure Python + numpy/scipy) has no FFI:
+ * its boundary is the Python functions re-exported by
+ * `spectral_chain/__init__.py:15-80`. Each entry point below replaces the
+ * numpy/LAPACK work behind one of those functions; the reference interface
+ * it replaces is cited per function (paths relative to
+ * /root/reference/pkg/src/spectral_chain/). INTEGRATION.md shows the ctypes
+ * binding the reference would add.
+ *
+ * Conventions
+ *  - Matrices are complex128 (interleaved re/im, 16 bytes), passed as plain
+ *    `void*` DEVICE pointers owned by the caller, column-major with a
+ *    leading dimension `ld*`, except the operator H of K1/K2 which is read
+ *    row-major (`H[m*ldh + k]`); `conj_h = 1` reads conj(H), so a
+ *    column-major Hermitian H can be passed unchanged.
+ *  - Work is enqueued on the context's stream (chfsi_ctx_set_stream) and is
+ *    stream-ordered; functions returning host values synchronise that stream.
+ *  - Every reduction has a fixed order: results are bitwise reproducible
+ *    run to run on the same device.
+ *  - Return value: CHFSI_OK (0) or a negative CHFSI_E* code;
+ *    chfsi_last_error() gives a thread-local message.
+ */
+#ifndef CHFSI_H_
+#define CHFSI_H_
+
+#if defined(__GNUC__)
+#define CHFSI_API __attribute__((visibility("default")))
+#else
+#define CHFSI_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CHFSI_OK 0
+#define CHFSI_EINVAL -1     /* bad argument -> ValueError                        */
+#define CHFSI_ECUDA -2      /* CUDA runtime failure                              */
+#define CHFSI_ECUBLAS -3    /* cuBLAS failure                                    */
+#define CHFSI_ECUSOLVER -4  /* cuSOLVER failure                                  */
+#define CHFSI_ENOTPD -5     /* Cholesky pivot <= 0 -> NotPositiveDefiniteError    */
+#define CHFSI_ERANK -6      /* rank-deficient panel -> RankDeficientError         */
+#define CHFSI_EEIG -7       /* dense eigensolver failed -> EigenSolverError       */
+#define CHFSI_ENCCL -8      /* NCCL failure                                      */
+
+typedef struct chfsi_ctx chfsi_ctx;
+
+CHFSI_API int chfsi_version(void);
+CHFSI_API const char* chfsi_last_error(void);
+
+/* One context per device and host thread of use; owns cuBLAS/cuSOLVER
+ * handles and a growable device workspace. */
+CHFSI_API int chfsi_ctx_create(int device, chfsi_ctx** out);
+CHFSI_API int chfsi_ctx_destroy(chfsi_ctx* ctx);
+CHFSI_API int chfsi_ctx_set_stream(chfsi_ctx* ctx, void* cuda_stream);
+/* Force the K1 tiling (bm=64; bn 32|64; cluster K-split 1|2|4|8) for tests
+ * and tuning; bm = 0 restores the automatic choice. */
+CHFSI_API int chfsi_ctx_set_tiling(chfsi_ctx* ctx, int bm, int bn, int split);
+
+/* ---------------------------------------------------------------- K1 ---
+ * One fused Chebyshev step (chfsi.py:203 / chfsi.py:206):
+ *   Ynext = alpha*(op(H) Ycur - c Ycur) - beta Yprev
+ * Yprev may alias Ynext (in-place ping-pong) or be NULL when beta == 0;
+ * Ycur must not alias Ynext. alpha=1, c=0, beta=0 is the plain product H*Y
+ * (the Rayleigh-Ritz H*panel of chfsi.py:342). */
+CHFSI_API int chfsi_cheb_step_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, int conj_h,
+                      const void* ycur, long long ldc, const void* yprev, long long ldp,
+                      void* ynext, long long ldn, double alpha, double c, double beta);
+
+/* Host-only: the filter's shift c and per-step (alpha_j, beta_j) exactly as
+ * chebyshev_filter computes them (chfsi.py:198-207). alphas/betas hold deg. */
+CHFSI_API int chfsi_filter_coeffs(int deg, double a, double b, double scale_ref, double* c,
+                        double* alphas, double* betas);
+
+/* Replaces chebyshev_filter(h, y, deg, window) (chfsi.py:179-208).
+ * y0 is read only; the result lands in buf_a (deg odd) or buf_b (deg even)
+ * and *result receives that pointer. y0 may equal buf_b (in place). */
+CHFSI_API int chfsi_filter_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, int conj_h,
+                   const void* y0, long long ldy0, void* buf_a, void* buf_b, long long ldb,
+                   int deg, double a, double b, double scale_ref, void** result);
+
+/* Introspection of the K1 tile choice for an (n, w) step. */
+CHFSI_API int chfsi_step_tiling(int n, int w, int* bm, int* bn, int* split);
+
+/* ---------------------------------------------------------------- K2 ---
+ * k-step Lanczos with full reorthogonalization (chfsi.py:125-162): q0 is
+ * the raw start vector (normalised on device), basis an n x k column-major
+ * workspace (ld n). Writes alphas[0..steps), betas[0..steps-1), the final
+ * residual norm and the step count to HOST memory. */
+CHFSI_API int chfsi_lanczos_z(chfsi_ctx* ctx, int n, int k, const void* H, long long ldh, int conj_h,
+                    const void* q0, void* basis, double* alphas, double* betas,
+                    double* beta_last, int* steps);
+
+/* ------------------------------------------------------- K3 / K4 (RR) ---
+ * Plain ZGEMM C = alpha op(A) op(B) + beta C (cuBLAS; trans 'N','T','C'). */
+CHFSI_API int chfsi_gemm_z(chfsi_ctx* ctx, char transa, char transb, int m, int n, int k, double alpha_re,
+                 double alpha_im, const void* A, long long lda, const void* B, long long ldb,
+                 double beta_re, double beta_im, void* C, long long ldc);
+
+/* Two classical Gram-Schmidt passes of work against locked
+ * (chfsi.py:251-253): work -= locked (locked^H work), twice. coef is an
+ * nlocked x w scratch block (ld nlocked). */
+CHFSI_API int chfsi_cgs_project_z(chfsi_ctx* ctx, int n, int nlocked, int w, const void* locked,
+                        long long ldl, void* work, long long ldw, void* coef);
+
+/* Householder QR orthonormalization with positive-real R diagonal
+ * (linalg.py:152-178). Q overwrites Y. If any |R_ii| < 1e-13 ||Y||_F the
+ * call returns CHFSI_ERANK, Y is left unmodified, and the offending column
+ * indices (ascending) are written to dead[0..*ndead) (dead holds n ints). */
+CHFSI_API int chfsi_qr_orthonormalize_z(chfsi_ctx* ctx, int m, int n, void* Y, long long ldy, int* dead,
+                              int* ndead);
+
+/* Dense Hermitian eigensolver (linalg.py:181-206): ascending values to the
+ * DEVICE array w, eigenvectors overwrite A. */
+CHFSI_API int chfsi_heevd_z(chfsi_ctx* ctx, int n, void* A, long long lda, double* w);
+
+/* res[j] = || HP[:,j] - lambda[j] P[:,j] ||_2 (chfsi.py:350); device arrays.
+ * P and lambda may be NULL (plain column norms). */
+CHFSI_API int chfsi_colnorm_residual_z(chfsi_ctx* ctx, int n, int w, const void* HP, long long ldhp,
+                             const void* P, long long ldp, const double* lambda, double* res);
+
+/* ------------------------------------------------------------------ K5 ---
+ * A <- (A + A^H)/2 in place (reduction.py:112, chfsi.py:346). */
+CHFSI_API int chfsi_symmetrize_z(chfsi_ctx* ctx, int n, void* A, long long lda);
+/* Hermitian validation (linalg.py:61-85): max|A - A^H| and max|A| to host. */
+CHFSI_API int chfsi_herm_defect_z(chfsi_ctx* ctx, int n, const void* A, long long lda, double* defect,
+                        double* maxabs);
+/* A <- conj(A) for an m x n block (row-major <-> column-major of a Hermitian). */
+CHFSI_API int chfsi_conj_z(chfsi_ctx* ctx, int m, int n, void* A, long long lda);
+/* Lower Cholesky in place, strict upper zeroed (linalg.py:116-129).
+ * Returns CHFSI_ENOTPD with *info = failing pivot (1-based). */
+CHFSI_API int chfsi_potrf_z(chfsi_ctx* ctx, int n, void* A, long long lda, int* info);
+/* B <- op(L)^-1 B (side 'L') or B op(L)^-1 (side 'R'), L lower non-unit
+ * (linalg.py:132-149). trans 'N' or 'C'. */
+CHFSI_API int chfsi_trsm_z(chfsi_ctx* ctx, char side, char trans, int m, int n, const void* L,
+                 long long ldl, void* B, long long ldb);
+/* to_standard (reduction.py:102-113): on entry A and B hold the pencil
+ * (column-major, or row-major with rowmajor_in = 1); on exit B holds L
+ * (lower, column-major) and A holds H = L^-1 A L^-H, re-symmetrised. */
+CHFSI_API int chfsi_to_standard_z(chfsi_ctx* ctx, int n, void* A, long long lda, void* B, long long ldb,
+                        int rowmajor_in, int* info);
+/* back_transform (reduction.py:122-134): Y <- L^-H Y in place. */
+CHFSI_API int chfsi_back_transform_z(chfsi_ctx* ctx, int n, int nev, const void* L, long long ldl, void* Y,
+                           long long ldy);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CHFSI_H_ */

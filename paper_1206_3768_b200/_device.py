@@ -1,0 +1,123 @@
+"""Device-memory plumbing: complex128 blocks in HBM as torch tensors.
+
+Layout rules of the device path:
+* n x w blocks (panels, locked vectors, H*panel, eigenvectors) are
+  column-major "F-blocks": a torch tensor of shape (n, w) with strides
+  (1, ld), ld >= n — each column contiguous, so column slices and locking
+  are pointer offsets and cuBLAS/cuSOLVER use them without transposes.
+* The operator H of K1/K2 may be row-major (as numpy hands it over) or
+  column-major (as the device reduction produces it); Hermitian symmetry
+  makes the second the conjugate of the first, so the kernels just flip a
+  `conj` flag instead of transposing 16 n^2 bytes.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from ._lib import BackendUnavailable
+
+C128 = torch.complex128
+
+
+def device():
+    if not torch.cuda.is_available():
+        raise BackendUnavailable("no CUDA device visible: the ChFSI path runs only on the GPU")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def fblock(n, w, dev=None):
+    """Uninitialised column-major n x w complex128 block on the device."""
+    return torch.empty((w, n), dtype=C128, device=dev or device()).t()
+
+
+def is_fblock(t):
+    return (
+        isinstance(t, torch.Tensor)
+        and t.is_cuda
+        and t.dtype == C128
+        and t.dim() == 2
+        and (t.stride(0) == 1 or t.shape[0] <= 1)
+        and (t.shape[1] <= 1 or t.stride(1) >= t.shape[0])
+    )
+
+
+def ld_of(t):
+    """Leading dimension of an F-block (>= rows, as BLAS requires)."""
+    return max(int(t.stride(1)) if t.shape[1] > 1 else int(t.shape[0]), int(t.shape[0]), 1)
+
+
+def _as_tensor(x):
+    if isinstance(x, torch.Tensor):
+        return x
+    a = np.asarray(x)
+    if a.ndim == 1:
+        a = a[:, None]
+    if a.dtype != np.complex128:
+        a = a.astype(np.complex128)
+    return torch.from_numpy(a)
+
+
+def to_fblock(x, copy=False):
+    """Device F-block view of ``x`` (numpy or torch, any strides).
+
+    Zero-copy when ``x`` already is a device complex128 F-block and
+    ``copy`` is False; otherwise one H2D/D2D copy into a fresh block.
+    """
+    if not copy and is_fblock(x):
+        return x
+    t = _as_tensor(x)
+    if t.dim() == 1:
+        t = t[:, None]
+    if t.dim() != 2:
+        raise ValueError(f"expected a 2-D block, got shape {tuple(t.shape)}")
+    out = fblock(t.shape[0], t.shape[1])
+    if t.dtype != C128:
+        t = t.to(C128)
+    out.copy_(t, non_blocking=True)
+    return out
+
+
+def to_device_matrix(x):
+    """Device complex128 square matrix, keeping row-major input row-major."""
+    t = _as_tensor(x)
+    if t.dim() != 2:
+        raise ValueError(f"expected a matrix, got shape {tuple(t.shape)}")
+    if t.dtype != C128:
+        t = t.to(C128)
+    dev = device()
+    if t.device != dev:
+        t = t.to(dev, non_blocking=True)
+    return t
+
+
+class Operator:
+    """The Hermitian operator H as the kernels read it (pointer, ld, conj)."""
+
+    __slots__ = ("tensor", "n", "ld", "conj")
+
+    def __init__(self, h):
+        t = to_device_matrix(h)
+        n = t.shape[0]
+        if t.shape != (n, n):
+            raise ValueError(f"operator must be square, got {tuple(t.shape)}")
+        if n > 1 and t.stride(1) == 1 and t.stride(0) >= n:
+            conj, ld = 0, t.stride(0)          # row-major H
+        elif n > 1 and t.stride(0) == 1 and t.stride(1) >= n:
+            conj, ld = 1, t.stride(1)          # column-major H == conj(H) row-major
+        else:
+            t = t.contiguous()
+            conj, ld = 0, max(n, 1)
+        self.tensor, self.n, self.ld, self.conj = t, n, ld, conj
+
+    @classmethod
+    def wrap(cls, h):
+        return h if isinstance(h, Operator) else cls(h)
+
+
+def to_host(x):
+    """numpy copy of a device tensor (test/report helper)."""
+    if isinstance(x, torch.Tensor):
+        return x.detach().cpu().numpy()
+    return np.asarray(x)

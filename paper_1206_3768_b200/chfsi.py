@@ -1,0 +1,471 @@
+"""Chebyshev Filtered Subspace Iteration with locking — device path.
+
+Drop-in for `spectral_chain.chfsi` (reference `chfsi.py:1-384`): same
+names, signatures, counters and exceptions. Every operation on n-sized data
+runs on the GPU through libchfsi:
+
+* the filter (K1, `chfsi_filter_z`: one fused DMMA kernel per recurrence
+  step, shift/scale/three-term update in the epilogue, ping-pong in place);
+* the Lanczos bound (K2, `chfsi_lanczos_z`: HBM-bound GEMV + deterministic
+  reorthogonalization, no host sync per step);
+* CGS against the locked block and the Householder QR (K3);
+* Rayleigh-Ritz (K4: H*panel through K1, cuBLAS Gram/rotations, cuSOLVER
+  zheevd on the blk x blk projection, fused residual column norms).
+
+Only O(blk) scalars cross to the host: the Ritz values and residual norms
+that drive locking (chfsi.py:352-373), the k x k Lanczos tridiagonal, and
+the random draws, which are made on the host with the caller's numpy
+Generator in exactly the reference order so iteration counts match.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.linalg
+import torch
+
+from ._device import C128, Operator, fblock, ld_of, to_fblock
+from ._lib import check, ctx, dptr, lib
+from .linalg import qr_orthonormalize_inplace
+from .linalg_errors import RankDeficientError
+from .reduction import EigenSolution
+
+__all__ = [
+    "ChfsiConfig",
+    "FilterWindow",
+    "ChfsiGuess",
+    "SolveReport",
+    "lanczos_upper_bound",
+    "chebyshev_filter",
+    "chebyshev_response",
+    "rayleigh_ritz",
+    "chfsi_solve",
+    "filter_flops",
+]
+
+
+@dataclass
+class ChfsiConfig:
+    """Solver parameters (chfsi.py:36-69).
+
+    ``blk`` defaults to ``nev + 40``; ``nex`` (BASELINE.json's name for the
+    extra vectors) is accepted as an alias: ``blk = nev + nex``.
+    """
+
+    nev: int
+    blk: int | None = None
+    deg: int = 25
+    tol: float = 1e-10
+    lanczos_steps: int | None = None
+    max_repeats: int = 50
+    nex: int | None = None
+
+    def __post_init__(self):
+        if self.nex is not None:
+            if self.blk is not None and self.blk != self.nev + self.nex:
+                raise ValueError("give either blk or nex, not conflicting values")
+            self.blk = self.nev + self.nex
+
+    def resolve(self, n):
+        """Fill in size-dependent defaults and validate against ``n``."""
+        blk = self.blk if self.blk is not None else self.nev + 40
+        blk = min(blk, n)
+        if not (1 <= self.nev <= blk <= n):
+            raise ValueError(f"need 1 <= nev <= blk <= n, got nev={self.nev}, blk={blk}, n={n}")
+        if self.deg < 1:
+            raise ValueError("polynomial degree must be >= 1")
+        if self.tol <= 0:
+            raise ValueError("tolerance must be positive")
+        if self.lanczos_steps is not None:
+            k = self.lanczos_steps
+        else:
+            k = min(3 * blk, max(10, n // 10))
+            k = max(k, min(10, 3 * blk))
+        k = max(2, min(k, n))
+        return blk, self.deg, self.tol, k, self.max_repeats
+
+
+@dataclass(frozen=True)
+class FilterWindow:
+    """Damped interval ``[a, b]`` and the growth anchor (chfsi.py:72-88)."""
+
+    a: float
+    b: float
+    scale_ref: float
+
+    def __post_init__(self):
+        if not self.a < self.b:
+            raise ValueError(f"need a < b, got a={self.a}, b={self.b}")
+        if not self.scale_ref < self.a:
+            raise ValueError(f"need scale_ref < a, got scale_ref={self.scale_ref}, a={self.a}")
+
+
+@dataclass(frozen=True)
+class ChfsiGuess:
+    """Warm start (chfsi.py:91-98): ``blk`` vectors (numpy or device
+    tensor) plus the previous lambda_1 and lambda_{blk+1}."""
+
+    vectors: object
+    lambda1: float
+    lambda_blk_plus_1: float
+
+
+@dataclass
+class SolveReport:
+    """Work counters of one solve (chfsi.py:101-122), same algebra:
+    ``matvecs == deg*filtered_vectors + lanczos_matvecs + residual_check_matvecs``.
+
+    Additive fields: device phase times (CUDA events, seconds), the filter
+    FLOP count (8 n^2 per column per degree), and the chained-mode tail
+    (the full final ``blk`` block and the largest final Ritz value, the
+    lambda_{blk+1} proxy of SURVEY G2).
+    """
+
+    inner_loops: int = 0
+    filtered_vectors: int = 0
+    matvecs: int = 0
+    lanczos_matvecs: int = 0
+    residual_check_matvecs: int = 0
+    locked_per_loop: list = field(default_factory=list)
+    final_residuals: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    wall_time: float = 0.0
+    converged: bool = False
+    operator_norm_estimate: float = 0.0
+    ritz_history: list = field(default_factory=list)
+    t_lanczos: float = 0.0
+    t_filter: float = 0.0
+    t_ortho: float = 0.0
+    t_rr: float = 0.0
+    filter_flops: float = 0.0
+    filter_launches: int = 0
+    tail_vectors: object = None
+    lambda_blk_plus_1: float = float("nan")
+
+
+def filter_flops(n, deg, columns):
+    """Algorithmic FLOPs of the filter: 8 n^2 per column per degree."""
+    return 8.0 * float(n) * float(n) * float(deg) * float(columns)
+
+
+def as_rng(seed_or_rng):
+    """Coerce None / int / tuple / Generator to a Generator (_util.py:8-12)."""
+    if isinstance(seed_or_rng, np.random.Generator):
+        return seed_or_rng
+    return np.random.default_rng(seed_or_rng)
+
+
+def random_block(rng, n, cols):
+    """Complex Gaussian block drawn on the host in the reference order
+    (_util.py:15-18), uploaded as a device F-block."""
+    re = rng.standard_normal((n, cols))
+    z = re + 1j * rng.standard_normal((n, cols))
+    return to_fblock(z)
+
+
+class _PhaseTimer:
+    """Accumulates device time of a phase with CUDA events on the launch stream."""
+
+    def __init__(self):
+        self.pairs = []
+
+    def start(self):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.pairs.append([e, None])
+
+    def stop(self):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.pairs[-1][1] = e
+
+    def seconds(self):
+        return sum(a.elapsed_time(b) for a, b in self.pairs if b is not None) / 1e3
+
+
+# --------------------------------------------------------------- Lanczos ---
+
+def _lanczos_estimates(op, k, rng):
+    """k-step Lanczos with full reorthogonalization on the device
+    (chfsi.py:125-162). Returns (ritz, beta_last, steps)."""
+    n = op.n
+    k = min(k, n)
+    q0 = rng.standard_normal(n) + 1j * rng.standard_normal(n)  # chfsi.py:137 draw order
+    q0d = torch.from_numpy(q0).to(op.tensor.device)
+    basis = fblock(n, k)
+    alphas = np.zeros(k)
+    betas = np.zeros(k)
+    beta_last = ctypes.c_double()
+    steps = ctypes.c_int()
+    pd = ctypes.POINTER(ctypes.c_double)
+    check(lib().chfsi_lanczos_z(ctx(), n, k, dptr(op.tensor), op.ld, op.conj, dptr(q0d),
+                                dptr(basis), alphas.ctypes.data_as(pd), betas.ctypes.data_as(pd),
+                                ctypes.byref(beta_last), ctypes.byref(steps)), "lanczos")
+    s = steps.value
+    if s == 1:
+        ritz = alphas[:1].copy()
+    else:
+        ritz = scipy.linalg.eigvalsh_tridiagonal(alphas[:s], betas[: s - 1])
+    return ritz, beta_last.value, s
+
+
+def lanczos_upper_bound(h, k, rng=None):
+    """Largest Ritz value plus the final residual norm (chfsi.py:165-176)."""
+    if k < 2:
+        raise ValueError("need at least 2 Lanczos steps")
+    ritz, beta_last, _ = _lanczos_estimates(Operator.wrap(h), k, as_rng(rng))
+    return float(ritz[-1] + beta_last)
+
+
+# ---------------------------------------------------------------- filter ---
+
+def _filter_into(op, y, buf_a, buf_b, deg, window):
+    """Run K1 deg times; y is read (may be buf_b for in-place). Returns the
+    buffer holding the result."""
+    res = ctypes.c_void_p()
+    n, w = y.shape
+    check(lib().chfsi_filter_z(ctx(), n, w, dptr(op.tensor), op.ld, op.conj, dptr(y), ld_of(y),
+                               dptr(buf_a), dptr(buf_b), ld_of(buf_a), deg, float(window.a),
+                               float(window.b), float(window.scale_ref), ctypes.byref(res)),
+          "chebyshev_filter")
+    return buf_a if res.value == buf_a.data_ptr() else buf_b
+
+
+def chebyshev_filter(h, y, deg, window):
+    """Degree-``deg`` scaled Chebyshev filter of the block ``y``
+    (chfsi.py:179-208) on the device; returns a new column-major device
+    block, ``y`` is untouched."""
+    if deg < 1:
+        raise ValueError("polynomial degree must be >= 1")
+    op = Operator.wrap(h)
+    ym = to_fblock(y)
+    if ym.shape[0] != op.n:
+        raise ValueError(f"operator/block shapes do not conform: {(op.n, op.n)} vs {tuple(ym.shape)}")
+    n, w = ym.shape
+    a, b = fblock(n, w), fblock(n, w)
+    return _filter_into(op, ym, a, b, deg, window)
+
+
+def chebyshev_response(lam, deg, window):
+    """Scalar filter response s_deg(lam) (chfsi.py:211-225) — host numpy:
+    it is the filter's own oracle, evaluated on eigenvalues only."""
+    lam = np.asarray(lam, dtype=float)
+    e = (window.b - window.a) / 2
+    c = (window.b + window.a) / 2
+    sigma = e / (window.scale_ref - c)
+    tau = 2.0 / sigma
+    s_prev = np.ones_like(lam)
+    s_cur = (sigma / e) * (lam - c)
+    for _ in range(deg - 1):
+        sigma_new = 1.0 / (tau - sigma)
+        s_next = (2 * sigma_new / e) * (lam - c) * s_cur - (sigma * sigma_new) * s_prev
+        s_prev, s_cur, sigma = s_cur, s_next, sigma_new
+    return s_cur
+
+
+# ---------------------------------------------------------- Rayleigh-Ritz ---
+
+def _apply_h(op, y, out):
+    check(lib().chfsi_cheb_step_z(ctx(), op.n, y.shape[1], dptr(op.tensor), op.ld, op.conj,
+                                  dptr(y), ld_of(y), None, 0, dptr(out), ld_of(out), 1.0, 0.0,
+                                  0.0), "H @ panel")
+
+
+def _gemm(ta, tb, m, n, k, a, b, c, alpha=1.0, beta=0.0):
+    check(lib().chfsi_gemm_z(ctx(), ta, tb, m, n, k, alpha, 0.0, dptr(a), ld_of(a), dptr(b),
+                             ld_of(b), beta, 0.0, dptr(c), ld_of(c)), "zgemm")
+
+
+def _rr_core(op, panel, hp, g, rot_p, rot_hp, ritz_d, res_d):
+    """HP = H P; G = P^H HP, symmetrized; zheevd; P W, HP W; residual norms
+    (chfsi.py:341-350). All device; returns nothing (results in buffers)."""
+    n, w = panel.shape
+    _apply_h(op, panel, hp)
+    _gemm(b"C", b"N", w, w, n, panel, hp, g)
+    check(lib().chfsi_symmetrize_z(ctx(), w, dptr(g), ld_of(g)), "symmetrize")
+    check(lib().chfsi_heevd_z(ctx(), w, dptr(g), ld_of(g), dptr(ritz_d)), "hermitian_eig")
+    _gemm(b"N", b"N", n, w, w, panel, g, rot_p)
+    _gemm(b"N", b"N", n, w, w, hp, g, rot_hp)
+    check(lib().chfsi_colnorm_residual_z(ctx(), n, w, dptr(rot_hp), ld_of(rot_hp), dptr(rot_p),
+                                         ld_of(rot_p), dptr(ritz_d), dptr(res_d)), "residuals")
+
+
+def rayleigh_ritz(h, y):
+    """Rayleigh-Ritz projection onto the orthonormal block ``y``
+    (chfsi.py:228-239): ascending Ritz values (host) and ``y @ w`` (device)."""
+    op = Operator.wrap(h)
+    ym = to_fblock(y)
+    n, w = ym.shape
+    hp, rot_p, rot_hp = fblock(n, w), fblock(n, w), fblock(n, w)
+    g = fblock(w, w)
+    ritz_d = torch.empty(w, dtype=torch.float64, device=ym.device)
+    res_d = torch.empty(w, dtype=torch.float64, device=ym.device)
+    _rr_core(op, ym, hp, g, rot_p, rot_hp, ritz_d, res_d)
+    return ritz_d.cpu().numpy(), rot_p
+
+
+# ------------------------------------------------------------ orthonormal ---
+
+def _orthonormalize_panel(work, locked, nlocked, coef, rng, retries=3):
+    """Two CGS passes against the locked block, then Householder QR with
+    rank repair (chfsi.py:242-261). ``work`` is overwritten by Q."""
+    n, w = work.shape
+    for attempt in range(retries + 1):
+        if nlocked:
+            check(lib().chfsi_cgs_project_z(ctx(), n, nlocked, w, dptr(locked), ld_of(locked),
+                                            dptr(work), ld_of(work), dptr(coef)), "cgs")
+        try:
+            return qr_orthonormalize_inplace(work)
+        except RankDeficientError as err:
+            if attempt == retries:
+                raise
+            idx = list(err.indices)
+            fresh = random_block(rng, n, len(idx))
+            for j, col in enumerate(idx):
+                work[:, col].copy_(fresh[:, j])
+    raise AssertionError("unreachable")
+
+
+def _safe_window(scale_ref, a, b):
+    """Clamp a refreshed window back to scale_ref < a < b (chfsi.py:264-271)."""
+    if not np.isfinite([scale_ref, a, b]).all() or not scale_ref < b:
+        return FilterWindow(a=scale_ref + 0.5, b=scale_ref + 1.0, scale_ref=scale_ref)
+    if not scale_ref < a < b:
+        a = scale_ref + 0.5 * (b - scale_ref)
+    return FilterWindow(a=a, b=b, scale_ref=scale_ref)
+
+
+# ----------------------------------------------------------------- solver ---
+
+def chfsi_solve(h, cfg, guess=None, rng=None, label=1):
+    """Compute the ``cfg.nev`` lowest eigenpairs of the Hermitian ``h``
+    (chfsi.py:274-384). ``h`` may be a numpy array (uploaded once) or a CUDA
+    tensor in either row- or column-major layout (used in place).
+
+    Returns ``(EigenSolution(form="standard"), SolveReport)``; the solution
+    vectors stay on the device.
+    """
+    t0 = time.perf_counter()
+    rng = as_rng(rng)
+    op = Operator.wrap(h)
+    n = op.n
+    blk, deg, tol, lancz_k, max_repeats = cfg.resolve(n)
+    report = SolveReport()
+    dev = op.tensor.device
+    t_lz, t_f, t_o, t_r = _PhaseTimer(), _PhaseTimer(), _PhaseTimer(), _PhaseTimer()
+
+    # HBM workspace: two panel buffers (filter ping-pong / rotation target),
+    # two H*panel buffers, the locked block, the projected matrix.
+    bufs = [fblock(n, blk), fblock(n, blk)]
+    hp_buf, hp_rot = fblock(n, blk), fblock(n, blk)
+    locked = fblock(n, max(cfg.nev, 1))
+    g_buf = fblock(blk, blk)
+    coef = fblock(max(cfg.nev, 1), blk)
+    ritz_d = torch.empty(blk, dtype=torch.float64, device=dev)
+    res_d = torch.empty(blk, dtype=torch.float64, device=dev)
+
+    t_lz.start()
+    if guess is not None:
+        gv = guess.vectors
+        shape = tuple(gv.shape)
+        if shape != (n, blk):
+            raise ValueError(f"guess block must be {n}x{blk}, got {shape}")
+        ritz, beta_last, steps = _lanczos_estimates(op, min(10, n), rng)
+        b_up = float(ritz[-1] + beta_last)
+        window = _safe_window(guess.lambda1, guess.lambda_blk_plus_1, b_up)
+        bufs[0].copy_(to_fblock(gv))
+    else:
+        ritz, beta_last, steps = _lanczos_estimates(op, lancz_k, rng)
+        b_up = float(ritz[-1] + beta_last)
+        if ritz.size > blk:
+            a = float(ritz[blk])
+        else:
+            a = float(ritz[-1] - 0.10 * (ritz[-1] - ritz[0]))
+        window = _safe_window(float(ritz[0]), a, b_up)
+        bufs[0].copy_(random_block(rng, n, blk))
+        qr_orthonormalize_inplace(bufs[0])
+    t_lz.stop()
+    report.lanczos_matvecs = steps
+    report.matvecs += steps
+    report.operator_norm_estimate = float(max(abs(ritz[0]), abs(ritz[-1])) + beta_last)
+
+    locked_vals: list[float] = []
+    locked_res: list[float] = []
+    nlocked = 0
+    pb, off, width = 0, 0, blk   # panel = bufs[pb][:, off:off+width]
+    ritz_vals = np.zeros(0)
+    rot_p = None
+    n_lock = 0
+
+    for _ in range(max_repeats):
+        report.inner_loops += 1
+        panel = bufs[pb][:, off:off + width]
+        other = bufs[1 - pb][:, :width]
+        t_f.start()
+        filtered = _filter_into(op, panel, other, panel, deg, window)
+        t_f.stop()
+        report.filter_launches += deg
+        report.filtered_vectors += width
+        report.matvecs += deg * width
+        report.filter_flops += filter_flops(n, deg, width)
+        q_in_other = filtered.data_ptr() == other.data_ptr()
+
+        t_o.start()
+        _orthonormalize_panel(filtered, locked, nlocked, coef, rng)
+        t_o.stop()
+
+        t_r.start()
+        rot_buf = bufs[pb] if q_in_other else bufs[1 - pb]
+        rot_p = rot_buf[:, :width]  # free: disjoint from Q by construction
+        _rr_core(op, filtered, hp_buf[:, :width], g_buf[:width, :width], rot_p,
+                 hp_rot[:, :width], ritz_d[:width], res_d[:width])
+        report.residual_check_matvecs += width
+        report.matvecs += width
+        host = torch.cat([ritz_d[:width], res_d[:width]]).cpu().numpy()
+        t_r.stop()
+        ritz_vals, res = host[:width], host[width:]
+
+        n_lock = 0
+        while n_lock < width and nlocked + n_lock < cfg.nev and res[n_lock] < tol:
+            n_lock += 1
+        if n_lock:
+            locked_vals.extend(float(v) for v in ritz_vals[:n_lock])
+            locked_res.extend(float(r) for r in res[:n_lock])
+            locked[:, nlocked:nlocked + n_lock].copy_(rot_p[:, :n_lock])
+            nlocked += n_lock
+        report.locked_per_loop.append(n_lock)
+
+        if len(locked_vals) >= cfg.nev:
+            report.converged = True
+            break
+
+        pb = 0 if rot_p.data_ptr() == bufs[0].data_ptr() else 1
+        off, width = n_lock, width - n_lock
+        window = _safe_window(float(ritz_vals[n_lock]), float(ritz_vals[-1]), window.b)
+
+    # chained-mode tail: [locked | unlocked remainder of the final panel]
+    if rot_p is not None:
+        tail = fblock(n, nlocked + rot_p.shape[1] - n_lock)
+        tail[:, :nlocked].copy_(locked[:, :nlocked])
+        tail[:, nlocked:].copy_(rot_p[:, n_lock:])
+        report.tail_vectors = tail
+        report.lambda_blk_plus_1 = float(ritz_vals[-1])
+
+    order = np.argsort(locked_vals, kind="stable")
+    vecs = locked[:, :nlocked]
+    if nlocked and not np.array_equal(order, np.arange(nlocked)):
+        idx = torch.from_numpy(order).to(dev)
+        vecs = vecs.index_select(1, idx)
+    sol = EigenSolution(values=np.asarray(locked_vals)[order], vectors=to_fblock(vecs, copy=True),
+                        form="standard", label=label)
+    report.final_residuals = np.asarray(locked_res)[order]
+    torch.cuda.current_stream().synchronize()
+    report.t_lanczos = t_lz.seconds()
+    report.t_filter = t_f.seconds()
+    report.t_ortho = t_o.seconds()
+    report.t_rr = t_r.seconds()
+    report.wall_time = time.perf_counter() - t0
+    return sol, report

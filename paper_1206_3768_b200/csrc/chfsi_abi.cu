@@ -1,0 +1,500 @@
+// C-ABI of libchfsi (declared in include/chfsi.h): context management,
+// cuBLAS/cuSOLVER calls for the small dense factorizations, and the
+// orchestration of the hand-written kernels (cheb_step.cu, aux_kernels.cu).
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/chfsi.h"
+#include "chfsi_internal.h"
+
+using chfsi::LanczosState;
+
+struct chfsi_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cublasHandle_t blas = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  void* ws = nullptr;  // cuSOLVER workspace (grown on demand)
+  size_t ws_bytes = 0;
+  void* scratch = nullptr;  // n-sized vectors (grown on demand)
+  size_t scratch_bytes = 0;
+  double* partial = nullptr;  // kRedBlocks doubles
+  double* scalars = nullptr;  // 16 doubles
+  int* dinfo = nullptr;
+  LanczosState* lstate = nullptr;
+  chfsi::StepTiling tiling{0, 0, 0};  // K1 tile override (bm == 0: automatic)
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CK_CUDA(expr)                                                                \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess)                                                           \
+      return fail(CHFSI_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));  \
+  } while (0)
+#define CK_BLAS(expr)                                                                        \
+  do {                                                                                       \
+    cublasStatus_t _s = (expr);                                                              \
+    if (_s != CUBLAS_STATUS_SUCCESS)                                                         \
+      return fail(CHFSI_ECUBLAS, std::string(#expr) + ": cublas status " + std::to_string(_s)); \
+  } while (0)
+#define CK_SOLVER(expr)                                                                     \
+  do {                                                                                      \
+    cusolverStatus_t _s = (expr);                                                           \
+    if (_s != CUSOLVER_STATUS_SUCCESS)                                                      \
+      return fail(CHFSI_ECUSOLVER,                                                          \
+                  std::string(#expr) + ": cusolver status " + std::to_string(_s));          \
+  } while (0)
+#define CK_ARG(cond, msg) \
+  do {                    \
+    if (!(cond)) return fail(CHFSI_EINVAL, msg); \
+  } while (0)
+#define CK(expr)              \
+  do {                        \
+    int _r = (expr);          \
+    if (_r != CHFSI_OK) return _r; \
+  } while (0)
+
+int ensure_ws(chfsi_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->ws_bytes) return CHFSI_OK;
+  CK_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->ws) CK_CUDA(cudaFree(ctx->ws));
+  ctx->ws = nullptr;
+  ctx->ws_bytes = 0;
+  CK_CUDA(cudaMalloc(&ctx->ws, bytes));
+  ctx->ws_bytes = bytes;
+  return CHFSI_OK;
+}
+
+int ensure_scratch(chfsi_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->scratch_bytes) return CHFSI_OK;
+  CK_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->scratch) CK_CUDA(cudaFree(ctx->scratch));
+  ctx->scratch = nullptr;
+  ctx->scratch_bytes = 0;
+  CK_CUDA(cudaMalloc(&ctx->scratch, bytes));
+  ctx->scratch_bytes = bytes;
+  return CHFSI_OK;
+}
+
+cublasOperation_t op_of(char t) {
+  switch (t) {
+    case 'T': case 't': return CUBLAS_OP_T;
+    case 'C': case 'c': return CUBLAS_OP_C;
+    default: return CUBLAS_OP_N;
+  }
+}
+
+bool valid_op(char t) { return t == 'N' || t == 'n' || t == 'T' || t == 't' || t == 'C' || t == 'c'; }
+
+}  // namespace
+
+extern "C" {
+
+int chfsi_version(void) { return 1; }
+
+const char* chfsi_last_error(void) { return g_last_error.c_str(); }
+
+int chfsi_ctx_create(int device, chfsi_ctx** out) {
+  CK_ARG(out != nullptr, "out is NULL");
+  *out = nullptr;
+  CK_CUDA(cudaSetDevice(device));
+  chfsi_ctx* ctx = new chfsi_ctx();
+  ctx->device = device;
+  if (cublasCreate(&ctx->blas) != CUBLAS_STATUS_SUCCESS) {
+    delete ctx;
+    return fail(CHFSI_ECUBLAS, "cublasCreate failed");
+  }
+  if (cusolverDnCreate(&ctx->solver) != CUSOLVER_STATUS_SUCCESS) {
+    cublasDestroy(ctx->blas);
+    delete ctx;
+    return fail(CHFSI_ECUSOLVER, "cusolverDnCreate failed");
+  }
+  // deterministic, exact FP64 arithmetic in the library GEMMs
+  cublasSetAtomicsMode(ctx->blas, CUBLAS_ATOMICS_NOT_ALLOWED);
+  cublasSetMathMode(ctx->blas, CUBLAS_DEFAULT_MATH);
+  cublasSetPointerMode(ctx->blas, CUBLAS_POINTER_MODE_HOST);
+  CK_CUDA(cudaMalloc(&ctx->partial, chfsi::kRedBlocks * sizeof(double)));
+  CK_CUDA(cudaMalloc(&ctx->scalars, 16 * sizeof(double)));
+  CK_CUDA(cudaMalloc(&ctx->dinfo, 4 * sizeof(int)));
+  CK_CUDA(cudaMalloc(&ctx->lstate, sizeof(LanczosState)));
+  *out = ctx;
+  return CHFSI_OK;
+}
+
+int chfsi_ctx_destroy(chfsi_ctx* ctx) {
+  if (!ctx) return CHFSI_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  cudaDeviceSynchronize();
+  if (ctx->blas) cublasDestroy(ctx->blas);
+  if (ctx->solver) cusolverDnDestroy(ctx->solver);
+  cudaFree(ctx->ws);
+  cudaFree(ctx->scratch);
+  cudaFree(ctx->partial);
+  cudaFree(ctx->scalars);
+  cudaFree(ctx->dinfo);
+  cudaFree(ctx->lstate);
+  delete ctx;
+  return CHFSI_OK;
+}
+
+int chfsi_ctx_set_tiling(chfsi_ctx* ctx, int bm, int bn, int split) {
+  CK_ARG(ctx, "ctx is NULL");
+  if (bm == 0) {
+    ctx->tiling = chfsi::StepTiling{0, 0, 0};
+    return CHFSI_OK;
+  }
+  CK_ARG(bm == 64 && (bn == 32 || bn == 64) && (split == 1 || split == 2 || split == 4 || split == 8),
+         "unsupported K1 tiling");
+  ctx->tiling = chfsi::StepTiling{bm, bn, split};
+  return CHFSI_OK;
+}
+
+int chfsi_ctx_set_stream(chfsi_ctx* ctx, void* stream) {
+  CK_ARG(ctx, "ctx is NULL");
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  CK_BLAS(cublasSetStream(ctx->blas, ctx->stream));
+  CK_SOLVER(cusolverDnSetStream(ctx->solver, ctx->stream));
+  return CHFSI_OK;
+}
+
+// ------------------------------------------------------------------- K1 ---
+
+int chfsi_cheb_step_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, int conj_h,
+                      const void* ycur, long long ldc, const void* yprev, long long ldp,
+                      void* ynext, long long ldn, double alpha, double c, double beta) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(n >= 0 && w >= 0, "negative size");
+  if (n == 0 || w == 0) return CHFSI_OK;
+  CK_ARG(H && ycur && ynext, "NULL operand");
+  CK_ARG(ldh >= n && ldc >= n && ldn >= n && (!yprev || ldp >= n), "leading dimension < n");
+  CK_ARG(ycur != ynext, "Ycur must not alias Ynext");
+  CK_CUDA(chfsi::cheb_step_launch(static_cast<const double2*>(H), ldh, conj_h != 0,
+                                  static_cast<const double2*>(ycur), ldc,
+                                  static_cast<const double2*>(yprev), ldp,
+                                  static_cast<double2*>(ynext), ldn, n, w, alpha, c, beta,
+                                  ctx->tiling, ctx->stream));
+  return CHFSI_OK;
+}
+
+int chfsi_filter_coeffs(int deg, double a, double b, double scale_ref, double* c, double* alphas,
+                        double* betas) {
+  CK_ARG(deg >= 1, "polynomial degree must be >= 1");
+  CK_ARG(c && alphas && betas, "NULL output");
+  // chfsi.py:198-207, operation for operation
+  const double e = (b - a) / 2;
+  const double cc = (b + a) / 2;
+  double sigma = e / (scale_ref - cc);
+  const double tau = 2.0 / sigma;
+  *c = cc;
+  alphas[0] = sigma / e;
+  betas[0] = 0.0;
+  for (int j = 1; j < deg; ++j) {
+    const double sigma_new = 1.0 / (tau - sigma);
+    alphas[j] = 2 * sigma_new / e;
+    betas[j] = sigma * sigma_new;
+    sigma = sigma_new;
+  }
+  return CHFSI_OK;
+}
+
+int chfsi_filter_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, int conj_h,
+                   const void* y0, long long ldy0, void* buf_a, void* buf_b, long long ldb,
+                   int deg, double a, double b, double scale_ref, void** result) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(deg >= 1, "polynomial degree must be >= 1");
+  CK_ARG(n >= 0 && w >= 0, "negative size");
+  CK_ARG(result, "result is NULL");
+  CK_ARG(buf_a != buf_b && y0 != buf_a, "buffers must be distinct (y0 may equal buf_b)");
+  std::vector<double> al(deg), be(deg);
+  double c = 0.0;
+  CK(chfsi_filter_coeffs(deg, a, b, scale_ref, &c, al.data(), be.data()));
+  *result = (deg % 2) ? buf_a : buf_b;
+  if (n == 0 || w == 0) return CHFSI_OK;
+  const chfsi::StepTiling tiling =
+      ctx->tiling.bm ? ctx->tiling : chfsi::choose_step_tiling(n, w);
+  const double2* hh = static_cast<const double2*>(H);
+  const double2* prev = nullptr;
+  long long ldp = 0;
+  const double2* cur = static_cast<const double2*>(y0);
+  long long ldcur = ldy0;
+  for (int j = 0; j < deg; ++j) {
+    double2* dst = static_cast<double2*>((j % 2 == 0) ? buf_a : buf_b);
+    CK_CUDA(chfsi::cheb_step_launch(hh, ldh, conj_h != 0, cur, ldcur, prev, ldp, dst, ldb, n, w,
+                                    al[j], c, be[j], tiling, ctx->stream));
+    prev = cur;
+    ldp = ldcur;
+    cur = dst;
+    ldcur = ldb;
+  }
+  return CHFSI_OK;
+}
+
+int chfsi_step_tiling(int n, int w, int* bm, int* bn, int* split) {
+  CK_ARG(bm && bn && split, "NULL output");
+  const chfsi::StepTiling t = chfsi::choose_step_tiling(n, w);
+  *bm = t.bm;
+  *bn = t.bn;
+  *split = t.split;
+  return CHFSI_OK;
+}
+
+// ------------------------------------------------------------------- K2 ---
+
+int chfsi_lanczos_z(chfsi_ctx* ctx, int n, int k, const void* H, long long ldh, int conj_h,
+                    const void* q0, void* basis, double* alphas, double* betas, double* beta_last,
+                    int* steps) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(n >= 1 && k >= 1 && k <= n, "need 1 <= k <= n");
+  CK_ARG(H && q0 && basis && alphas && betas && beta_last && steps, "NULL argument");
+  // scratch: u, r (n each), coef (k), alphas_d, betas_d (k doubles each)
+  const size_t vec = (size_t)n * sizeof(double2);
+  CK(ensure_scratch(ctx, 2 * vec + (size_t)k * sizeof(double2) + 2 * (size_t)k * sizeof(double) + 256));
+  char* base = static_cast<char*>(ctx->scratch);
+  double2* u = reinterpret_cast<double2*>(base);
+  double2* r = reinterpret_cast<double2*>(base + vec);
+  double2* coef = reinterpret_cast<double2*>(base + 2 * vec);
+  double* al_d = reinterpret_cast<double*>(base + 2 * vec + (size_t)k * sizeof(double2));
+  double* be_d = al_d + k;
+  double2* V = static_cast<double2*>(basis);
+  const double2* hh = static_cast<const double2*>(H);
+  cudaStream_t s = ctx->stream;
+  LanczosState* st = ctx->lstate;
+  const int* done = &st->done;
+  double* nrm = ctx->scalars;
+  CK_CUDA(cudaMemsetAsync(st, 0, sizeof(LanczosState), s));
+  CK_CUDA(cudaMemsetAsync(be_d, 0, (size_t)k * sizeof(double), s));
+  // q = q0 / ||q0||  (chfsi.py:137-138)
+  CK_CUDA(chfsi::norm2_launch(static_cast<const double2*>(q0), n, ctx->partial, nrm, nullptr, s));
+  CK_CUDA(chfsi::div_scalar_launch(static_cast<const double2*>(q0), nrm, V, n, s));
+  for (int i = 0; i < k; ++i) {
+    const double2* q = V + (long long)i * n;
+    CK_CUDA(chfsi::gemv_rows_launch(hh, ldh, conj_h != 0, q, u, n, done, s));
+    CK_CUDA(chfsi::dot_re_launch(q, u, n, ctx->partial, al_d + i, done, s));
+    CK_CUDA(chfsi::lanczos_residual_launch(u, q, i ? V + (long long)(i - 1) * n : nullptr,
+                                           al_d + i, i ? be_d + i - 1 : nullptr, r, n, done, s));
+    CK_CUDA(chfsi::colsdot_launch(V, n, n, i + 1, r, coef, done, s));
+    CK_CUDA(chfsi::sub_vcoef_launch(V, n, n, i + 1, coef, r, done, s));
+    CK_CUDA(chfsi::norm2_launch(r, n, ctx->partial, nrm, done, s));
+    CK_CUDA(chfsi::lanczos_advance_launch(r, nrm, i + 1 < k ? V + (long long)(i + 1) * n : nullptr,
+                                          be_d + i, st, i, k, n, s));
+  }
+  LanczosState hst;
+  CK_CUDA(cudaMemcpyAsync(&hst, st, sizeof(hst), cudaMemcpyDeviceToHost, s));
+  CK_CUDA(cudaMemcpyAsync(alphas, al_d, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK_CUDA(cudaMemcpyAsync(betas, be_d, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK_CUDA(cudaStreamSynchronize(s));
+  *steps = hst.steps;
+  *beta_last = hst.beta_last;
+  return CHFSI_OK;
+}
+
+// ------------------------------------------------------------ K3 / K4 ---
+
+int chfsi_gemm_z(chfsi_ctx* ctx, char transa, char transb, int m, int n, int k, double alpha_re,
+                 double alpha_im, const void* A, long long lda, const void* B, long long ldb,
+                 double beta_re, double beta_im, void* C, long long ldc) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(valid_op(transa) && valid_op(transb), "unknown transpose flag");
+  CK_ARG(m >= 0 && n >= 0 && k >= 0, "negative size");
+  if (m == 0 || n == 0) return CHFSI_OK;
+  const cuDoubleComplex al = make_cuDoubleComplex(alpha_re, alpha_im);
+  const cuDoubleComplex be = make_cuDoubleComplex(beta_re, beta_im);
+  CK_BLAS(cublasZgemm(ctx->blas, op_of(transa), op_of(transb), m, n, k, &al,
+                      static_cast<const cuDoubleComplex*>(A), (int)lda,
+                      static_cast<const cuDoubleComplex*>(B), (int)ldb, &be,
+                      static_cast<cuDoubleComplex*>(C), (int)ldc));
+  return CHFSI_OK;
+}
+
+int chfsi_cgs_project_z(chfsi_ctx* ctx, int n, int nlocked, int w, const void* locked,
+                        long long ldl, void* work, long long ldw, void* coef) {
+  CK_ARG(ctx, "ctx is NULL");
+  if (nlocked == 0 || w == 0 || n == 0) return CHFSI_OK;
+  for (int pass = 0; pass < 2; ++pass) {
+    CK(chfsi_gemm_z(ctx, 'C', 'N', nlocked, w, n, 1.0, 0.0, locked, ldl, work, ldw, 0.0, 0.0,
+                    coef, nlocked));
+    CK(chfsi_gemm_z(ctx, 'N', 'N', n, w, nlocked, -1.0, 0.0, locked, ldl, coef, nlocked, 1.0,
+                    0.0, work, ldw));
+  }
+  return CHFSI_OK;
+}
+
+int chfsi_qr_orthonormalize_z(chfsi_ctx* ctx, int m, int n, void* Y, long long ldy, int* dead,
+                              int* ndead) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(m >= n && n >= 0, "need rows >= cols");
+  CK_ARG(ndead && dead, "NULL output");
+  *ndead = 0;
+  if (n == 0) return CHFSI_OK;
+  CK_ARG(ldy == m, "QR needs a packed block (ldy == m)");
+  cudaStream_t s = ctx->stream;
+  double2* y = static_cast<double2*>(Y);
+  // scratch: backup copy of Y (m*n), tau (n), rdiag (n)
+  const size_t blk = (size_t)m * n * sizeof(double2);
+  CK(ensure_scratch(ctx, blk + 2 * (size_t)n * sizeof(double2)));
+  double2* backup = static_cast<double2*>(ctx->scratch);
+  double2* tau = backup + (size_t)m * n;
+  double2* rdiag = tau + n;
+  double* fro = ctx->scalars + 1;
+  CK_CUDA(cudaMemcpyAsync(backup, y, blk, cudaMemcpyDeviceToDevice, s));
+  CK_CUDA(chfsi::norm2_launch(y, (long long)m * n, ctx->partial, fro, nullptr, s));
+  int lwork = 0, lwork2 = 0;
+  CK_SOLVER(cusolverDnZgeqrf_bufferSize(ctx->solver, m, n, reinterpret_cast<cuDoubleComplex*>(y),
+                                        m, &lwork));
+  CK_SOLVER(cusolverDnZungqr_bufferSize(ctx->solver, m, n, n,
+                                        reinterpret_cast<cuDoubleComplex*>(y), m,
+                                        reinterpret_cast<cuDoubleComplex*>(tau), &lwork2));
+  if (lwork2 > lwork) lwork = lwork2;
+  CK(ensure_ws(ctx, (size_t)lwork * sizeof(cuDoubleComplex)));
+  CK_SOLVER(cusolverDnZgeqrf(ctx->solver, m, n, reinterpret_cast<cuDoubleComplex*>(y), m,
+                             reinterpret_cast<cuDoubleComplex*>(tau),
+                             static_cast<cuDoubleComplex*>(ctx->ws), lwork, ctx->dinfo));
+  CK_CUDA(chfsi::extract_diag_launch(y, m, n, rdiag, s));
+  std::vector<double2> hd(n);
+  double hfro = 0.0;
+  CK_CUDA(cudaMemcpyAsync(hd.data(), rdiag, (size_t)n * sizeof(double2), cudaMemcpyDeviceToHost, s));
+  CK_CUDA(cudaMemcpyAsync(&hfro, fro, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK_CUDA(cudaStreamSynchronize(s));
+  const double thresh = 1e-13 * hfro;  // linalg.py:173
+  int nd = 0;
+  for (int j = 0; j < n; ++j)
+    if (std::hypot(hd[j].x, hd[j].y) < thresh) dead[nd++] = j;
+  if (nd) {
+    *ndead = nd;
+    CK_CUDA(cudaMemcpyAsync(y, backup, blk, cudaMemcpyDeviceToDevice, s));
+    return fail(CHFSI_ERANK, "rank-deficient columns");
+  }
+  CK_SOLVER(cusolverDnZungqr(ctx->solver, m, n, n, reinterpret_cast<cuDoubleComplex*>(y), m,
+                             reinterpret_cast<cuDoubleComplex*>(tau),
+                             static_cast<cuDoubleComplex*>(ctx->ws), lwork, ctx->dinfo));
+  CK_CUDA(chfsi::phase_fix_launch(y, m, m, n, rdiag, s));
+  return CHFSI_OK;
+}
+
+int chfsi_heevd_z(chfsi_ctx* ctx, int n, void* A, long long lda, double* w) {
+  CK_ARG(ctx, "ctx is NULL");
+  if (n == 0) return CHFSI_OK;
+  CK_ARG(A && w && lda >= n, "bad argument");
+  int lwork = 0;
+  cuDoubleComplex* a = static_cast<cuDoubleComplex*>(A);
+  CK_SOLVER(cusolverDnZheevd_bufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR,
+                                        CUBLAS_FILL_MODE_LOWER, n, a, (int)lda, w, &lwork));
+  CK(ensure_ws(ctx, (size_t)lwork * sizeof(cuDoubleComplex)));
+  CK_SOLVER(cusolverDnZheevd(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, a,
+                             (int)lda, w, static_cast<cuDoubleComplex*>(ctx->ws), lwork,
+                             ctx->dinfo));
+  int info = 0;
+  CK_CUDA(cudaMemcpyAsync(&info, ctx->dinfo, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (info != 0) return fail(CHFSI_EEIG, "zheevd failed to converge, info=" + std::to_string(info));
+  return CHFSI_OK;
+}
+
+int chfsi_colnorm_residual_z(chfsi_ctx* ctx, int n, int w, const void* HP, long long ldhp,
+                             const void* P, long long ldp, const double* lambda, double* res) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(HP && res, "NULL argument");
+  CK_CUDA(chfsi::colnorm_residual_launch(static_cast<const double2*>(HP), ldhp,
+                                         static_cast<const double2*>(P), ldp, lambda, n, w, res,
+                                         ctx->stream));
+  return CHFSI_OK;
+}
+
+// ------------------------------------------------------------------- K5 ---
+
+int chfsi_symmetrize_z(chfsi_ctx* ctx, int n, void* A, long long lda) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_CUDA(chfsi::symmetrize_launch(static_cast<double2*>(A), lda, n, ctx->stream));
+  return CHFSI_OK;
+}
+
+int chfsi_herm_defect_z(chfsi_ctx* ctx, int n, const void* A, long long lda, double* defect,
+                        double* maxabs) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(defect && maxabs, "NULL output");
+  double* out = ctx->scalars + 4;
+  CK_CUDA(chfsi::herm_defect_launch(static_cast<const double2*>(A), lda, n, out, ctx->stream));
+  double h[2];
+  CK_CUDA(cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  CK_CUDA(cudaStreamSynchronize(ctx->stream));
+  *defect = h[0];
+  *maxabs = h[1];
+  return CHFSI_OK;
+}
+
+int chfsi_conj_z(chfsi_ctx* ctx, int m, int n, void* A, long long lda) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_CUDA(chfsi::conj_inplace_launch(static_cast<double2*>(A), lda, m, n, ctx->stream));
+  return CHFSI_OK;
+}
+
+int chfsi_potrf_z(chfsi_ctx* ctx, int n, void* A, long long lda, int* info) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(info, "info is NULL");
+  *info = 0;
+  if (n == 0) return CHFSI_OK;
+  cuDoubleComplex* a = static_cast<cuDoubleComplex*>(A);
+  int lwork = 0;
+  CK_SOLVER(cusolverDnZpotrf_bufferSize(ctx->solver, CUBLAS_FILL_MODE_LOWER, n, a, (int)lda, &lwork));
+  CK(ensure_ws(ctx, (size_t)lwork * sizeof(cuDoubleComplex)));
+  CK_SOLVER(cusolverDnZpotrf(ctx->solver, CUBLAS_FILL_MODE_LOWER, n, a, (int)lda,
+                             static_cast<cuDoubleComplex*>(ctx->ws), lwork, ctx->dinfo));
+  CK_CUDA(cudaMemcpyAsync(info, ctx->dinfo, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (*info != 0)
+    return fail(CHFSI_ENOTPD, "Cholesky pivot " + std::to_string(*info) + " is not positive");
+  CK_CUDA(chfsi::zero_upper_launch(static_cast<double2*>(A), lda, n, ctx->stream));
+  return CHFSI_OK;
+}
+
+int chfsi_trsm_z(chfsi_ctx* ctx, char side, char trans, int m, int n, const void* L,
+                 long long ldl, void* B, long long ldb) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(side == 'L' || side == 'R', "side must be 'L' or 'R'");
+  CK_ARG(trans == 'N' || trans == 'C', "trans must be 'N' or 'C'");
+  if (m == 0 || n == 0) return CHFSI_OK;
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
+  CK_BLAS(cublasZtrsm(ctx->blas, side == 'L' ? CUBLAS_SIDE_LEFT : CUBLAS_SIDE_RIGHT,
+                      CUBLAS_FILL_MODE_LOWER, op_of(trans), CUBLAS_DIAG_NON_UNIT, m, n, &one,
+                      static_cast<const cuDoubleComplex*>(L), (int)ldl,
+                      static_cast<cuDoubleComplex*>(B), (int)ldb));
+  return CHFSI_OK;
+}
+
+int chfsi_to_standard_z(chfsi_ctx* ctx, int n, void* A, long long lda, void* B, long long ldb,
+                        int rowmajor_in, int* info) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(info, "info is NULL");
+  if (rowmajor_in) {  // Hermitian: row-major bytes == conj of the column-major matrix
+    CK(chfsi_conj_z(ctx, n, n, A, lda));
+    CK(chfsi_conj_z(ctx, n, n, B, ldb));
+  }
+  CK(chfsi_potrf_z(ctx, n, B, ldb, info));                  // B = L L^H
+  CK(chfsi_trsm_z(ctx, 'L', 'N', n, n, B, ldb, A, lda));    // Z = L^-1 A
+  CK(chfsi_trsm_z(ctx, 'R', 'C', n, n, B, ldb, A, lda));    // H = Z L^-H
+  CK(chfsi_symmetrize_z(ctx, n, A, lda));                   // (H + H^H)/2
+  return CHFSI_OK;
+}
+
+int chfsi_back_transform_z(chfsi_ctx* ctx, int n, int nev, const void* L, long long ldl, void* Y,
+                           long long ldy) {
+  return chfsi_trsm_z(ctx, 'L', 'C', n, nev, L, ldl, Y, ldy);
+}
+
+}  // extern "C"

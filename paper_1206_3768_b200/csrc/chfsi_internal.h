@@ -1,0 +1,83 @@
+// Internal (C++) declarations shared by the kernel translation units and
+// the C-ABI layer. Not part of the public interface (see include/chfsi.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace chfsi {
+
+struct StepTiling {
+  int bm;     // 0 = choose automatically
+  int bn;
+  int split;  // K split across a thread-block cluster (1, 2, 4, 8)
+};
+
+StepTiling choose_step_tiling(int n, int w);
+
+// K1: Ynext = alpha*(op(H) Ycur - c Ycur) - beta Yprev; Yprev may alias Ynext
+// (or be null when beta == 0). op(H) = H (row-major read) or conj(H).
+cudaError_t cheb_step_launch(const double2* h, long long ldh, bool conj_h, const double2* ycur,
+                             long long ldc, const double2* yprev, long long ldp, double2* ynext,
+                             long long ldn, int n, int w, double alpha, double c, double beta,
+                             StepTiling tiling, cudaStream_t stream);
+
+// ---- auxiliary kernels (aux_kernels.cu) ----
+// u = op(H) q for a row-major H (conj_h: conj(H)).
+cudaError_t gemv_rows_launch(const double2* h, long long ldh, bool conj_h, const double2* q,
+                             double2* u, int n, const int* done, cudaStream_t s);
+// Deterministic reductions. partial buffers must hold kRedBlocks entries.
+constexpr int kRedBlocks = 296;
+constexpr int kRedThreads = 256;
+// out = Re(x^H y) or ||x||_2 (op 0/1); x,y length n.
+cudaError_t dot_re_launch(const double2* x, const double2* y, int n, double* partial, double* out,
+                          const int* done, cudaStream_t s);
+cudaError_t norm2_launch(const double2* x, long long n, double* partial, double* out,
+                         const int* done, cudaStream_t s);
+// out[j] = x_j^H r for columns j < ncols of col-major V (ld).
+cudaError_t colsdot_launch(const double2* v, long long ldv, int n, int ncols, const double2* r,
+                           double2* out, const int* done, cudaStream_t s);
+// r[i] -= sum_j V[i,j] coef[j]   (fixed j order)
+cudaError_t sub_vcoef_launch(const double2* v, long long ldv, int n, int ncols,
+                             const double2* coef, double2* r, const int* done, cudaStream_t s);
+
+// Lanczos step pieces with device-side control state.
+struct LanczosState {
+  int done;
+  int steps;
+  double beta_last;
+};
+cudaError_t lanczos_residual_launch(const double2* u, const double2* q, const double2* qprev,
+                                    const double* alpha_i, const double* beta_prev, double2* r,
+                                    int n, const int* done, cudaStream_t s);
+cudaError_t lanczos_advance_launch(const double2* r, const double* beta, double2* qnext,
+                                   double* betas_i, LanczosState* st, int i, int k, int n,
+                                   cudaStream_t s);
+
+// res[j] = || HP[:,j] - lambda[j] P[:,j] ||_2  (col-major, one block per column)
+cudaError_t colnorm_residual_launch(const double2* hp, long long ldhp, const double2* p,
+                                    long long ldp, const double* lambda, int n, int w,
+                                    double* res, cudaStream_t s);
+// res[j] = || X[:,j] ||_2
+cudaError_t colnorm_launch(const double2* x, long long ldx, int n, int w, double* res,
+                           cudaStream_t s);
+// A <- (A + A^H)/2 in place (square, col-major or row-major alike)
+cudaError_t symmetrize_launch(double2* a, long long lda, int n, cudaStream_t s);
+// out[0] = max |A - A^H|, out[1] = max |A|
+cudaError_t herm_defect_launch(const double2* a, long long lda, int n, double* out,
+                               cudaStream_t s);
+// A <- conj(A) elementwise (m x n col-major block); also zero strict upper if tril
+cudaError_t conj_inplace_launch(double2* a, long long lda, int m, int n, cudaStream_t s);
+cudaError_t zero_upper_launch(double2* a, long long lda, int n, cudaStream_t s);
+// Q[:, j] *= conj(d_j / |d_j|), d_j = R[j, j] read from the (separate) diag array
+cudaError_t phase_fix_launch(double2* q, long long ldq, int m, int n, const double2* rdiag,
+                             cudaStream_t s);
+// diag[j] = A[j, j]
+cudaError_t extract_diag_launch(const double2* a, long long lda, int n, double2* diag,
+                                cudaStream_t s);
+// y = x / *d (complex / real, round-to-nearest division)
+cudaError_t div_scalar_launch(const double2* x, const double* d, double2* y, int n, cudaStream_t s);
+// Y[:, j] = X[:, j]
+cudaError_t copy_cols_launch(const double2* x, long long ldx, double2* y, long long ldy, int m,
+                             int n, cudaStream_t s);
+
+}  // namespace chfsi

@@ -1,0 +1,138 @@
+"""Sequence driver on the device — drop-in for the solver path of
+`spectral_chain.harness` (reference `harness.py:149-289`).
+
+Two protocols over a correlated sequence of pencils (label 1..N):
+
+* ``mode="harness"`` — the reference's parity protocol (harness.py:235-255):
+  problem l >= 2 is warm-started from the DENSE eigendecomposition of
+  problem l-1 (here cuSOLVER zheevd on the device), lambda_1 and
+  lambda_{blk+1} taken from that full spectrum; rng ``(seed, l, 1)``.
+* ``mode="chained"`` — production warm starts: problem l >= 2
+  starts from the previous ChFSI tail block ``[locked | unlocked panel]``
+  and its Ritz window; no dense solve anywhere.
+
+Problem 1 is always a cold start with rng ``(seed, 1, 0)``. Every problem
+runs to_standard -> chfsi_solve -> back_transform on the device.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .chfsi import ChfsiConfig, ChfsiGuess, chfsi_solve
+from .linalg import hermitian_eig
+from .reduction import EigenPencil, EigenSolution, back_transform, to_standard
+
+__all__ = [
+    "OracleMismatchError",
+    "oracle_solve",
+    "ProblemResult",
+    "solve_sequence",
+    "check_oracle",
+]
+
+_ORACLE_TOL = 1e-8  # harness.py:49
+
+
+class OracleMismatchError(RuntimeError):
+    """An iterative solve disagreed with the direct solver (harness.py:68-69)."""
+
+
+def oracle_solve(pencil, nev):
+    """Dense direct solution of a pencil on the device (harness.py:149-161):
+    (standard-form solution of ``nev`` pairs, reduced problem, full spectrum)."""
+    sp = to_standard(pencil)
+    values, vectors = hermitian_eig(sp.h)
+    sol = EigenSolution(values=values[:nev], vectors=vectors[:, :nev], form="standard",
+                        label=pencil.label)
+    return sol, sp, values
+
+
+def check_oracle(values, oracle_values, label, start="warm"):
+    """|lambda - lambda_dense| <= 1e-8 * spectrum scale (harness.py:179-185)."""
+    scale = float(max(abs(oracle_values[0]), abs(oracle_values[-1]), 1e-300))
+    err = float(np.abs(np.asarray(values) - oracle_values[: len(values)]).max(initial=0.0))
+    if err > _ORACLE_TOL * scale:
+        raise OracleMismatchError(
+            f"problem {label} ({start} start): eigenvalue error {err:.3e} exceeds "
+            f"{_ORACLE_TOL:.0e} on spectrum scale {scale:.3e}")
+    return err
+
+
+@dataclass
+class ProblemResult:
+    label: int
+    values: np.ndarray
+    solution: EigenSolution          # generalized form (x = L^-H y), device vectors
+    standard_vectors: object         # standard-form y (device) — for parity checks
+    report: object
+    t_reduce: float = 0.0
+    t_solve: float = 0.0
+    t_back: float = 0.0
+    dense_values: np.ndarray | None = None
+    extra: dict = field(default_factory=dict)
+
+
+def _as_pencil(p):
+    if isinstance(p, EigenPencil):
+        return p
+    label, a, b = p
+    return EigenPencil(a=a, b=b, label=label)
+
+
+def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on_problem=None):
+    """Solve a correlated sequence on the device.
+
+    ``pencils`` yields EigenPencil or ``(label, A, B)`` (numpy or torch).
+    ``cfg`` is a ChfsiConfig (``nex`` accepted). Returns a list of
+    ProblemResult; ``on_problem(result)`` is called after each problem.
+    """
+    if mode not in ("chained", "harness"):
+        raise ValueError(f"unknown mode {mode!r}")
+    out = []
+    guess = None
+    for item in pencils:
+        pencil = _as_pencil(item)
+        n = pencil.n
+        blk = cfg.resolve(n)[0]
+        if mode == "harness" and blk >= n:
+            raise ValueError(f"chfsi warm starts need blk < n (blk={blk}, n={n})")
+        t0 = time.perf_counter()
+        sp = to_standard(pencil)
+        torch.cuda.current_stream().synchronize()
+        t1 = time.perf_counter()
+        start = 0 if guess is None else 1
+        rng = np.random.default_rng((seed, pencil.label, start))
+        sol, rep = chfsi_solve(sp.h, cfg, guess=guess, rng=rng, label=pencil.label)
+        t2 = time.perf_counter()
+        gsol = back_transform(sp.cholesky_factor, sol)
+        torch.cuda.current_stream().synchronize()
+        t3 = time.perf_counter()
+        res = ProblemResult(label=pencil.label, values=sol.values, solution=gsol,
+                            standard_vectors=sol.vectors if keep_standard else None, report=rep,
+                            t_reduce=t1 - t0, t_solve=t2 - t1, t_back=t3 - t2)
+        if mode == "harness":
+            dv, dvec = hermitian_eig(sp.h)
+            res.dense_values = dv
+            guess = ChfsiGuess(vectors=dvec[:, :blk], lambda1=float(dv[0]),
+                               lambda_blk_plus_1=float(dv[blk]))
+        else:
+            if rep.tail_vectors is not None and rep.tail_vectors.shape[1] == blk and sol.nev:
+                guess = ChfsiGuess(vectors=rep.tail_vectors, lambda1=float(sol.values[0]),
+                                   lambda_blk_plus_1=float(rep.lambda_blk_plus_1))
+            else:  # a partial solve leaves no full block: restart cold
+                guess = None
+        out.append(res)
+        if on_problem is not None:
+            on_problem(res)
+        del sp
+    return out
+
+
+def default_config(cfg):
+    """ChfsiConfig for a BASELINE config (sequence.BaselineConfig)."""
+    return ChfsiConfig(nev=cfg.nev, nex=cfg.nex, deg=cfg.deg, tol=cfg.tol)

