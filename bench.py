@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 ChFSI hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2]
+    python bench.py --impl reference ...          # CPU reference arm
+
+One STEP = one full correlated sequence of BASELINE config ``--config``
+(default C2: n=2048, N=10, nev=128, nex=32, deg=16, tol=1e-10) solved in
+chained mode (problem 1 cold, problems 2..N warm-started from the previous
+ChFSI block): to_standard -> chfsi_solve -> back_transform per problem.
+
+Reported (one JSON line on rank 0):
+* ``value``  = filter FLOPs of the sequence (8 n^2 per filtered column per
+  degree) / device time-to-solution of the sequence, inputs resident in HBM
+  — the "Chebyshev filter GFLOP/s" of the whole job; ``ms_per_step`` is the
+  time-to-solution per sequence;
+* ``e2e``    = the same metric through the public API with HOST (pinned)
+  inputs: H2D of every A, B and D2H of every eigenpair inside the timed region;
+* ``roofline`` = the fused filter kernel K1 alone: filter FLOPs / summed
+  device time of the filter launches (CUDA events on the launch stream) vs
+  the measured FP64 DMMA peak;
+* ``cpu_baseline`` = the numpy oracle port of the reference path on this
+  host's cores, on a bounded sample (problems 1-2 of the same sequence).
+
+Multi-GPU (torchrun, N>1): the sequence is not sharded at C1/C2 — every
+rank solves its own replica ("scaling": "weak", no data-path collective);
+value = N x sequence FLOPs / max-over-ranks time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "Chebyshev filter FP64 GFLOP/s (% of peak) and time-to-solution per sequence"
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+K1_TRAFFIC_FILE = os.path.join(ROOT, "profiles", "k1_traffic.json")
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--mode", choices=["chained", "harness"], default="chained")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=2, help="problems in the CPU sample")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks ---
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        self.proc.wait(timeout=10)
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), float(parts[2]), parts[3:7]))
+            except ValueError:
+                continue
+        os.unlink(self.path)
+        if not rows:
+            return None
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[3]) if v == "Active"})
+        loaded = [r[0] for r in rows if r[2] > 250.0] or [r[0] for r in rows]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(r[2] for r in rows)}
+
+
+# ------------------------------------------------------------------ inputs ---
+
+def host_sequence(cfg_b, limit=None):
+    from paper_1206_3768_b200.sequence import iter_baseline_sequence
+
+    out = []
+    for label, a, b in iter_baseline_sequence(cfg_b.n, cfg_b.length, seed=0):
+        out.append((label, a, b))
+        if limit is not None and len(out) >= limit:
+            break
+    return out
+
+
+# --------------------------------------------------------------- CPU arm ---
+
+def cpu_sample(seq, cfg_b, mode="chained"):
+    """Oracle port (numpy restatement of the reference path) on this host."""
+    from oracle import chfsi_oracle as orc
+
+    t0 = time.perf_counter()
+    res = orc.run_sequence(seq, cfg_b.nev, cfg_b.nex, cfg_b.deg, cfg_b.tol, seed=0, mode=mode)
+    wall = time.perf_counter() - t0
+    flops = sum(r["filter_flops"] for r in res)
+    return flops, wall, res
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_1206_3768_b200.sequence import BASELINE_CONFIGS
+
+    cfg_b = BASELINE_CONFIGS[args.config]
+    seq = host_sequence(cfg_b, limit=args.cpu_sample)
+    for _ in range(args.warmup):
+        cpu_sample(seq[:1], cfg_b)
+    times, flops = [], 0.0
+    for _ in range(args.steps):
+        f, wall, _ = cpu_sample(seq, cfg_b)
+        times.append(wall)
+        flops = f
+    total = sum(times)
+    value = flops * args.steps / total / 1e9
+    cores = os.cpu_count()
+    sample = (f"{args.config} problems 1-{len(seq)} (1 cold + {len(seq) - 1} warm, chained), "
+              f"to_standard+chfsi_solve+back_transform, numpy/OpenBLAS on {cores} threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "complex128 (f64)", "data": "synthetic",
+        "config": {"workload": f"{args.config} (CPU sample: {len(seq)} problems)",
+                   "n": cfg_b.n, "nev": cfg_b.nev, "nex": cfg_b.nex, "deg": cfg_b.deg},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- GPU arm ---
+
+def run_ours(args):
+    import torch
+
+    import paper_1206_3768_b200 as pkg
+    from paper_1206_3768_b200 import _lib
+    from paper_1206_3768_b200.harness import default_config, solve_sequence
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    cfg_b = pkg.BASELINE_CONFIGS[args.config]
+    cfg = default_config(cfg_b)
+    seq = host_sequence(cfg_b)
+    n = cfg_b.n
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # resident inputs (HBM) for `value`
+    dev_pencils = [pkg.EigenPencil(a=torch.from_numpy(a).to(dev), b=torch.from_numpy(b).to(dev),
+                                   label=lab) for lab, a, b in seq]
+
+    def device_step():
+        return solve_sequence(dev_pencils, cfg, seed=0, mode=args.mode)
+
+    for _ in range(args.warmup):
+        device_step()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    lc0 = _lib.lib().chfsi_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    results = [device_step() for _ in range(args.steps)]
+    e1.record()
+    barrier()
+    launches = _lib.lib().chfsi_launch_count() - lc0
+    clk = clocks.stop()
+    t_dev = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+
+    flops_seq = sum(r.report.filter_flops for r in results[-1])
+    f_time = sum(r.report.t_filter for res in results for r in res)
+    f_flops = sum(r.report.filter_flops for res in results for r in res)
+    f_launch = sum(r.report.filter_launches for res in results for r in res)
+    value = world * flops_seq * args.steps / t_dev / 1e9
+
+    # e2e through the public API from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        pinned = [(lab, torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory())
+                  for lab, a, b in seq]
+        h2d = sum(a.numel() * 16 + b.numel() * 16 for _, a, b in pinned)
+
+        def e2e_step():
+            out = solve_sequence(((lab, a, b) for lab, a, b in pinned), cfg, seed=0,
+                                 mode=args.mode)
+            host = [(r.values, r.solution.vectors.cpu()) for r in out]
+            return out, host
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        d2h = 0
+        for _ in range(args.steps):
+            out, host = e2e_step()
+        barrier()
+        t_e2e = max_over_ranks(time.perf_counter() - t0)
+        d2h = sum(v.nbytes + x.numel() * 16 for v, x in host)
+        flops_e2e = sum(r.report.filter_flops for r in out)
+        e2e = {"value": world * flops_e2e * args.steps / t_e2e / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": t_e2e / args.steps * 1e3}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sample = seq[: args.cpu_sample]
+        f, wall, _ = cpu_sample(sample, cfg_b)
+        cpu = {"value": f / wall / 1e9, "unit": "GFLOP/s", "cores": os.cpu_count(),
+               "kind": "port",
+               "sample": f"{args.config} problems 1-{len(sample)} chained (1 cold + "
+                         f"{len(sample) - 1} warm), numpy oracle port, {wall:.1f} s"}
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return 0
+
+    peak = 37.08
+    peak_src = "measured DMMA.8x8x4 peak (profiles/fp64_peak_r01.json); MEASURED_PEAKS.json has no FP64"
+    if os.path.exists(FP64_PEAK_FILE):
+        pk = json.load(open(FP64_PEAK_FILE))
+        peak = float(pk.get("fp64_dmma_tflops", peak))
+    achieved = f_flops / f_time / 1e12 if f_time > 0 else 0.0
+    traffic = None
+    if os.path.exists(K1_TRAFFIC_FILE):
+        traffic = json.load(open(K1_TRAFFIC_FILE)).get(args.config)
+    per_problem = [{"label": r.label, "loops": r.report.inner_loops, "matvecs": r.report.matvecs,
+                    "filtered": r.report.filtered_vectors, "converged": r.report.converged,
+                    "t_solve_ms": round(r.t_solve * 1e3, 3)} for r in results[-1]]
+    line = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "complex128 (f64)", "data": "synthetic",
+        "config": {
+            "workload": f"{args.config}: n={n} N={cfg_b.length} nev={cfg_b.nev} nex={cfg_b.nex} "
+                        f"deg={cfg_b.deg} tol={cfg_b.tol:g}, {args.mode} warm starts, "
+                        "one step = the whole sequence",
+            "value_definition": "filter FLOPs (8 n^2 deg per filtered column) / time-to-solution",
+            "l2": f"inputs larger than L2: {len(seq)} distinct pencils "
+                  f"({len(seq) * 32 * n * n / 1e9:.2f} GB) per step",
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+        },
+        "time_to_solution_s": t_dev / args.steps,
+        "filter_kernel_gflops": achieved * 1e3,
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "cheb_step_kernel (K1)",
+                     "avg_launch_us": f_time / max(f_launch, 1) * 1e6,
+                     "flops_per_launch": f_flops / max(f_launch, 1), "peak_source": peak_src},
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "per_problem": per_problem,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

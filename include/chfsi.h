@@ -49,6 +49,8 @@ typedef struct chfsi_ctx chfsi_ctx;
 
 CHFSI_API int chfsi_version(void);
 CHFSI_API const char* chfsi_last_error(void);
+/* Number of libchfsi kernel launches so far in this process (all devices). */
+CHFSI_API long long chfsi_launch_count(void);
 
 /* One context per device and host thread of use; owns cuBLAS/cuSOLVER
  * handles and a growable device workspace. */

@@ -54,6 +54,7 @@ _pi = ctypes.POINTER(ctypes.c_int)
 _SIGNATURES = {
     "chfsi_version": [],
     "chfsi_last_error": [],
+    "chfsi_launch_count": [],
     "chfsi_ctx_create": [_i, ctypes.POINTER(_vp)],
     "chfsi_ctx_destroy": [_vp],
     "chfsi_ctx_set_stream": [_vp, _vp],
@@ -77,7 +78,7 @@ _SIGNATURES = {
     "chfsi_to_standard_z": [_vp, _i, _vp, _ll, _vp, _ll, _i, _pi],
     "chfsi_back_transform_z": [_vp, _i, _i, _vp, _ll, _vp, _ll],
 }
-_RESTYPES = {"chfsi_last_error": ctypes.c_char_p}
+_RESTYPES = {"chfsi_last_error": ctypes.c_char_p, "chfsi_launch_count": ctypes.c_longlong}
 
 
 def symbols():

@@ -381,6 +381,7 @@ cudaError_t gemv_rows_launch(const double2* h, long long ldh, bool conj_h, const
                              double2* u, int n, const int* done, cudaStream_t s) {
   const int threads = 256;
   const int blocks = grid_for((long long)n * 32, threads, kNumSMs * 8);
+  note_launch();
   if (conj_h) gemv_rows_kernel<true><<<blocks, threads, 0, s>>>(h, ldh, q, u, n, done);
   else gemv_rows_kernel<false><<<blocks, threads, 0, s>>>(h, ldh, q, u, n, done);
   return cudaGetLastError();
@@ -388,14 +389,18 @@ cudaError_t gemv_rows_launch(const double2* h, long long ldh, bool conj_h, const
 
 cudaError_t dot_re_launch(const double2* x, const double2* y, int n, double* partial, double* out,
                           const int* done, cudaStream_t s) {
+  note_launch();
   reduce_partial_kernel<0><<<kRedBlocks, kRedThreads, 0, s>>>(x, y, n, partial, done);
+  note_launch();
   reduce_final_kernel<0><<<1, 1024, 0, s>>>(partial, kRedBlocks, out, done);
   return cudaGetLastError();
 }
 
 cudaError_t norm2_launch(const double2* x, long long n, double* partial, double* out,
                          const int* done, cudaStream_t s) {
+  note_launch();
   reduce_partial_kernel<1><<<kRedBlocks, kRedThreads, 0, s>>>(x, nullptr, n, partial, done);
+  note_launch();
   reduce_final_kernel<1><<<1, 1024, 0, s>>>(partial, kRedBlocks, out, done);
   return cudaGetLastError();
 }
@@ -403,6 +408,7 @@ cudaError_t norm2_launch(const double2* x, long long n, double* partial, double*
 cudaError_t colsdot_launch(const double2* v, long long ldv, int n, int ncols, const double2* r,
                            double2* out, const int* done, cudaStream_t s) {
   if (ncols <= 0) return cudaSuccess;
+  note_launch();
   colsdot_kernel<<<ncols, 256, 0, s>>>(v, ldv, n, r, out, done);
   return cudaGetLastError();
 }
@@ -410,6 +416,7 @@ cudaError_t colsdot_launch(const double2* v, long long ldv, int n, int ncols, co
 cudaError_t sub_vcoef_launch(const double2* v, long long ldv, int n, int ncols,
                              const double2* coef, double2* r, const int* done, cudaStream_t s) {
   if (ncols <= 0) return cudaSuccess;
+  note_launch();
   sub_vcoef_kernel<<<(n + 127) / 128, 128, 0, s>>>(v, ldv, n, ncols, coef, r, done);
   return cudaGetLastError();
 }
@@ -417,6 +424,7 @@ cudaError_t sub_vcoef_launch(const double2* v, long long ldv, int n, int ncols,
 cudaError_t lanczos_residual_launch(const double2* u, const double2* q, const double2* qprev,
                                     const double* alpha_i, const double* beta_prev, double2* r,
                                     int n, const int* done, cudaStream_t s) {
+  note_launch();
   lanczos_residual_kernel<<<(n + 255) / 256, 256, 0, s>>>(u, q, qprev, alpha_i, beta_prev, r, n,
                                                           done);
   return cudaGetLastError();
@@ -425,6 +433,7 @@ cudaError_t lanczos_residual_launch(const double2* u, const double2* q, const do
 cudaError_t lanczos_advance_launch(const double2* r, const double* beta, double2* qnext,
                                    double* betas_i, LanczosState* st, int i, int k, int n,
                                    cudaStream_t s) {
+  note_launch();
   lanczos_advance_kernel<<<(n + 255) / 256, 256, 0, s>>>(r, beta, qnext, betas_i, st, i, k, n);
   return cudaGetLastError();
 }
@@ -433,6 +442,7 @@ cudaError_t colnorm_residual_launch(const double2* hp, long long ldhp, const dou
                                     long long ldp, const double* lambda, int n, int w,
                                     double* res, cudaStream_t s) {
   if (w <= 0) return cudaSuccess;
+  note_launch();
   colnorm_residual_kernel<<<w, 256, 0, s>>>(hp, ldhp, p, ldp, lambda, n, res);
   return cudaGetLastError();
 }
@@ -445,6 +455,7 @@ cudaError_t colnorm_launch(const double2* x, long long ldx, int n, int w, double
 cudaError_t symmetrize_launch(double2* a, long long lda, int n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   const int nb = (n + TS - 1) / TS;
+  note_launch();
   symmetrize_kernel<<<dim3(nb, nb), dim3(32, 8), 0, s>>>(a, lda, n);
   return cudaGetLastError();
 }
@@ -454,6 +465,7 @@ cudaError_t herm_defect_launch(const double2* a, long long lda, int n, double* o
   cudaError_t e = cudaMemsetAsync(out, 0, 2 * sizeof(double), s);
   if (e != cudaSuccess || n <= 0) return e;
   const int nb = (n + TS - 1) / TS;
+  note_launch();
   herm_defect_kernel<<<dim3(nb, nb), dim3(32, 8), 0, s>>>(
       a, lda, n, reinterpret_cast<unsigned long long*>(out));
   return cudaGetLastError();
@@ -461,12 +473,14 @@ cudaError_t herm_defect_launch(const double2* a, long long lda, int n, double* o
 
 cudaError_t conj_inplace_launch(double2* a, long long lda, int m, int n, cudaStream_t s) {
   if (m <= 0 || n <= 0) return cudaSuccess;
+  note_launch();
   conj_inplace_kernel<<<grid_for((long long)m * n, 256), 256, 0, s>>>(a, lda, m, n);
   return cudaGetLastError();
 }
 
 cudaError_t zero_upper_launch(double2* a, long long lda, int n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
+  note_launch();
   zero_upper_kernel<<<grid_for((long long)n * n, 256), 256, 0, s>>>(a, lda, n);
   return cudaGetLastError();
 }
@@ -474,6 +488,7 @@ cudaError_t zero_upper_launch(double2* a, long long lda, int n, cudaStream_t s) 
 cudaError_t phase_fix_launch(double2* q, long long ldq, int m, int n, const double2* rdiag,
                              cudaStream_t s) {
   if (m <= 0 || n <= 0) return cudaSuccess;
+  note_launch();
   phase_fix_kernel<<<grid_for((long long)m * n, 256), 256, 0, s>>>(q, ldq, m, n, rdiag);
   return cudaGetLastError();
 }
@@ -481,12 +496,14 @@ cudaError_t phase_fix_launch(double2* q, long long ldq, int m, int n, const doub
 cudaError_t extract_diag_launch(const double2* a, long long lda, int n, double2* diag,
                                 cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
+  note_launch();
   extract_diag_kernel<<<(n + 255) / 256, 256, 0, s>>>(a, lda, n, diag);
   return cudaGetLastError();
 }
 
 cudaError_t div_scalar_launch(const double2* x, const double* d, double2* y, int n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
+  note_launch();
   div_scalar_kernel<<<(n + 255) / 256, 256, 0, s>>>(x, d, y, n);
   return cudaGetLastError();
 }
@@ -494,6 +511,7 @@ cudaError_t div_scalar_launch(const double2* x, const double* d, double2* y, int
 cudaError_t copy_cols_launch(const double2* x, long long ldx, double2* y, long long ldy, int m,
                              int n, cudaStream_t s) {
   if (m <= 0 || n <= 0) return cudaSuccess;
+  note_launch();
   copy_cols_kernel<<<grid_for((long long)m * n, 256), 256, 0, s>>>(x, ldx, y, ldy, m, n);
   return cudaGetLastError();
 }

@@ -246,6 +246,7 @@ cudaError_t launch_cfg(const ChebStepParams& p0, int tiles_m, cudaStream_t strea
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  note_launch();
   return cudaLaunchKernelEx(&cfg, kern, p);
 }
 

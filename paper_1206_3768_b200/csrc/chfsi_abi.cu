@@ -4,6 +4,7 @@
 #include <cublas_v2.h>
 #include <cusolverDn.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -14,6 +15,11 @@
 #include "chfsi_internal.h"
 
 using chfsi::LanczosState;
+
+namespace chfsi {
+static std::atomic<long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace chfsi
 
 struct chfsi_ctx {
   int device = 0;
@@ -106,6 +112,8 @@ bool valid_op(char t) { return t == 'N' || t == 'n' || t == 'T' || t == 't' || t
 extern "C" {
 
 int chfsi_version(void) { return 1; }
+
+long long chfsi_launch_count(void) { return chfsi::g_launches.load(std::memory_order_relaxed); }
 
 const char* chfsi_last_error(void) { return g_last_error.c_str(); }
 

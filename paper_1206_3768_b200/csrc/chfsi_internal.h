@@ -6,6 +6,9 @@
 
 namespace chfsi {
 
+// Counts launches of libchfsi's own kernels (chfsi_launch_count()).
+void note_launch();
+
 struct StepTiling {
   int bm;     // 0 = choose automatically
   int bn;

@@ -128,6 +128,10 @@ def sequence_case(cfg_name, vector_labels):
     for label, a, b in iter_baseline_sequence(cfg.n, cfg.length, seed=0):
         out[f"{label}/a_sha"] = np.bytes_(sha(a))
         out[f"{label}/b_sha"] = np.bytes_(sha(b))
+        # host-BLAS-independent fingerprint (the QR/GEMM of the generator
+        # round differently on other CPUs; the GPU box checks these instead)
+        out[f"{label}/a_probe"] = a[::37, ::41].copy()
+        out[f"{label}/b_probe"] = b[::37, ::41].copy()
         t0 = time.perf_counter()
         pencil = sc.EigenPencil(a=a, b=b, label=label)
         sol_full, sp, vals = sc.oracle_solve(pencil, max(cfg.blk + 1, cfg.nev))
