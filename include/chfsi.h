@@ -57,9 +57,10 @@ CHFSI_API long long chfsi_launch_count(void);
 CHFSI_API int chfsi_ctx_create(int device, chfsi_ctx** out);
 CHFSI_API int chfsi_ctx_destroy(chfsi_ctx* ctx);
 CHFSI_API int chfsi_ctx_set_stream(chfsi_ctx* ctx, void* cuda_stream);
-/* Force the K1 tiling (bm=64; bn 32|64; cluster K-split 1|2|4|8) for tests
- * and tuning; bm = 0 restores the automatic choice. */
-CHFSI_API int chfsi_ctx_set_tiling(chfsi_ctx* ctx, int bm, int bn, int split);
+/* Force the K1 tiling for tests and tuning: bm = 64, bn = 16|32|64 columns
+ * per CTA tile, grid = number of persistent CTAs (0 = all resident CTAs;
+ * fewer CTAs exercise other stream-K splits). bm = 0 restores automatic. */
+CHFSI_API int chfsi_ctx_set_tiling(chfsi_ctx* ctx, int bm, int bn, int grid);
 
 /* ---------------------------------------------------------------- K1 ---
  * One fused Chebyshev step (chfsi.py:203 / chfsi.py:206):

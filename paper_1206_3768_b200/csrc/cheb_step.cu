@@ -13,25 +13,35 @@
 // conjugate, so a column-major Hermitian H (cuBLAS/cuSOLVER output) is used
 // as-is. Y blocks are column-major (Y[col*ld + row]). complex128 interleaved.
 //
-// Tiling: CTA tile BM x BN (complex), K in slabs of BK=16 staged through a
-// STAGES-deep cp.async ring in shared memory (pitch padded so the 16-byte
-// fragment loads are bank-conflict free). Thin shapes (small w, small n) are
-// split along K across a thread-block cluster; the partial tiles are summed
-// in FIXED order through distributed shared memory, so the result is
-// bitwise run-to-run reproducible (reference test_chfsi.py:234-241).
-#include <cooperative_groups.h>
+// Schedule: a persistent grid of exactly the resident CTAs (2 per SM) walks
+// a linearised (tile, k-slab) iteration space — whole tiles first
+// ("data-parallel" waves, consecutive CTAs on neighbouring column tiles of
+// one H row panel so the panel is shared through L2), then the remaining
+// tiles split evenly across all CTAs by k-slab ("stream-K"). A tile whose
+// k-range is split is finished by the CTA holding its last slab: it waits
+// for its peers' published partial tiles and sums them in FIXED peer order,
+// so every launch is bitwise reproducible (reference test_chfsi.py:234-241)
+// and no SM idles on a wave tail, whatever (n, w) the locking leaves.
+//
+// Pipeline: K slabs of BK=16 complex staged global->shared with a
+// STAGES-deep cp.async ring; 16-byte chunks XOR-swizzled on row parity so
+// the per-lane 16-byte fragment loads (8 rows x 4 k) are bank-conflict free.
+#include <cstdint>
 
 #include "chfsi_internal.h"
 #include "common.cuh"
 
-namespace cg = cooperative_groups;
-
 namespace chfsi {
 
-constexpr int BK = 16;              // complex elements per K slab
-constexpr int ROWB = BK * 16 + 64;  // smem row pitch (bytes); == 64 mod 128
+namespace {
 
-struct ChebStepParams {
+constexpr int BM = 64;
+constexpr int BK = 16;             // complex elements per K slab
+constexpr int ROWB = BK * 16;      // 256-byte smem rows (swizzled, no padding)
+constexpr int THREADS = 256;       // 8 warps
+constexpr int CTAS_PER_SM = 2;
+
+struct StepParams {
   const double2* h;
   long long ldh;
   const double2* ycur;
@@ -40,16 +50,30 @@ struct ChebStepParams {
   long long ldp;
   double2* ynext;
   long long ldn;
-  int n;        // rows of H and Y, also the contraction length
-  int w;        // columns of Y
-  int tiles_n;  // ceil(w / BN)
-  int k_split;  // contraction extent of one split (multiple of BK)
+  int n, w;
+  int tiles_n;
+  int kiters;          // K slabs per tile
+  int dp_waves;        // whole tiles per CTA before the stream-K part
+  int sk_first;        // first stream-K tile
+  long long sk_iters;  // stream-K iterations (tiles * kiters)
+  int sk_ctas;         // CTAs sharing the stream-K part (<= grid)
   double alpha, c, beta;
-  int read_cur;   // epilogue needs Ycur (c != 0)
-  int read_prev;  // epilogue needs Yprev (beta != 0)
+  int read_cur, read_prev;
+  double* partials;    // [grid][ACC][THREADS]
+  unsigned* flags;     // [grid]
+  unsigned epoch;
 };
 
-__device__ __forceinline__ void epilogue_store(const ChebStepParams& p, int row, int col, double ar,
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void epilogue_store(const StepParams& p, int row, int col, double ar,
                                                double ai) {
   double tr = ar, ti = ai;
   if (p.read_cur) {
@@ -59,112 +83,90 @@ __device__ __forceinline__ void epilogue_store(const ChebStepParams& p, int row,
   }
   tr = dmul(p.alpha, tr);
   ti = dmul(p.alpha, ti);
-  double2* dst = p.ynext + (long long)col * p.ldn + row;
   if (p.read_prev) {
     const double2 yp = p.yprev[(long long)col * p.ldp + row];
     tr = dsub(tr, dmul(p.beta, yp.x));
     ti = dsub(ti, dmul(p.beta, yp.y));
   }
-  *dst = make_double2(tr, ti);
+  p.ynext[(long long)col * p.ldn + row] = make_double2(tr, ti);
 }
 
-template <int BM, int BN, int WM, int WN, int STAGES, bool CONJ, int SPLIT>
-__global__ void __launch_bounds__(WM* WN * 32, 1) cheb_step_kernel(const ChebStepParams p) {
-  constexpr int THREADS = WM * WN * 32;
+// byte offset of 16-byte chunk `kk` of smem row `r` (row-parity XOR swizzle)
+__device__ __forceinline__ int swz(int r, int kk) { return r * ROWB + ((kk ^ ((r & 1) << 2)) << 4); }
+
+template <int BN, int WM, int WN, int STAGES, bool CONJ>
+__global__ void __launch_bounds__(THREADS, CTAS_PER_SM) cheb_step_kernel(const StepParams p) {
   constexpr int TM = BM / WM, TN = BN / WN;
   constexpr int MI = TM / 8, NI = TN / 8;
+  constexpr int ACC = MI * NI * 4;
   constexpr int STAGE_BYTES = (BM + BN) * ROWB;
+  static_assert(WM * WN * 32 == THREADS, "8 warps");
   static_assert(MI >= 1 && NI >= 1, "warp tile too small");
-  static_assert(SPLIT == 1 || BM % SPLIT == 0, "split must divide BM");
   extern __shared__ __align__(128) unsigned char smem[];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp / WN, wn = warp % WN;
-  const int tile = blockIdx.x / SPLIT;
-  const int split = blockIdx.x % SPLIT;
-  const int tm = tile / p.tiles_n, tn = tile % p.tiles_n;
-  const int m0 = tm * BM, n0 = tn * BN;
-  const int kbeg = split * p.k_split;
-  const int kend = min(p.n, kbeg + p.k_split);
-  const int nslab = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+  const int G = gridDim.x, cta = blockIdx.x;
 
-  double cr[MI][NI][2], ci[MI][NI][2];
-#pragma unroll
-  for (int i = 0; i < MI; ++i)
-#pragma unroll
-    for (int j = 0; j < NI; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+  // ---- this CTA's slice of the linearised iteration space
+  const int dp_iters = p.dp_waves * p.kiters;
+  long long sb = 0, se = 0;
+  if (cta < p.sk_ctas) {
+    sb = (long long)cta * p.sk_iters / p.sk_ctas;
+    se = (long long)(cta + 1) * p.sk_iters / p.sk_ctas;
+  }
+  const int total = dp_iters + (int)(se - sb);
+  if (total == 0) return;
 
-  auto load_slab = [&](int slab, int stage) {
+  auto locate = [&](int j, int& tile, int& kk) {
+    if (j < dp_iters) {
+      tile = cta + (j / p.kiters) * G;
+      kk = j % p.kiters;
+    } else {
+      const long long s = sb + (j - dp_iters);
+      tile = p.sk_first + (int)(s / p.kiters);
+      kk = (int)(s % p.kiters);
+    }
+  };
+
+  auto load_iter = [&](int j, int stage) {
+    int tile, kk;
+    locate(j, tile, kk);
+    const int m0 = (tile / p.tiles_n) * BM, n0 = (tile % p.tiles_n) * BN;
+    const int k0 = kk * BK;
     unsigned char* sa = smem + stage * STAGE_BYTES;
-    unsigned char* sb = sa + BM * ROWB;
-    const int k0 = kbeg + slab * BK;
+    unsigned char* sb_ = sa + BM * ROWB;
 #pragma unroll
-    for (int it = 0; it < (BM * BK + THREADS - 1) / THREADS; ++it) {
+    for (int it = 0; it < (BM * BK) / THREADS; ++it) {
       const int id = tid + it * THREADS;
-      if (id < BM * BK) {
-        const int r = id / BK, kk = id % BK;
-        const int gm = m0 + r, gk = k0 + kk;
-        const bool ok = gm < p.n && gk < kend;
-        cp_async16(sa + r * ROWB + kk * 16, ok ? p.h + (long long)gm * p.ldh + gk : p.h, ok);
-      }
+      const int r = id / BK, c16 = id % BK;
+      const int gm = m0 + r, gk = k0 + c16;
+      const bool ok = gm < p.n && gk < p.n;
+      cp_async16(sa + swz(r, c16), ok ? p.h + (long long)gm * p.ldh + gk : p.h, ok);
     }
 #pragma unroll
     for (int it = 0; it < (BN * BK + THREADS - 1) / THREADS; ++it) {
       const int id = tid + it * THREADS;
-      if (id < BN * BK) {
-        const int r = id / BK, kk = id % BK;
-        const int gn = n0 + r, gk = k0 + kk;
-        const bool ok = gn < p.w && gk < kend;
-        cp_async16(sb + r * ROWB + kk * 16, ok ? p.ycur + (long long)gn * p.ldc + gk : p.ycur, ok);
+      if ((BN * BK) % THREADS == 0 || id < BN * BK) {
+        const int r = id / BK, c16 = id % BK;
+        const int gn = n0 + r, gk = k0 + c16;
+        const bool ok = gn < p.w && gk < p.n;
+        cp_async16(sb_ + swz(r, c16), ok ? p.ycur + (long long)gn * p.ldc + gk : p.ycur, ok);
       }
     }
   };
 
+  double acc[MI][NI][4];  // [.][.][0..1] real, [2..3] imag of C[g][2t+e]
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nslab) load_slab(s, s);
-    cp_async_commit();
-  }
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NI; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
 
-  for (int slab = 0; slab < nslab; ++slab) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    const int nxt = slab + STAGES - 1;
-    if (nxt < nslab) load_slab(nxt, nxt % STAGES);
-    cp_async_commit();
-
-    const unsigned char* sa = smem + (slab % STAGES) * STAGE_BYTES + (wm * TM + g) * ROWB + t * 16;
-    const unsigned char* sb = smem + (slab % STAGES) * STAGE_BYTES + BM * ROWB + (wn * TN + g) * ROWB + t * 16;
-#pragma unroll
-    for (int k4 = 0; k4 < BK / 4; ++k4) {
-      double2 a[MI], b[NI];
-#pragma unroll
-      for (int i = 0; i < MI; ++i) a[i] = lds128(sa + i * 8 * ROWB + k4 * 64);
-#pragma unroll
-      for (int j = 0; j < NI; ++j) b[j] = lds128(sb + j * 8 * ROWB + k4 * 64);
-      // Re/Im of (a or conj(a)) * b: four real DMMAs per complex 8x8x4 block.
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < NI; ++j) {
-          dmma884(cr[i][j], a[i].x, b[j].x);
-          dmma884(ci[i][j], a[i].x, b[j].y);
-        }
-#pragma unroll
-      for (int i = 0; i < MI; ++i) {
-        const double ai = a[i].y, nai = -a[i].y;
-#pragma unroll
-        for (int j = 0; j < NI; ++j) {
-          dmma884(cr[i][j], CONJ ? ai : nai, b[j].y);
-          dmma884(ci[i][j], CONJ ? nai : ai, b[j].x);
-        }
-      }
-    }
-  }
-  cp_async_wait<0>();
-
-  if constexpr (SPLIT == 1) {
+  auto epilogue = [&](int tile) {
+    const int m0 = (tile / p.tiles_n) * BM, n0 = (tile % p.tiles_n) * BN;
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -173,131 +175,184 @@ __global__ void __launch_bounds__(WM* WN * 32, 1) cheb_step_kernel(const ChebSte
         for (int e = 0; e < 2; ++e) {
           const int row = m0 + wm * TM + i * 8 + g;
           const int col = n0 + wn * TN + j * 8 + 2 * t + e;
-          if (row < p.n && col < p.w) epilogue_store(p, row, col, cr[i][j][e], ci[i][j][e]);
+          if (row < p.n && col < p.w) epilogue_store(p, row, col, acc[i][j][e], acc[i][j][2 + e]);
         }
-  } else {
-    // Deterministic split-K: stage the partial tile column-major in this
-    // CTA's smem, then CTA r of the cluster sums rows [r*BM/S, (r+1)*BM/S)
-    // over ranks 0..S-1 in order and applies the epilogue.
-    constexpr int RP = BM + 2;  // column pitch (complex) of the partial tile
-    static_assert(BN * RP * 16 <= STAGES * STAGE_BYTES, "partial tile does not fit");
-    cg::cluster_group cluster = cg::this_cluster();
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < total) load_iter(s, s);
+    cp_async_commit();
+  }
+
+  const int arow = (wm * TM + g), brow = (wn * TN + g);
+  for (int j = 0; j < total; ++j) {
+    cp_async_wait<STAGES - 2>();
     __syncthreads();
-    double2* red = reinterpret_cast<double2*>(smem);
+    if (j + STAGES - 1 < total) load_iter(j + STAGES - 1, (j + STAGES - 1) % STAGES);
+    cp_async_commit();
+
+    const unsigned char* sa = smem + (j % STAGES) * STAGE_BYTES;
+    const unsigned char* sbm = sa + BM * ROWB;
+#pragma unroll
+    for (int k4 = 0; k4 < BK / 4; ++k4) {
+      double2 a[MI], b[NI];
+#pragma unroll
+      for (int i = 0; i < MI; ++i) a[i] = lds128(sa + swz(arow + i * 8, k4 * 4 + t));
+#pragma unroll
+      for (int jj = 0; jj < NI; ++jj) b[jj] = lds128(sbm + swz(brow + jj * 8, k4 * 4 + t));
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int jj = 0; jj < NI; ++jj) {
+          double(&cr)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][0]);
+          double(&ci)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][2]);
+          dmma884(cr, a[i].x, b[jj].x);
+          dmma884(ci, a[i].x, b[jj].y);
+        }
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        const double ai = a[i].y, nai = -a[i].y;
+#pragma unroll
+        for (int jj = 0; jj < NI; ++jj) {
+          double(&cr)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][0]);
+          double(&ci)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][2]);
+          dmma884(cr, CONJ ? ai : nai, b[jj].y);
+          dmma884(ci, CONJ ? nai : ai, b[jj].x);
+        }
+      }
+    }
+
+    // ---- end of a tile segment?
+    int tile, kk;
+    locate(j, tile, kk);
+    const bool tile_end = kk == p.kiters - 1;
+    if (!tile_end && j != total - 1) continue;
+    if (j < dp_iters) {
+      epilogue(tile);
+    } else {
+      const long long s = sb + (j - dp_iters);
+      const long long tile_s0 = (s / p.kiters) * p.kiters;  // first SK iteration of the tile
+      const bool whole = tile_end && (tile_s0 >= sb);
+      if (whole) {
+        epilogue(tile);
+      } else if (tile_end) {
+        // owner: peers are the CTAs whose ranges hold [tile_s0, sb)
+        const int first = (int)(((tile_s0 + 1) * p.sk_ctas + p.sk_iters - 1) / p.sk_iters) - 1;
+        if (tid == 0) {
+          for (int q = first; q < cta; ++q)
+            while (ld_acquire(p.flags + q) != p.epoch) __nanosleep(64);
+        }
+        __syncthreads();
+        // fixed fold order: own partial, then peers first..cta-1
+        for (int q = first; q < cta; ++q) {
+          const double* src = p.partials + (size_t)q * ACC * THREADS + tid;
+#pragma unroll
+          for (int i = 0; i < MI; ++i)
+#pragma unroll
+            for (int jj = 0; jj < NI; ++jj)
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                acc[i][jj][e] = dadd(acc[i][jj][e], __ldcg(src + ((i * NI + jj) * 4 + e) * THREADS));
+        }
+        epilogue(tile);
+      } else {
+        // non-owner: publish this CTA's partial of its last tile
+        double* dst = p.partials + (size_t)cta * ACC * THREADS + tid;
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int jj = 0; jj < NI; ++jj)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) __stcg(dst + ((i * NI + jj) * 4 + e) * THREADS, acc[i][jj][e]);
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) st_release(p.flags + cta, p.epoch);
+      }
+    }
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
-      for (int j = 0; j < NI; ++j)
+      for (int jj = 0; jj < NI; ++jj)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = wm * TM + i * 8 + g;
-          const int cidx = wn * TN + j * 8 + 2 * t + e;
-          red[cidx * RP + r] = make_double2(cr[i][j][e], ci[i][j][e]);
-        }
-    cluster.sync();
-    const int rank = static_cast<int>(cluster.block_rank());
-    constexpr int RPER = BM / SPLIT;
-    for (int idx = tid; idx < RPER * BN; idx += THREADS) {
-      const int rr = rank * RPER + idx % RPER, cc = idx / RPER;
-      const int row = m0 + rr, col = n0 + cc;
-      double sr = 0.0, si = 0.0;
-#pragma unroll
-      for (int q = 0; q < SPLIT; ++q) {
-        const double2* rem = cluster.map_shared_rank(red, q);
-        const double2 v = rem[cc * RP + rr];
-        sr = dadd(sr, v.x);
-        si = dadd(si, v.y);
-      }
-      if (row < p.n && col < p.w) epilogue_store(p, row, col, sr, si);
-    }
-    cluster.sync();
+        for (int e = 0; e < 4; ++e) acc[i][jj][e] = 0.0;
   }
+  cp_async_wait<0>();
 }
 
-// ------------------------------------------------------------------ host ---
+// --------------------------------------------------------------- host ---
 
-namespace {
+struct Variant {
+  const void* fn;
+  int smem;
+  int resident;  // CTAs per SM actually achievable
+  int acc;       // doubles per thread in a partial tile
+};
 
-template <int BM, int BN, int WM, int WN, int STAGES, bool CONJ, int SPLIT>
-cudaError_t launch_cfg(const ChebStepParams& p0, int tiles_m, cudaStream_t stream) {
-  constexpr int THREADS = WM * WN * 32;
-  constexpr int SMEM = STAGES * (BM + BN) * ROWB;
-  auto kern = cheb_step_kernel<BM, BN, WM, WN, STAGES, CONJ, SPLIT>;
-  static bool attr_set = false;  // per template instance
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  ChebStepParams p = p0;
-  p.tiles_n = (p.w + BN - 1) / BN;
-  const int kper = (p.n + SPLIT - 1) / SPLIT;
-  p.k_split = ((kper + BK - 1) / BK) * BK;
-  const int ctas = tiles_m * p.tiles_n * SPLIT;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(ctas, 1, 1);
-  cfg.blockDim = dim3(THREADS, 1, 1);
-  cfg.dynamicSmemBytes = SMEM;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = SPLIT;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  note_launch();
-  return cudaLaunchKernelEx(&cfg, kern, p);
+template <int BN, int WM, int WN, int STAGES, bool CONJ>
+Variant make_variant() {
+  Variant v{};
+  auto fn = cheb_step_kernel<BN, WM, WN, STAGES, CONJ>;
+  v.fn = reinterpret_cast<const void*>(fn);
+  v.smem = STAGES * (BM + BN) * ROWB;
+  v.acc = (BM / WM / 8) * (BN / WN / 8) * 4;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, THREADS, v.smem);
+  v.resident = occ > 0 ? occ : 1;
+  return v;
 }
 
-template <int BM, int BN, int WM, int WN, int STAGES, bool CONJ>
-cudaError_t launch_split(const ChebStepParams& p, int split, cudaStream_t s) {
-  const int tiles_m = (p.n + BM - 1) / BM;
-  switch (split) {
-    case 1: return launch_cfg<BM, BN, WM, WN, STAGES, CONJ, 1>(p, tiles_m, s);
-    case 2: return launch_cfg<BM, BN, WM, WN, STAGES, CONJ, 2>(p, tiles_m, s);
-    case 4: return launch_cfg<BM, BN, WM, WN, STAGES, CONJ, 4>(p, tiles_m, s);
-    case 8: return launch_cfg<BM, BN, WM, WN, STAGES, CONJ, 8>(p, tiles_m, s);
-    default: return cudaErrorInvalidValue;
-  }
-}
-
-// Modelled cost (in MAC-slab units) of one launch: waves x per-CTA work,
-// plus the fixed pipeline fill and the split reduction.
-double model_cost(int n, int w, int bm, int bn, int split) {
-  const long long tiles = (long long)((n + bm - 1) / bm) * ((w + bn - 1) / bn);
-  const long long ctas = tiles * split;
-  const long long waves = (ctas + kNumSMs - 1) / kNumSMs;
-  const int kper = (((n + split - 1) / split + BK - 1) / BK) * BK;
-  const double per_cta = (double)bm * bn * (kper + 3.0 * BK) + (split > 1 ? 4.0 * bm * bn * split : 0.0);
-  return waves * per_cta;
+const Variant& variant(int bn, bool conj) {
+  // function-local statics: initialised once, on first use (device set by caller)
+  static const Variant v16 = make_variant<16, 8, 1, 4, false>();
+  static const Variant v16c = make_variant<16, 8, 1, 4, true>();
+  static const Variant v32 = make_variant<32, 4, 2, 4, false>();
+  static const Variant v32c = make_variant<32, 4, 2, 4, true>();
+  static const Variant v64 = make_variant<64, 2, 4, 3, false>();
+  static const Variant v64c = make_variant<64, 2, 4, 3, true>();
+  if (bn == 16) return conj ? v16c : v16;
+  if (bn == 32) return conj ? v32c : v32;
+  return conj ? v64c : v64;
 }
 
 }  // namespace
 
 StepTiling choose_step_tiling(int n, int w) {
-  StepTiling best{64, 64, 1};
+  // least padded work, mild preference for wider tiles (operand reuse)
+  const int bns[3] = {64, 32, 16};
+  const double pen[3] = {1.0, 1.03, 1.10};
+  StepTiling best{BM, 64, 0};
   double best_cost = 1e300;
-  const int bns[2] = {64, 32};
-  const int splits[4] = {1, 2, 4, 8};
-  for (int bn : bns)
-    for (int s : splits) {
-      if (s > 1 && (n + s - 1) / s < 2 * BK) continue;
-      const double c = model_cost(n, w, 64, bn, s) * (bn == 32 ? 1.04 : 1.0);
-      if (c < best_cost) {
-        best_cost = c;
-        best = StepTiling{64, bn, s};
-      }
+  for (int i = 0; i < 3; ++i) {
+    const double padded = (double)((w + bns[i] - 1) / bns[i]) * bns[i];
+    const double cost = padded * pen[i];
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = StepTiling{BM, bns[i], 0};
     }
+  }
+  (void)n;
   return best;
 }
+
+size_t step_workspace_doubles(int max_grid) { return (size_t)max_grid * 64 * THREADS; }
+
+int step_grid_size(int bn, bool conj) { return variant(bn, conj).resident * kNumSMs; }
 
 cudaError_t cheb_step_launch(const double2* h, long long ldh, bool conj_h, const double2* ycur,
                              long long ldc, const double2* yprev, long long ldp, double2* ynext,
                              long long ldn, int n, int w, double alpha, double c, double beta,
-                             StepTiling tiling, cudaStream_t stream) {
+                             StepTiling tiling, const StepWorkspace& ws, cudaStream_t stream) {
   if (n <= 0 || w <= 0) return cudaSuccess;
-  ChebStepParams p{};
+  if (tiling.bm == 0) tiling = choose_step_tiling(n, w);
+  if (tiling.bn != 16 && tiling.bn != 32 && tiling.bn != 64) return cudaErrorInvalidValue;
+  const Variant& v = variant(tiling.bn, conj_h);
+  int grid = v.resident * kNumSMs;
+  if (tiling.split > 0 && tiling.split < grid) grid = tiling.split;  // test/tuning override
+  if (grid > ws.max_grid) return cudaErrorInvalidValue;
+
+  StepParams p{};
   p.h = h;
   p.ldh = ldh;
   p.ycur = ycur;
@@ -308,20 +363,25 @@ cudaError_t cheb_step_launch(const double2* h, long long ldh, bool conj_h, const
   p.ldn = ldn;
   p.n = n;
   p.w = w;
+  p.tiles_n = (w + tiling.bn - 1) / tiling.bn;
+  const int tiles_m = (n + BM - 1) / BM;
+  const long long tiles = (long long)tiles_m * p.tiles_n;
+  p.kiters = (n + BK - 1) / BK;
+  p.dp_waves = tiles >= 2LL * grid ? (int)(tiles / grid) - 1 : 0;
+  p.sk_first = p.dp_waves * grid;
+  p.sk_iters = (tiles - p.sk_first) * p.kiters;
+  p.sk_ctas = (int)(p.sk_iters < grid ? p.sk_iters : grid);
   p.alpha = alpha;
   p.c = c;
   p.beta = beta;
   p.read_cur = c != 0.0;
   p.read_prev = (beta != 0.0) && yprev != nullptr;
-  if (tiling.bm == 0) tiling = choose_step_tiling(n, w);
-  if (tiling.bm != 64) return cudaErrorInvalidValue;
-  if (tiling.bn == 64)
-    return conj_h ? launch_split<64, 64, 2, 4, 4, true>(p, tiling.split, stream)
-                  : launch_split<64, 64, 2, 4, 4, false>(p, tiling.split, stream);
-  if (tiling.bn == 32)
-    return conj_h ? launch_split<64, 32, 4, 2, 4, true>(p, tiling.split, stream)
-                  : launch_split<64, 32, 4, 2, 4, false>(p, tiling.split, stream);
-  return cudaErrorInvalidValue;
+  p.partials = ws.partials;
+  p.flags = ws.flags;
+  p.epoch = ++*ws.epoch;
+  void* args[] = {&p};
+  note_launch();
+  return cudaLaunchKernel(v.fn, dim3(grid), dim3(THREADS), args, v.smem, stream);
 }
 
 }  // namespace chfsi

@@ -35,6 +35,8 @@ struct chfsi_ctx {
   int* dinfo = nullptr;
   LanczosState* lstate = nullptr;
   chfsi::StepTiling tiling{0, 0, 0};  // K1 tile override (bm == 0: automatic)
+  chfsi::StepWorkspace step_ws{nullptr, nullptr, nullptr, 0};
+  unsigned step_epoch = 0;
 };
 
 namespace {
@@ -140,6 +142,13 @@ int chfsi_ctx_create(int device, chfsi_ctx** out) {
   CK_CUDA(cudaMalloc(&ctx->scalars, 16 * sizeof(double)));
   CK_CUDA(cudaMalloc(&ctx->dinfo, 4 * sizeof(int)));
   CK_CUDA(cudaMalloc(&ctx->lstate, sizeof(LanczosState)));
+  // K1 stream-K scratch: partial tiles and ready flags for every resident CTA
+  ctx->step_ws.max_grid = chfsi::kNumSMs * 4;
+  CK_CUDA(cudaMalloc(&ctx->step_ws.partials,
+                     chfsi::step_workspace_doubles(ctx->step_ws.max_grid) * sizeof(double)));
+  CK_CUDA(cudaMalloc(&ctx->step_ws.flags, ctx->step_ws.max_grid * sizeof(unsigned)));
+  CK_CUDA(cudaMemset(ctx->step_ws.flags, 0, ctx->step_ws.max_grid * sizeof(unsigned)));
+  ctx->step_ws.epoch = &ctx->step_epoch;
   *out = ctx;
   return CHFSI_OK;
 }
@@ -157,6 +166,8 @@ int chfsi_ctx_destroy(chfsi_ctx* ctx) {
   cudaFree(ctx->scalars);
   cudaFree(ctx->dinfo);
   cudaFree(ctx->lstate);
+  cudaFree(ctx->step_ws.partials);
+  cudaFree(ctx->step_ws.flags);
   delete ctx;
   return CHFSI_OK;
 }
@@ -167,7 +178,8 @@ int chfsi_ctx_set_tiling(chfsi_ctx* ctx, int bm, int bn, int split) {
     ctx->tiling = chfsi::StepTiling{0, 0, 0};
     return CHFSI_OK;
   }
-  CK_ARG(bm == 64 && (bn == 32 || bn == 64) && (split == 1 || split == 2 || split == 4 || split == 8),
+  CK_ARG(bm == 64 && (bn == 16 || bn == 32 || bn == 64) && split >= 0 &&
+             split <= ctx->step_ws.max_grid,
          "unsupported K1 tiling");
   ctx->tiling = chfsi::StepTiling{bm, bn, split};
   return CHFSI_OK;
@@ -196,7 +208,7 @@ int chfsi_cheb_step_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh
                                   static_cast<const double2*>(ycur), ldc,
                                   static_cast<const double2*>(yprev), ldp,
                                   static_cast<double2*>(ynext), ldn, n, w, alpha, c, beta,
-                                  ctx->tiling, ctx->stream));
+                                  ctx->tiling, ctx->step_ws, ctx->stream));
   return CHFSI_OK;
 }
 
@@ -244,7 +256,7 @@ int chfsi_filter_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, i
   for (int j = 0; j < deg; ++j) {
     double2* dst = static_cast<double2*>((j % 2 == 0) ? buf_a : buf_b);
     CK_CUDA(chfsi::cheb_step_launch(hh, ldh, conj_h != 0, cur, ldcur, prev, ldp, dst, ldb, n, w,
-                                    al[j], c, be[j], tiling, ctx->stream));
+                                    al[j], c, be[j], tiling, ctx->step_ws, ctx->stream));
     prev = cur;
     ldp = ldcur;
     cur = dst;

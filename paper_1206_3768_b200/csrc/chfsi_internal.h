@@ -10,19 +10,29 @@ namespace chfsi {
 void note_launch();
 
 struct StepTiling {
-  int bm;     // 0 = choose automatically
-  int bn;
-  int split;  // K split across a thread-block cluster (1, 2, 4, 8)
+  int bm;     // 0 = choose automatically (bm is always 64)
+  int bn;     // 16, 32 or 64 columns per CTA tile
+  int split;  // grid override for tests/tuning (0 = all resident CTAs)
+};
+
+// Stream-K scratch owned by the context: partial tiles + ready flags.
+struct StepWorkspace {
+  double* partials;
+  unsigned* flags;
+  unsigned* epoch;  // host-side launch counter (flag generation)
+  int max_grid;
 };
 
 StepTiling choose_step_tiling(int n, int w);
+size_t step_workspace_doubles(int max_grid);
+int step_grid_size(int bn, bool conj);
 
 // K1: Ynext = alpha*(op(H) Ycur - c Ycur) - beta Yprev; Yprev may alias Ynext
 // (or be null when beta == 0). op(H) = H (row-major read) or conj(H).
 cudaError_t cheb_step_launch(const double2* h, long long ldh, bool conj_h, const double2* ycur,
                              long long ldc, const double2* yprev, long long ldp, double2* ynext,
                              long long ldn, int n, int w, double alpha, double c, double beta,
-                             StepTiling tiling, cudaStream_t stream);
+                             StepTiling tiling, const StepWorkspace& ws, cudaStream_t stream);
 
 // ---- auxiliary kernels (aux_kernels.cu) ----
 // u = op(H) q for a row-major H (conj_h: conj(H)).

@@ -70,8 +70,10 @@ def fb(x):
     return to_fblock(x, copy=True)
 
 
-TILINGS = [(64, 64, 1), (64, 64, 2), (64, 64, 4), (64, 64, 8), (64, 32, 1), (64, 32, 4),
-           (64, 32, 8)]
+# (bm, bn, grid): grid 0 = every resident CTA; small grids force other
+# data-parallel / stream-K splits and multi-peer fix-ups
+TILINGS = [(64, 64, 0), (64, 32, 0), (64, 16, 0), (64, 64, 1), (64, 32, 7), (64, 16, 13),
+           (64, 64, 150), (64, 32, 296)]
 
 
 @pytest.mark.parametrize("tiling", TILINGS)
