@@ -6,6 +6,8 @@
 
 namespace chfsi {
 
+constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
+
 // Counts launches of libchfsi's own kernels (chfsi_launch_count()).
 void note_launch();
 

@@ -6,7 +6,7 @@
 
 namespace chfsi {
 
-constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
+
 
 // ---- cp.async (LDGSTS): 16-byte global->shared copy with zero fill -------
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
