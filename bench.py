@@ -294,7 +294,12 @@ def run_ours(args):
         traffic = json.load(open(K1_TRAFFIC_FILE)).get(args.config)
     per_problem = [{"label": r.label, "loops": r.report.inner_loops, "matvecs": r.report.matvecs,
                     "filtered": r.report.filtered_vectors, "converged": r.report.converged,
-                    "t_solve_ms": round(r.t_solve * 1e3, 3)} for r in results[-1]]
+                    "t_solve_ms": round(r.t_solve * 1e3, 3),
+                    "t_reduce_ms": round(r.t_reduce * 1e3, 3),
+                    "t_back_ms": round(r.t_back * 1e3, 3),
+                    "dev_ms": {k: round(getattr(r.report, "t_" + k) * 1e3, 3)
+                               for k in ("lanczos", "filter", "ortho", "rr")}}
+                   for r in results[-1]]
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3,

@@ -118,16 +118,30 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) cheb_step_kernel(const S
   }
   const int total = dp_iters + (int)(se - sb);
   if (total == 0) return;
+  // If the range ends inside a tile, that head-of-tile segment is a partial
+  // another CTA (the tile's owner) will consume: compute and publish it
+  // FIRST, so owners never wait on a chain of peers. Local order:
+  //   [publish segment] [data-parallel tiles] [rest of the stream-K range]
+  int pub = 0;
+  if (se > sb && (se % p.kiters) != 0) {
+    const long long head = ((se - 1) / p.kiters) * p.kiters;
+    pub = (int)(se - (head > sb ? head : sb));
+  }
 
   auto locate = [&](int j, int& tile, int& kk) {
-    if (j < dp_iters) {
-      tile = cta + (j / p.kiters) * G;
-      kk = j % p.kiters;
+    long long s;
+    if (j < pub) {
+      s = se - pub + j;
+    } else if (j < pub + dp_iters) {
+      const int d = j - pub;
+      tile = cta + (d / p.kiters) * G;
+      kk = d % p.kiters;
+      return;
     } else {
-      const long long s = sb + (j - dp_iters);
-      tile = p.sk_first + (int)(s / p.kiters);
-      kk = (int)(s % p.kiters);
+      s = sb + (j - pub - dp_iters);
     }
+    tile = p.sk_first + (int)(s / p.kiters);
+    kk = (int)(s % p.kiters);
   };
 
   auto load_iter = [&](int j, int stage) {
@@ -227,16 +241,28 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) cheb_step_kernel(const S
     int tile, kk;
     locate(j, tile, kk);
     const bool tile_end = kk == p.kiters - 1;
-    if (!tile_end && j != total - 1) continue;
-    if (j < dp_iters) {
+    const bool pub_end = pub > 0 && j == pub - 1;
+    if (!tile_end && !pub_end) continue;
+    if (pub_end) {
+      // non-owner: publish the partial head of this CTA's last tile
+      double* dst = p.partials + (size_t)cta * ACC * THREADS + tid;
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int jj = 0; jj < NI; ++jj)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) __stcg(dst + ((i * NI + jj) * 4 + e) * THREADS, acc[i][jj][e]);
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) st_release(p.flags + cta, p.epoch);
+    } else if (j < pub + dp_iters) {
       epilogue(tile);
     } else {
-      const long long s = sb + (j - dp_iters);
+      const long long s = sb + (j - pub - dp_iters);
       const long long tile_s0 = (s / p.kiters) * p.kiters;  // first SK iteration of the tile
-      const bool whole = tile_end && (tile_s0 >= sb);
-      if (whole) {
+      if (tile_s0 >= sb) {
         epilogue(tile);
-      } else if (tile_end) {
+      } else {
         // owner: peers are the CTAs whose ranges hold [tile_s0, sb)
         const int first = (int)(((tile_s0 + 1) * p.sk_ctas + p.sk_iters - 1) / p.sk_iters) - 1;
         if (tid == 0) {
@@ -256,18 +282,6 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) cheb_step_kernel(const S
                 acc[i][jj][e] = dadd(acc[i][jj][e], __ldcg(src + ((i * NI + jj) * 4 + e) * THREADS));
         }
         epilogue(tile);
-      } else {
-        // non-owner: publish this CTA's partial of its last tile
-        double* dst = p.partials + (size_t)cta * ACC * THREADS + tid;
-#pragma unroll
-        for (int i = 0; i < MI; ++i)
-#pragma unroll
-          for (int jj = 0; jj < NI; ++jj)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) __stcg(dst + ((i * NI + jj) * 4 + e) * THREADS, acc[i][jj][e]);
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) st_release(p.flags + cta, p.epoch);
       }
     }
 #pragma unroll
