@@ -33,9 +33,8 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
-import tempfile
+import threading
 import time
 
 import numpy as np
@@ -60,57 +59,66 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=2, help="problems in the CPU sample")
+    ap.add_argument("--no-clocks", action="store_true", help="diagnostics: no clock sampler")
     return ap.parse_args()
 
 
 # ------------------------------------------------------------------ clocks ---
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region."""
+    """SM clock / throttle-reason sampling during the timed region (the
+    nvidia-smi clocks line of B200_PROFILING.md, read through NVML from a
+    background thread every 200 ms — the same counters without spawning
+    nvidia-smi, whose queries stall kernel launches)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown")
+    REASONS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+               "hw_thermal_slowdown": 0x40, "hw_power_brake": 0x80}
 
-    def __init__(self, index):
+    def __init__(self, index, period=0.2):
         self.index = index
-        self.proc = None
-        self.path = None
+        self.period = period
+        self.rows = []
+        self.thread = None
+        self.stop_evt = threading.Event()
+
+    def _run(self):
+        import pynvml as nv
+
+        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop_evt.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((sm, smax, pw, rs))
+            except Exception:  # noqa: BLE001 - sampling must never break the bench
+                pass
+            self.stop_evt.wait(self.period)
 
     def start(self):
-        fd, self.path = tempfile.mkstemp(suffix=".csv")
-        os.close(fd)
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except OSError:
-            self.proc = None
+            import pynvml as nv
+
+            nv.nvmlInit()
+        except Exception:  # noqa: BLE001
+            return
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
 
     def stop(self):
-        if self.proc is None:
+        if self.thread is None:
             return None
-        self.proc.terminate()
-        self.proc.wait(timeout=10)
-        rows = []
-        for line in open(self.path):
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                rows.append((float(parts[0]), float(parts[1]), float(parts[2]), parts[3:7]))
-            except ValueError:
-                continue
-        os.unlink(self.path)
+        self.stop_evt.set()
+        self.thread.join(timeout=5)
+        rows = self.rows
         if not rows:
             return None
-        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
-        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[3]) if v == "Active"})
+        reasons = sorted({k for r in rows for k, bit in self.REASONS.items() if r[3] & bit})
         loaded = [r[0] for r in rows if r[2] > 250.0] or [r[0] for r in rows]
         return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(r[1] for r in rows),
                 "reasons": reasons, "samples": len(rows),
-                "power_w_max": max(r[2] for r in rows)}
+                "power_w_max": max(r[2] for r in rows), "source": "NVML, 200 ms"}
 
 
 # ------------------------------------------------------------------ inputs ---
@@ -225,7 +233,8 @@ def run_ours(args):
         device_step()
     barrier()
     clocks = ClockSampler(local)
-    clocks.start()
+    if not args.no_clocks:
+        clocks.start()
     lc0 = _lib.lib().chfsi_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
