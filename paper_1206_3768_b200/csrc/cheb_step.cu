@@ -108,65 +108,83 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) cheb_step_kernel(const S
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp / WN, wn = warp % WN;
   const int G = gridDim.x, cta = blockIdx.x;
+  const int kiters = p.kiters;
 
-  // ---- this CTA's slice of the linearised iteration space
-  const int dp_iters = p.dp_waves * p.kiters;
-  long long sb = 0, se = 0;
+  // ---- this CTA's slice of the linearised iteration space (64-bit once)
+  const int dp_iters = p.dp_waves * kiters;
+  int sb = 0, se = 0;
   if (cta < p.sk_ctas) {
-    sb = (long long)cta * p.sk_iters / p.sk_ctas;
-    se = (long long)(cta + 1) * p.sk_iters / p.sk_ctas;
+    sb = (int)((long long)cta * p.sk_iters / p.sk_ctas);
+    se = (int)((long long)(cta + 1) * p.sk_iters / p.sk_ctas);
   }
-  const int total = dp_iters + (int)(se - sb);
+  const int total = dp_iters + (se - sb);
   if (total == 0) return;
   // If the range ends inside a tile, that head-of-tile segment is a partial
-  // another CTA (the tile's owner) will consume: compute and publish it
+  // the tile's owner (a later CTA) will consume: compute and publish it
   // FIRST, so owners never wait on a chain of peers. Local order:
   //   [publish segment] [data-parallel tiles] [rest of the stream-K range]
   int pub = 0;
-  if (se > sb && (se % p.kiters) != 0) {
-    const long long head = ((se - 1) / p.kiters) * p.kiters;
-    pub = (int)(se - (head > sb ? head : sb));
+  if (se > sb && (se % kiters) != 0) {
+    const int head = ((se - 1) / kiters) * kiters;
+    pub = se - (head > sb ? head : sb);
   }
+  const int sk_tile0 = p.sk_first + sb / kiters, sk_kk0 = sb % kiters;
 
-  auto locate = [&](int j, int& tile, int& kk) {
-    long long s;
-    if (j < pub) {
-      s = se - pub + j;
-    } else if (j < pub + dp_iters) {
-      const int d = j - pub;
-      tile = cta + (d / p.kiters) * G;
-      kk = d % p.kiters;
-      return;
+  // Cursor over that order; advanced incrementally (no per-slab division).
+  struct Cursor {
+    int j, tile, kk, m0, n0;
+  };
+  auto set_tile = [&](Cursor& c, int tile, int kk) {
+    c.tile = tile;
+    c.kk = kk;
+    c.m0 = (tile / p.tiles_n) * BM;
+    c.n0 = (tile % p.tiles_n) * BN;
+  };
+  auto start = [&](Cursor& c) {
+    c.j = 0;
+    if (pub > 0) {
+      const int s0 = se - pub;
+      set_tile(c, p.sk_first + s0 / kiters, s0 % kiters);
+    } else if (dp_iters > 0) {
+      set_tile(c, cta, 0);
     } else {
-      s = sb + (j - pub - dp_iters);
+      set_tile(c, sk_tile0, sk_kk0);
     }
-    tile = p.sk_first + (int)(s / p.kiters);
-    kk = (int)(s % p.kiters);
+  };
+  auto advance = [&](Cursor& c) {
+    ++c.j;
+    ++c.kk;
+    if (pub > 0 && c.j == pub) {
+      if (dp_iters > 0) set_tile(c, cta, 0);
+      else set_tile(c, sk_tile0, sk_kk0);
+    } else if (dp_iters > 0 && c.j == pub + dp_iters) {
+      set_tile(c, sk_tile0, sk_kk0);
+    } else if (c.kk == kiters) {
+      set_tile(c, c.tile + ((c.j < pub + dp_iters) ? G : 1), 0);
+    }
   };
 
-  auto load_iter = [&](int j, int stage) {
-    int tile, kk;
-    locate(j, tile, kk);
-    const int m0 = (tile / p.tiles_n) * BM, n0 = (tile % p.tiles_n) * BN;
-    const int k0 = kk * BK;
+  // per-thread global->smem copy coordinates (fixed for the whole kernel)
+  const int lrow = tid / BK, lcol = tid % BK;  // row lrow + it*(THREADS/BK), 16-byte chunk lcol
+  auto load_iter = [&](const Cursor& c, int stage) {
+    const int k0 = c.kk * BK + lcol;
     unsigned char* sa = smem + stage * STAGE_BYTES;
-    unsigned char* sb_ = sa + BM * ROWB;
+    unsigned char* sbuf = sa + BM * ROWB;
+    const bool kok = k0 < p.n;
 #pragma unroll
     for (int it = 0; it < (BM * BK) / THREADS; ++it) {
-      const int id = tid + it * THREADS;
-      const int r = id / BK, c16 = id % BK;
-      const int gm = m0 + r, gk = k0 + c16;
-      const bool ok = gm < p.n && gk < p.n;
-      cp_async16(sa + swz(r, c16), ok ? p.h + (long long)gm * p.ldh + gk : p.h, ok);
+      const int r = lrow + it * (THREADS / BK);
+      const int gm = c.m0 + r;
+      const bool ok = kok && gm < p.n;
+      cp_async16(sa + swz(r, lcol), ok ? p.h + (long long)gm * p.ldh + k0 : p.h, ok);
     }
 #pragma unroll
     for (int it = 0; it < (BN * BK + THREADS - 1) / THREADS; ++it) {
-      const int id = tid + it * THREADS;
-      if ((BN * BK) % THREADS == 0 || id < BN * BK) {
-        const int r = id / BK, c16 = id % BK;
-        const int gn = n0 + r, gk = k0 + c16;
-        const bool ok = gn < p.w && gk < p.n;
-        cp_async16(sb_ + swz(r, c16), ok ? p.ycur + (long long)gn * p.ldc + gk : p.ycur, ok);
+      const int r = lrow + it * (THREADS / BK);
+      if ((BN * BK) % THREADS == 0 || r < BN) {
+        const int gn = c.n0 + r;
+        const bool ok = kok && gn < p.w;
+        cp_async16(sbuf + swz(r, lcol), ok ? p.ycur + (long long)gn * p.ldc + k0 : p.ycur, ok);
       }
     }
   };
@@ -179,117 +197,136 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) cheb_step_kernel(const S
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
 
-  auto epilogue = [&](int tile) {
-    const int m0 = (tile / p.tiles_n) * BM, n0 = (tile % p.tiles_n) * BN;
+  auto epilogue = [&](const Cursor& c) {
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
       for (int j = 0; j < NI; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int row = m0 + wm * TM + i * 8 + g;
-          const int col = n0 + wn * TN + j * 8 + 2 * t + e;
+          const int row = c.m0 + wm * TM + i * 8 + g;
+          const int col = c.n0 + wn * TN + j * 8 + 2 * t + e;
           if (row < p.n && col < p.w) epilogue_store(p, row, col, acc[i][j][e], acc[i][j][2 + e]);
         }
   };
 
+  Cursor lc;
+  start(lc);
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < total) load_iter(s, s);
+    if (lc.j < total) {
+      load_iter(lc, s);
+      advance(lc);
+    }
     cp_async_commit();
   }
 
-  const int arow = (wm * TM + g), brow = (wn * TN + g);
+  // fragment addresses: rows arow+8i / brow+8j, chunk (k4*4 + t) ^ swizzle
+  const int arow = wm * TM + g, brow = wn * TN + g;
+  Cursor cc;
+  start(cc);
   for (int j = 0; j < total; ++j) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
-    if (j + STAGES - 1 < total) load_iter(j + STAGES - 1, (j + STAGES - 1) % STAGES);
+    if (lc.j < total) {
+      load_iter(lc, lc.j % STAGES);
+      advance(lc);
+    }
     cp_async_commit();
 
     const unsigned char* sa = smem + (j % STAGES) * STAGE_BYTES;
     const unsigned char* sbm = sa + BM * ROWB;
+    double2 a[2][MI], b[2][NI];
+#pragma unroll
+    for (int i = 0; i < MI; ++i) a[0][i] = lds128(sa + swz(arow + i * 8, t));
+#pragma unroll
+    for (int jj = 0; jj < NI; ++jj) b[0][jj] = lds128(sbm + swz(brow + jj * 8, t));
 #pragma unroll
     for (int k4 = 0; k4 < BK / 4; ++k4) {
-      double2 a[MI], b[NI];
+      const int cur = k4 & 1, nxt = cur ^ 1;
+      if (k4 + 1 < BK / 4) {  // prefetch the next k4 fragments (software pipeline)
 #pragma unroll
-      for (int i = 0; i < MI; ++i) a[i] = lds128(sa + swz(arow + i * 8, k4 * 4 + t));
+        for (int i = 0; i < MI; ++i) a[nxt][i] = lds128(sa + swz(arow + i * 8, (k4 + 1) * 4 + t));
 #pragma unroll
-      for (int jj = 0; jj < NI; ++jj) b[jj] = lds128(sbm + swz(brow + jj * 8, k4 * 4 + t));
+        for (int jj = 0; jj < NI; ++jj)
+          b[nxt][jj] = lds128(sbm + swz(brow + jj * 8, (k4 + 1) * 4 + t));
+      }
+      // Re/Im of (a or conj(a)) * b: four real DMMAs per complex 8x8x4 block
 #pragma unroll
       for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int jj = 0; jj < NI; ++jj) {
           double(&cr)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][0]);
           double(&ci)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][2]);
-          dmma884(cr, a[i].x, b[jj].x);
-          dmma884(ci, a[i].x, b[jj].y);
+          dmma884(cr, a[cur][i].x, b[cur][jj].x);
+          dmma884(ci, a[cur][i].x, b[cur][jj].y);
         }
 #pragma unroll
       for (int i = 0; i < MI; ++i) {
-        const double ai = a[i].y, nai = -a[i].y;
+        const double ai = a[cur][i].y, nai = -a[cur][i].y;
 #pragma unroll
         for (int jj = 0; jj < NI; ++jj) {
           double(&cr)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][0]);
           double(&ci)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][2]);
-          dmma884(cr, CONJ ? ai : nai, b[jj].y);
-          dmma884(ci, CONJ ? nai : ai, b[jj].x);
+          dmma884(cr, CONJ ? ai : nai, b[cur][jj].y);
+          dmma884(ci, CONJ ? nai : ai, b[cur][jj].x);
         }
       }
     }
 
     // ---- end of a tile segment?
-    int tile, kk;
-    locate(j, tile, kk);
-    const bool tile_end = kk == p.kiters - 1;
+    const bool tile_end = cc.kk == kiters - 1;
     const bool pub_end = pub > 0 && j == pub - 1;
-    if (!tile_end && !pub_end) continue;
-    if (pub_end) {
-      // non-owner: publish the partial head of this CTA's last tile
-      double* dst = p.partials + (size_t)cta * ACC * THREADS + tid;
+    if (tile_end || pub_end) {
+      if (pub_end) {
+        // non-owner: publish the partial head of this CTA's last tile
+        double* dst = p.partials + (size_t)cta * ACC * THREADS + tid;
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int jj = 0; jj < NI; ++jj)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) __stcg(dst + ((i * NI + jj) * 4 + e) * THREADS, acc[i][jj][e]);
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) st_release(p.flags + cta, p.epoch);
+      } else if (j < pub + dp_iters) {
+        epilogue(cc);
+      } else {
+        const int tile_s0 = (cc.tile - p.sk_first) * kiters;  // first SK iteration of the tile
+        if (tile_s0 >= sb) {
+          epilogue(cc);
+        } else {
+          // owner: the peers are the CTAs whose ranges hold [tile_s0, sb)
+          const int first =
+              (int)(((long long)(tile_s0 + 1) * p.sk_ctas + p.sk_iters - 1) / p.sk_iters) - 1;
+          if (tid == 0) {
+            for (int q = first; q < cta; ++q)
+              while (ld_acquire(p.flags + q) != p.epoch) __nanosleep(64);
+          }
+          __syncthreads();
+          // fixed fold order: own partial, then peers first..cta-1
+          for (int q = first; q < cta; ++q) {
+            const double* src = p.partials + (size_t)q * ACC * THREADS + tid;
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+              for (int jj = 0; jj < NI; ++jj)
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  acc[i][jj][e] = dadd(acc[i][jj][e], __ldcg(src + ((i * NI + jj) * 4 + e) * THREADS));
+          }
+          epilogue(cc);
+        }
+      }
 #pragma unroll
       for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int jj = 0; jj < NI; ++jj)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) __stcg(dst + ((i * NI + jj) * 4 + e) * THREADS, acc[i][jj][e]);
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) st_release(p.flags + cta, p.epoch);
-    } else if (j < pub + dp_iters) {
-      epilogue(tile);
-    } else {
-      const long long s = sb + (j - pub - dp_iters);
-      const long long tile_s0 = (s / p.kiters) * p.kiters;  // first SK iteration of the tile
-      if (tile_s0 >= sb) {
-        epilogue(tile);
-      } else {
-        // owner: peers are the CTAs whose ranges hold [tile_s0, sb)
-        const int first = (int)(((tile_s0 + 1) * p.sk_ctas + p.sk_iters - 1) / p.sk_iters) - 1;
-        if (tid == 0) {
-          for (int q = first; q < cta; ++q)
-            while (ld_acquire(p.flags + q) != p.epoch) __nanosleep(64);
-        }
-        __syncthreads();
-        // fixed fold order: own partial, then peers first..cta-1
-        for (int q = first; q < cta; ++q) {
-          const double* src = p.partials + (size_t)q * ACC * THREADS + tid;
-#pragma unroll
-          for (int i = 0; i < MI; ++i)
-#pragma unroll
-            for (int jj = 0; jj < NI; ++jj)
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                acc[i][jj][e] = dadd(acc[i][jj][e], __ldcg(src + ((i * NI + jj) * 4 + e) * THREADS));
-        }
-        epilogue(tile);
-      }
+          for (int e = 0; e < 4; ++e) acc[i][jj][e] = 0.0;
     }
-#pragma unroll
-    for (int i = 0; i < MI; ++i)
-#pragma unroll
-      for (int jj = 0; jj < NI; ++jj)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[i][jj][e] = 0.0;
+    advance(cc);
   }
   cp_async_wait<0>();
 }
