@@ -35,11 +35,10 @@ namespace chfsi {
 
 namespace {
 
-constexpr int BM = 64;
 constexpr int BK = 16;             // complex elements per K slab
 constexpr int ROWB = BK * 16;      // 256-byte smem rows (swizzled, no padding)
-constexpr int THREADS = 256;       // 8 warps
-constexpr int CTAS_PER_SM = 2;
+constexpr int kMaxThreads = 256;
+constexpr int kMaxAcc = 32;        // doubles per thread in a partial tile (upper bound)
 
 struct StepParams {
   const double2* h;
@@ -94,13 +93,15 @@ __device__ __forceinline__ void epilogue_store(const StepParams& p, int row, int
 // byte offset of 16-byte chunk `kk` of smem row `r` (row-parity XOR swizzle)
 __device__ __forceinline__ int swz(int r, int kk) { return r * ROWB + ((kk ^ ((r & 1) << 2)) << 4); }
 
-template <int BN, int WM, int WN, int STAGES, bool CONJ>
-__global__ void __launch_bounds__(THREADS, CTAS_PER_SM) cheb_step_kernel(const StepParams p) {
+template <int BM, int BN, int WM, int WN, int STAGES, int MINB, bool CONJ>
+__global__ void __launch_bounds__(WM* WN * 32, MINB) cheb_step_kernel(const StepParams p) {
+  constexpr int THREADS = WM * WN * 32;
   constexpr int TM = BM / WM, TN = BN / WN;
   constexpr int MI = TM / 8, NI = TN / 8;
   constexpr int ACC = MI * NI * 4;
   constexpr int STAGE_BYTES = (BM + BN) * ROWB;
-  static_assert(WM * WN * 32 == THREADS, "8 warps");
+  static_assert(THREADS <= kMaxThreads && ACC <= kMaxAcc, "workspace bound");
+  static_assert((BM * BK) % THREADS == 0, "A-tile copy split");
   static_assert(MI >= 1 && NI >= 1, "warp tile too small");
   extern __shared__ __align__(128) unsigned char smem[];
 
@@ -335,36 +336,43 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) cheb_step_kernel(const S
 
 struct Variant {
   const void* fn;
-  int smem;
+  int bm, bn, threads, smem;
   int resident;  // CTAs per SM actually achievable
-  int acc;       // doubles per thread in a partial tile
 };
 
-template <int BN, int WM, int WN, int STAGES, bool CONJ>
+template <int BM, int BN, int WM, int WN, int STAGES, int MINB, bool CONJ>
 Variant make_variant() {
   Variant v{};
-  auto fn = cheb_step_kernel<BN, WM, WN, STAGES, CONJ>;
+  auto fn = cheb_step_kernel<BM, BN, WM, WN, STAGES, MINB, CONJ>;
   v.fn = reinterpret_cast<const void*>(fn);
+  v.bm = BM;
+  v.bn = BN;
+  v.threads = WM * WN * 32;
   v.smem = STAGES * (BM + BN) * ROWB;
-  v.acc = (BM / WM / 8) * (BN / WN / 8) * 4;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, THREADS, v.smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, v.threads, v.smem);
   v.resident = occ > 0 ? occ : 1;
   return v;
 }
 
-const Variant& variant(int bn, bool conj) {
-  // function-local statics: initialised once, on first use (device set by caller)
-  static const Variant v16 = make_variant<16, 8, 1, 4, false>();
-  static const Variant v16c = make_variant<16, 8, 1, 4, true>();
-  static const Variant v32 = make_variant<32, 4, 2, 4, false>();
-  static const Variant v32c = make_variant<32, 4, 2, 4, true>();
-  static const Variant v64 = make_variant<64, 2, 4, 3, false>();
-  static const Variant v64c = make_variant<64, 2, 4, 3, true>();
-  if (bn == 16) return conj ? v16c : v16;
-  if (bn == 32) return conj ? v32c : v32;
-  return conj ? v64c : v64;
+// (bm, bn) -> kernel configuration. Function-local statics: built once, on
+// first use (the caller has set the device).
+const Variant* variant(int bm, int bn, bool conj) {
+#define CHFSI_V(BM_, BN_, WM_, WN_, ST_, MB_)                                         \
+  if (bm == BM_ && bn == BN_) {                                                       \
+    static const Variant a = make_variant<BM_, BN_, WM_, WN_, ST_, MB_, false>();     \
+    static const Variant b = make_variant<BM_, BN_, WM_, WN_, ST_, MB_, true>();      \
+    return conj ? &b : &a;                                                            \
+  }
+  CHFSI_V(64, 16, 8, 1, 4, 2)
+  CHFSI_V(64, 32, 4, 2, 4, 2)
+  CHFSI_V(64, 64, 2, 4, 3, 2)
+  CHFSI_V(32, 32, 2, 2, 4, 3)
+  CHFSI_V(32, 64, 2, 2, 3, 3)
+  CHFSI_V(128, 32, 4, 2, 3, 1)
+#undef CHFSI_V
+  return nullptr;
 }
 
 }  // namespace
@@ -373,23 +381,26 @@ StepTiling choose_step_tiling(int n, int w) {
   // least padded work, mild preference for wider tiles (operand reuse)
   const int bns[3] = {64, 32, 16};
   const double pen[3] = {1.0, 1.03, 1.10};
-  StepTiling best{BM, 64, 0};
+  StepTiling best{64, 64, 0};
   double best_cost = 1e300;
   for (int i = 0; i < 3; ++i) {
     const double padded = (double)((w + bns[i] - 1) / bns[i]) * bns[i];
     const double cost = padded * pen[i];
     if (cost < best_cost) {
       best_cost = cost;
-      best = StepTiling{BM, bns[i], 0};
+      best = StepTiling{64, bns[i], 0};
     }
   }
   (void)n;
   return best;
 }
 
-size_t step_workspace_doubles(int max_grid) { return (size_t)max_grid * 64 * THREADS; }
+size_t step_workspace_doubles(int max_grid) { return (size_t)max_grid * kMaxAcc * kMaxThreads; }
 
-int step_grid_size(int bn, bool conj) { return variant(bn, conj).resident * kNumSMs; }
+int step_grid_size(int bn, bool conj) {
+  const Variant* v = variant(64, bn, conj);
+  return v ? v->resident * kNumSMs : 0;
+}
 
 cudaError_t cheb_step_launch(const double2* h, long long ldh, bool conj_h, const double2* ycur,
                              long long ldc, const double2* yprev, long long ldp, double2* ynext,
@@ -397,8 +408,10 @@ cudaError_t cheb_step_launch(const double2* h, long long ldh, bool conj_h, const
                              StepTiling tiling, const StepWorkspace& ws, cudaStream_t stream) {
   if (n <= 0 || w <= 0) return cudaSuccess;
   if (tiling.bm == 0) tiling = choose_step_tiling(n, w);
-  if (tiling.bn != 16 && tiling.bn != 32 && tiling.bn != 64) return cudaErrorInvalidValue;
-  const Variant& v = variant(tiling.bn, conj_h);
+  const Variant* vp = variant(tiling.bm, tiling.bn, conj_h);
+  if (vp == nullptr) return cudaErrorInvalidValue;
+  const Variant& v = *vp;
+  const int BM = v.bm;
   int grid = v.resident * kNumSMs;
   if (tiling.split > 0 && tiling.split < grid) grid = tiling.split;  // test/tuning override
   if (grid > ws.max_grid) return cudaErrorInvalidValue;
@@ -432,7 +445,7 @@ cudaError_t cheb_step_launch(const double2* h, long long ldh, bool conj_h, const
   p.epoch = ++*ws.epoch;
   void* args[] = {&p};
   note_launch();
-  return cudaLaunchKernel(v.fn, dim3(grid), dim3(THREADS), args, v.smem, stream);
+  return cudaLaunchKernel(v.fn, dim3(grid), dim3(v.threads), args, v.smem, stream);
 }
 
 }  // namespace chfsi

@@ -178,7 +178,7 @@ int chfsi_ctx_set_tiling(chfsi_ctx* ctx, int bm, int bn, int split) {
     ctx->tiling = chfsi::StepTiling{0, 0, 0};
     return CHFSI_OK;
   }
-  CK_ARG(bm == 64 && (bn == 16 || bn == 32 || bn == 64) && split >= 0 &&
+  CK_ARG((bm == 32 || bm == 64 || bm == 128) && (bn == 16 || bn == 32 || bn == 64) && split >= 0 &&
              split <= ctx->step_ws.max_grid,
          "unsupported K1 tiling");
   ctx->tiling = chfsi::StepTiling{bm, bn, split};

@@ -1,8 +1,8 @@
 """K1 throughput sweep vs cuBLAS ZGEMM at the BASELINE filter shapes.
 
-    python tools/k1_sweep.py [--quick]
-Prints one JSON line per (n, w): K1 TFLOP/s (fused step, CUDA events over
-deg launches) and cuBLAS ZGEMM TFLOP/s for the bare product.
+    python tools/k1_sweep.py [--quick] [--variants auto,64x32,32x32,...]
+Prints one JSON line per (n, w, variant): K1 TFLOP/s (fused step, CUDA
+events over deg launches) and cuBLAS ZGEMM TFLOP/s for the bare product.
 """
 import argparse
 import json
@@ -21,12 +21,31 @@ from paper_1206_3768_b200.chfsi import _filter_into
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--quick", action="store_true")
-ap.add_argument("--bn", type=int, default=0)
+ap.add_argument("--variants", default="auto")
+ap.add_argument("--shapes", default="")
+ap.add_argument("--no-cublas", action="store_true")
 a = ap.parse_args()
 shapes = [(512, 48), (2048, 160), (2048, 100), (2048, 40), (5000, 600), (5000, 250),
           (12000, 1400)]
+if a.shapes:
+    shapes = [tuple(int(v) for v in s.split("x")) for s in a.shapes.split(",")]
 if a.quick:
     shapes = shapes[:5]
+variants = a.variants.split(",")
+
+
+def timed(fn, reps):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fn()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
 hcache = {}
 for n, w in shapes:
     if n not in hcache:
@@ -39,31 +58,23 @@ for n, w in shapes:
     y = fblock(n, w)
     y.copy_(torch.randn(n, w, dtype=torch.complex128, device="cuda"))
     x = fblock(n, w)
-    if a.bn:
-        _lib.check(_lib.lib().chfsi_ctx_set_tiling(_lib.ctx(), 64, a.bn, 0))
     win = pkg.FilterWindow(a=-5.0, b=60.0, scale_ref=-70.0)
     deg = 8
     reps = 3 if n <= 5000 else 1
-    _filter_into(op, y, x, y, deg, win)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        _filter_into(op, y, x, y, deg, win)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / (reps * deg)
-    yy = torch.randn(n, w, dtype=torch.complex128, device="cuda")
-    z = h @ yy
-    torch.cuda.synchronize()
-    e0.record()
-    for _ in range(reps * 2):
-        z = h @ yy
-    e1.record()
-    torch.cuda.synchronize()
-    ms_c = e0.elapsed_time(e1) / (reps * 2)
-    fl = 8.0 * n * n * w
-    print(json.dumps({"n": n, "w": w, "k1_us": round(ms * 1e3, 2), "k1_tflops": round(fl / ms / 1e9, 2),
-                      "cublas_us": round(ms_c * 1e3, 2), "cublas_tflops": round(fl / ms_c / 1e9, 2)}),
-          flush=True)
+    cub = None
+    if not a.no_cublas:
+        yy = torch.randn(n, w, dtype=torch.complex128, device="cuda")
+        ms_c = timed(lambda: h @ yy, reps * 2)
+        cub = 8.0 * n * n * w / ms_c / 1e9
+    for v in variants:
+        if v == "auto":
+            _lib.check(_lib.lib().chfsi_ctx_set_tiling(_lib.ctx(), 0, 0, 0))
+        else:
+            bm, bn = (int(t) for t in v.split("x"))
+            _lib.check(_lib.lib().chfsi_ctx_set_tiling(_lib.ctx(), bm, bn, 0))
+        ms = timed(lambda: _filter_into(op, y, x, y, deg, win), reps) / deg
+        fl = 8.0 * n * n * w
+        print(json.dumps({"n": n, "w": w, "variant": v, "k1_us": round(ms * 1e3, 2),
+                          "k1_tflops": round(fl / ms / 1e9, 2),
+                          "cublas_tflops": None if cub is None else round(cub, 2)}), flush=True)
     _lib.check(_lib.lib().chfsi_ctx_set_tiling(_lib.ctx(), 0, 0, 0))
