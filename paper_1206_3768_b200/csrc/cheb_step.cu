@@ -13,19 +13,27 @@
 // conjugate, so a column-major Hermitian H (cuBLAS/cuSOLVER output) is used
 // as-is. Y blocks are column-major (Y[col*ld + row]). complex128 interleaved.
 //
-// Schedule: a persistent grid of exactly the resident CTAs (2 per SM) walks
-// a linearised (tile, k-slab) iteration space — whole tiles first
-// ("data-parallel" waves, consecutive CTAs on neighbouring column tiles of
-// one H row panel so the panel is shared through L2), then the remaining
-// tiles split evenly across all CTAs by k-slab ("stream-K"). A tile whose
-// k-range is split is finished by the CTA holding its last slab: it waits
-// for its peers' published partial tiles and sums them in FIXED peer order,
-// so every launch is bitwise reproducible (reference test_chfsi.py:234-241)
-// and no SM idles on a wave tail, whatever (n, w) the locking leaves.
+// Operand staging: TMA (cp.async.bulk.tensor, one elected thread) streams
+// BK=16-complex k-slabs of the H row panel and of the Y column panel into a
+// STAGES-deep shared-memory ring, completion tracked by mbarriers (full: TMA
+// bytes landed; empty: all warps done reading). Each 256-byte k-row is split
+// in two 128-byte TMA boxes with the hardware 128B swizzle; fragment rows are
+// permuted inside each 8-row group (sigma) so the per-lane 16-byte fragment
+// loads are bank-conflict free under that swizzle. Out-of-range rows,
+// columns and k are zero-filled by the TMA unit (no predication in the loop).
 //
-// Pipeline: K slabs of BK=16 complex staged global->shared with a
-// STAGES-deep cp.async ring; 16-byte chunks XOR-swizzled on row parity so
-// the per-lane 16-byte fragment loads (8 rows x 4 k) are bank-conflict free.
+// Schedule: a persistent grid of exactly the resident CTAs walks a
+// linearised (tile, k-slab) iteration space — whole tiles in data-parallel
+// waves (consecutive CTAs on neighbouring column tiles of one H row panel,
+// so the panel is read from HBM once and reused through L2), the remaining
+// tiles split evenly by k-slab ("stream-K"). A split tile is finished by the
+// CTA holding its last slab, which waits for the peers' published partial
+// tiles and folds them in FIXED order: every launch is bitwise reproducible
+// (reference test_chfsi.py:234-241) and no SM idles in a wave tail, whatever
+// (n, w) the locking leaves. A CTA computes and publishes its partial
+// head-of-tile segment first, so owners never wait on a chain of peers.
+#include <cuda.h>
+
 #include <cstdint>
 
 #include "chfsi_internal.h"
@@ -35,14 +43,12 @@ namespace chfsi {
 
 namespace {
 
-constexpr int BK = 16;             // complex elements per K slab
-constexpr int ROWB = BK * 16;      // 256-byte smem rows (swizzled, no padding)
+constexpr int BK = 16;             // complex elements per K slab (two 128-byte halves)
+constexpr int HALF = 128;          // bytes per row per half-slab (one TMA box row)
 constexpr int kMaxThreads = 256;
 constexpr int kMaxAcc = 32;        // doubles per thread in a partial tile (upper bound)
 
 struct StepParams {
-  const double2* h;
-  long long ldh;
   const double2* ycur;
   long long ldc;
   const double2* yprev;
@@ -63,6 +69,40 @@ struct StepParams {
   unsigned epoch;
 };
 
+// ------------------------------------------------------------ PTX helpers ---
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map, unsigned bar,
+                                            int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -71,6 +111,11 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
+
+// fragment row g of an 8-row group -> smem row inside the group. Rows g and
+// g+1 (same LDS.128 phase) land 4 apart, i.e. in opposite 64-byte halves
+// of the 128B-swizzled row, so the 8 lanes of a phase hit 32 distinct banks.
+__device__ __forceinline__ int sigma(int g) { return ((g & 1) << 2) | (g >> 1); }
 
 __device__ __forceinline__ void epilogue_store(const StepParams& p, int row, int col, double ar,
                                                double ai) {
@@ -90,20 +135,28 @@ __device__ __forceinline__ void epilogue_store(const StepParams& p, int row, int
   p.ynext[(long long)col * p.ldn + row] = make_double2(tr, ti);
 }
 
-// byte offset of 16-byte chunk `kk` of smem row `r` (row-parity XOR swizzle)
-__device__ __forceinline__ int swz(int r, int kk) { return r * ROWB + ((kk ^ ((r & 1) << 2)) << 4); }
-
 template <int BM, int BN, int WM, int WN, int STAGES, int MINB, bool CONJ>
-__global__ void __launch_bounds__(WM* WN * 32, MINB) cheb_step_kernel(const StepParams p) {
-  constexpr int THREADS = WM * WN * 32;
+__global__ void __launch_bounds__(WM* WN * 32, MINB)
+    cheb_step_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const StepParams p) {
+  constexpr int NWARPS = WM * WN;
+  constexpr int THREADS = NWARPS * 32;
   constexpr int TM = BM / WM, TN = BN / WN;
   constexpr int MI = TM / 8, NI = TN / 8;
   constexpr int ACC = MI * NI * 4;
-  constexpr int STAGE_BYTES = (BM + BN) * ROWB;
+  constexpr int A_BYTES = BM * HALF;  // one half-slab of A
+  constexpr int B_BYTES = BN * HALF;
+  constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
   static_assert(THREADS <= kMaxThreads && ACC <= kMaxAcc, "workspace bound");
-  static_assert((BM * BK) % THREADS == 0, "A-tile copy split");
   static_assert(MI >= 1 && NI >= 1, "warp tile too small");
-  extern __shared__ __align__(128) unsigned char smem[];
+  static_assert(A_BYTES % 1024 == 0 && B_BYTES % 1024 == 0, "128B swizzle needs 1024B-aligned boxes");
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 128B-swizzled TMA destinations must be 1024-byte aligned (offset kept
+  // relative to the __shared__ array so loads stay LDS, not generic LD)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  const unsigned smem0 = smem_u32(smem);
+  const unsigned full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -120,10 +173,7 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) cheb_step_kernel(const Step
   }
   const int total = dp_iters + (se - sb);
   if (total == 0) return;
-  // If the range ends inside a tile, that head-of-tile segment is a partial
-  // the tile's owner (a later CTA) will consume: compute and publish it
-  // FIRST, so owners never wait on a chain of peers. Local order:
-  //   [publish segment] [data-parallel tiles] [rest of the stream-K range]
+  // Local order: [publish segment] [data-parallel tiles] [rest of stream-K]
   int pub = 0;
   if (se > sb && (se % kiters) != 0) {
     const int head = ((se - 1) / kiters) * kiters;
@@ -131,7 +181,6 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) cheb_step_kernel(const Step
   }
   const int sk_tile0 = p.sk_first + sb / kiters, sk_kk0 = sb % kiters;
 
-  // Cursor over that order; advanced incrementally (no per-slab division).
   struct Cursor {
     int j, tile, kk, m0, n0;
   };
@@ -164,31 +213,36 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) cheb_step_kernel(const Step
       set_tile(c, c.tile + ((c.j < pub + dp_iters) ? G : 1), 0);
     }
   };
-
-  // per-thread global->smem copy coordinates (fixed for the whole kernel)
-  const int lrow = tid / BK, lcol = tid % BK;  // row lrow + it*(THREADS/BK), 16-byte chunk lcol
-  auto load_iter = [&](const Cursor& c, int stage) {
-    const int k0 = c.kk * BK + lcol;
-    unsigned char* sa = smem + stage * STAGE_BYTES;
-    unsigned char* sbuf = sa + BM * ROWB;
-    const bool kok = k0 < p.n;
-#pragma unroll
-    for (int it = 0; it < (BM * BK) / THREADS; ++it) {
-      const int r = lrow + it * (THREADS / BK);
-      const int gm = c.m0 + r;
-      const bool ok = kok && gm < p.n;
-      cp_async16(sa + swz(r, lcol), ok ? p.h + (long long)gm * p.ldh + k0 : p.h, ok);
-    }
-#pragma unroll
-    for (int it = 0; it < (BN * BK + THREADS - 1) / THREADS; ++it) {
-      const int r = lrow + it * (THREADS / BK);
-      if ((BN * BK) % THREADS == 0 || r < BN) {
-        const int gn = c.n0 + r;
-        const bool ok = kok && gn < p.w;
-        cp_async16(sbuf + swz(r, lcol), ok ? p.ycur + (long long)gn * p.ldc + k0 : p.ycur, ok);
-      }
-    }
+  // one elected thread: arm the stage's barrier and issue its four TMA boxes
+  auto issue = [&](const Cursor& c, int stage) {
+    const unsigned dst = smem0 + stage * STAGE_BYTES, bar = full0 + 8 * stage;
+    const int x = c.kk * (2 * BK);  // in doubles
+    mbar_expect_tx(bar, STAGE_BYTES);
+    tma_load_2d(dst, &tmA, bar, x, c.m0);
+    tma_load_2d(dst + A_BYTES, &tmA, bar, x + BK, c.m0);
+    tma_load_2d(dst + 2 * A_BYTES, &tmB, bar, x, c.n0);
+    tma_load_2d(dst + 2 * A_BYTES + B_BYTES, &tmB, bar, x + BK, c.n0);
   };
+
+  if (tid == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, NWARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  Cursor lc;
+  start(lc);
+  if (tid == 0) {
+    for (int s = 0; s < STAGES && lc.j < total; ++s) {
+      issue(lc, s);
+      advance(lc);
+    }
+  }
 
   double acc[MI][NI][4];  // [.][.][0..1] real, [2..3] imag of C[g][2t+e]
 #pragma unroll
@@ -198,6 +252,7 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) cheb_step_kernel(const Step
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
 
+  const int sg = sigma(g);
   auto epilogue = [&](const Cursor& c) {
 #pragma unroll
     for (int i = 0; i < MI; ++i)
@@ -205,53 +260,37 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) cheb_step_kernel(const Step
       for (int j = 0; j < NI; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int row = c.m0 + wm * TM + i * 8 + g;
-          const int col = c.n0 + wn * TN + j * 8 + 2 * t + e;
+          const int row = c.m0 + wm * TM + i * 8 + sg;
+          const int col = c.n0 + wn * TN + j * 8 + sigma(2 * t + e);
           if (row < p.n && col < p.w) epilogue_store(p, row, col, acc[i][j][e], acc[i][j][2 + e]);
         }
   };
 
-  Cursor lc;
-  start(lc);
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (lc.j < total) {
-      load_iter(lc, s);
-      advance(lc);
-    }
-    cp_async_commit();
-  }
+  // per-thread fragment byte offsets: row (warp base + sigma(g)) * 128, and
+  // the swizzled chunk for even / odd k4 within a 128-byte half
+  const int lo = (t ^ (g >> 1)) << 4;
+  const int off_even = ((g & 1) << 6) | lo, off_odd = (((g & 1) ^ 1) << 6) | lo;
+  const unsigned char* a_base = smem + (wm * TM + sg) * HALF;
+  const unsigned char* b_base = smem + 2 * A_BYTES + (wn * TN + sg) * HALF;
 
-  // fragment addresses: rows arow+8i / brow+8j, chunk (k4*4 + t) ^ swizzle
-  const int arow = wm * TM + g, brow = wn * TN + g;
   Cursor cc;
   start(cc);
+  int stage = 0;
+  unsigned phase = 0;
   for (int j = 0; j < total; ++j) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    if (lc.j < total) {
-      load_iter(lc, lc.j % STAGES);
-      advance(lc);
-    }
-    cp_async_commit();
-
-    const unsigned char* sa = smem + (j % STAGES) * STAGE_BYTES;
-    const unsigned char* sbm = sa + BM * ROWB;
-    double2 a[2][MI], b[2][NI];
-#pragma unroll
-    for (int i = 0; i < MI; ++i) a[0][i] = lds128(sa + swz(arow + i * 8, t));
-#pragma unroll
-    for (int jj = 0; jj < NI; ++jj) b[0][jj] = lds128(sbm + swz(brow + jj * 8, t));
+    mbar_wait(full0 + 8 * stage, phase);
+    const unsigned char* sa = a_base + stage * STAGE_BYTES;
+    const unsigned char* sbm = b_base + stage * STAGE_BYTES;
 #pragma unroll
     for (int k4 = 0; k4 < BK / 4; ++k4) {
-      const int cur = k4 & 1, nxt = cur ^ 1;
-      if (k4 + 1 < BK / 4) {  // prefetch the next k4 fragments (software pipeline)
+      const int off = (k4 & 1) ? off_odd : off_even;
+      const unsigned char* ah = sa + (k4 >> 1) * A_BYTES + off;
+      const unsigned char* bh = sbm + (k4 >> 1) * B_BYTES + off;
+      double2 a[MI], b[NI];
 #pragma unroll
-        for (int i = 0; i < MI; ++i) a[nxt][i] = lds128(sa + swz(arow + i * 8, (k4 + 1) * 4 + t));
+      for (int i = 0; i < MI; ++i) a[i] = lds128(ah + i * 8 * HALF);
 #pragma unroll
-        for (int jj = 0; jj < NI; ++jj)
-          b[nxt][jj] = lds128(sbm + swz(brow + jj * 8, (k4 + 1) * 4 + t));
-      }
+      for (int jj = 0; jj < NI; ++jj) b[jj] = lds128(bh + jj * 8 * HALF);
       // Re/Im of (a or conj(a)) * b: four real DMMAs per complex 8x8x4 block
 #pragma unroll
       for (int i = 0; i < MI; ++i)
@@ -259,20 +298,32 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) cheb_step_kernel(const Step
         for (int jj = 0; jj < NI; ++jj) {
           double(&cr)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][0]);
           double(&ci)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][2]);
-          dmma884(cr, a[cur][i].x, b[cur][jj].x);
-          dmma884(ci, a[cur][i].x, b[cur][jj].y);
+          dmma884(cr, a[i].x, b[jj].x);
+          dmma884(ci, a[i].x, b[jj].y);
         }
 #pragma unroll
       for (int i = 0; i < MI; ++i) {
-        const double ai = a[cur][i].y, nai = -a[cur][i].y;
+        const double ai = a[i].y, nai = -a[i].y;
 #pragma unroll
         for (int jj = 0; jj < NI; ++jj) {
           double(&cr)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][0]);
           double(&ci)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][2]);
-          dmma884(cr, CONJ ? ai : nai, b[cur][jj].y);
-          dmma884(ci, CONJ ? nai : ai, b[cur][jj].x);
+          dmma884(cr, CONJ ? ai : nai, b[jj].y);
+          dmma884(ci, CONJ ? nai : ai, b[jj].x);
         }
       }
+    }
+    // release the stage; the elected thread refills it once every warp has
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * stage);
+    if (tid == 0 && lc.j < total) {
+      mbar_wait(empty0 + 8 * stage, phase);
+      issue(lc, stage);
+      advance(lc);
+    }
+    if (++stage == STAGES) {
+      stage = 0;
+      phase ^= 1u;
     }
 
     // ---- end of a tile segment?
@@ -329,10 +380,41 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) cheb_step_kernel(const Step
     }
     advance(cc);
   }
-  cp_async_wait<0>();
 }
 
 // --------------------------------------------------------------- host ---
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// 2-D map over a complex128 matrix seen as doubles: dim0 = 2*len (contiguous),
+// dim1 = count vectors `ld` complex apart; box = 16 doubles x rows, 128B swizzle.
+bool encode_map(CUtensorMap* map, const void* base, long long len, long long count, long long ld,
+                int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)(2 * len), (cuuint64_t)count};
+  const cuuint64_t strides[1] = {(cuuint64_t)(ld * 16)};
+  const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 struct Variant {
   const void* fn;
@@ -348,7 +430,7 @@ Variant make_variant() {
   v.bm = BM;
   v.bn = BN;
   v.threads = WM * WN * 32;
-  v.smem = STAGES * (BM + BN) * ROWB;
+  v.smem = STAGES * 2 * (BM + BN) * HALF + 2 * STAGES * 8 + 1024;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem);
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, v.threads, v.smem);
@@ -359,15 +441,15 @@ Variant make_variant() {
 // (bm, bn) -> kernel configuration. Function-local statics: built once, on
 // first use (the caller has set the device).
 const Variant* variant(int bm, int bn, bool conj) {
-#define CHFSI_V(BM_, BN_, WM_, WN_, ST_, MB_)                                         \
-  if (bm == BM_ && bn == BN_) {                                                       \
-    static const Variant a = make_variant<BM_, BN_, WM_, WN_, ST_, MB_, false>();     \
-    static const Variant b = make_variant<BM_, BN_, WM_, WN_, ST_, MB_, true>();      \
-    return conj ? &b : &a;                                                            \
+#define CHFSI_V(BM_, BN_, WM_, WN_, ST_, MB_)                                     \
+  if (bm == BM_ && bn == BN_) {                                                   \
+    static const Variant a = make_variant<BM_, BN_, WM_, WN_, ST_, MB_, false>(); \
+    static const Variant b = make_variant<BM_, BN_, WM_, WN_, ST_, MB_, true>();  \
+    return conj ? &b : &a;                                                        \
   }
   CHFSI_V(64, 16, 8, 1, 4, 2)
   CHFSI_V(64, 32, 4, 2, 4, 2)
-  CHFSI_V(64, 64, 2, 4, 3, 2)
+  CHFSI_V(64, 64, 4, 2, 3, 2)
   CHFSI_V(32, 32, 2, 2, 4, 3)
   CHFSI_V(32, 64, 2, 2, 3, 3)
   CHFSI_V(128, 32, 4, 2, 3, 1)
@@ -411,14 +493,15 @@ cudaError_t cheb_step_launch(const double2* h, long long ldh, bool conj_h, const
   const Variant* vp = variant(tiling.bm, tiling.bn, conj_h);
   if (vp == nullptr) return cudaErrorInvalidValue;
   const Variant& v = *vp;
-  const int BM = v.bm;
   int grid = v.resident * kNumSMs;
   if (tiling.split > 0 && tiling.split < grid) grid = tiling.split;  // test/tuning override
   if (grid > ws.max_grid) return cudaErrorInvalidValue;
 
+  alignas(64) CUtensorMap tmA, tmB;
+  if (!encode_map(&tmA, h, n, n, ldh, v.bm) || !encode_map(&tmB, ycur, n, w, ldc, v.bn))
+    return cudaErrorInvalidValue;
+
   StepParams p{};
-  p.h = h;
-  p.ldh = ldh;
   p.ycur = ycur;
   p.ldc = ldc;
   p.yprev = yprev ? yprev : ynext;
@@ -427,8 +510,8 @@ cudaError_t cheb_step_launch(const double2* h, long long ldh, bool conj_h, const
   p.ldn = ldn;
   p.n = n;
   p.w = w;
-  p.tiles_n = (w + tiling.bn - 1) / tiling.bn;
-  const int tiles_m = (n + BM - 1) / BM;
+  p.tiles_n = (w + v.bn - 1) / v.bn;
+  const int tiles_m = (n + v.bm - 1) / v.bm;
   const long long tiles = (long long)tiles_m * p.tiles_n;
   p.kiters = (n + BK - 1) / BK;
   p.dp_waves = tiles >= 2LL * grid ? (int)(tiles / grid) - 1 : 0;
@@ -443,7 +526,7 @@ cudaError_t cheb_step_launch(const double2* h, long long ldh, bool conj_h, const
   p.partials = ws.partials;
   p.flags = ws.flags;
   p.epoch = ++*ws.epoch;
-  void* args[] = {&p};
+  void* args[] = {&tmA, &tmB, &p};
   note_launch();
   return cudaLaunchKernel(v.fn, dim3(grid), dim3(v.threads), args, v.smem, stream);
 }

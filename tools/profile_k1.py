@@ -15,18 +15,23 @@ import torch
 import paper_1206_3768_b200 as pkg
 from paper_1206_3768_b200._device import Operator, fblock
 from paper_1206_3768_b200.chfsi import _filter_into
+from paper_1206_3768_b200 import _lib
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=2048)
 ap.add_argument("--w", type=int, default=160)
 ap.add_argument("--deg", type=int, default=16)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--variant", default="auto")
 a = ap.parse_args()
 torch.manual_seed(0)
 g = torch.randn(a.n, a.n, dtype=torch.complex128, device="cuda")
 h = (g + g.conj().T) / 2
 del g
 op = Operator(h)
+if a.variant != "auto":
+    bm, bn = (int(t) for t in a.variant.split("x"))
+    _lib.check(_lib.lib().chfsi_ctx_set_tiling(_lib.ctx(), bm, bn, 0))
 y = fblock(a.n, a.w)
 y.copy_(torch.randn(a.n, a.w, dtype=torch.complex128, device="cuda"))
 x = fblock(a.n, a.w)
