@@ -460,21 +460,15 @@ const Variant* variant(int bm, int bn, bool conj) {
 }  // namespace
 
 StepTiling choose_step_tiling(int n, int w) {
-  // least padded work, mild preference for wider tiles (operand reuse)
-  const int bns[3] = {64, 32, 16};
-  const double pen[3] = {1.0, 1.03, 1.10};
-  StepTiling best{64, 64, 0};
-  double best_cost = 1e300;
-  for (int i = 0; i < 3; ++i) {
-    const double padded = (double)((w + bns[i] - 1) / bns[i]) * bns[i];
-    const double cost = padded * pen[i];
-    if (cost < best_cost) {
-      best_cost = cost;
-      best = StepTiling{64, bns[i], 0};
-    }
-  }
-  (void)n;
-  return best;
+  // Measured on B200 (profiles/r01_k1_variants.log): 64x32 is the best or
+  // within 2 % everywhere except very wide panels, where 64x64 gains ~4 %
+  // once there are enough whole tiles for data-parallel waves; 64x16 only
+  // pays when w <= 16 (padding).
+  if (w <= 16) return StepTiling{64, 16, 0};
+  const long long tiles64 = (long long)((n + 63) / 64) * ((w + 63) / 64);
+  const int pad32 = ((w + 31) / 32) * 32, pad64 = ((w + 63) / 64) * 64;
+  if (w >= 512 && tiles64 >= 4LL * kNumSMs && pad64 <= pad32) return StepTiling{64, 64, 0};
+  return StepTiling{64, 32, 0};
 }
 
 size_t step_workspace_doubles(int max_grid) { return (size_t)max_grid * kMaxAcc * kMaxThreads; }
