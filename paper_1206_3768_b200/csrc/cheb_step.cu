@@ -321,6 +321,9 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
       issue(lc, stage);
       advance(lc);
     }
+    // warp 0 must reconverge before its next mma.sync.aligned (lane 0 may
+    // have spun on the empty barrier while lanes 1-31 ran ahead)
+    __syncwarp();
     if (++stage == STAGES) {
       stage = 0;
       phase ^= 1u;
