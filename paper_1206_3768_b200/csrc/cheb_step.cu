@@ -279,6 +279,9 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
   unsigned phase = 0;
   for (int j = 0; j < total; ++j) {
     mbar_wait(full0 + 8 * stage, phase);
+    // mma.sync.aligned needs the whole warp converged: lane 0 of warp 0 may
+    // still be issuing TMA (prologue) or spinning on an empty barrier
+    __syncwarp();
     const unsigned char* sa = a_base + stage * STAGE_BYTES;
     const unsigned char* sbm = b_base + stage * STAGE_BYTES;
 #pragma unroll
