@@ -369,6 +369,21 @@ __global__ void div_scalar_kernel(const double2* __restrict__ x, const double* d
   }
 }
 
+__global__ void add_diag_shift_kernel(double2* a, long long lda, int n, const double* fro,
+                                      double coef) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const double f = *fro;
+    a[(long long)i * lda + i].x += coef * f * f;
+  }
+}
+
+__global__ void diag_accumulate_kernel(const double2* r, long long ldr, int n, double* acc,
+                                       int first) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) acc[i] = (first ? 1.0 : acc[i]) * r[(long long)i * ldr + i].x;
+}
+
 inline int grid_for(long long total, int threads, int cap = kNumSMs * 16) {
   long long g = (total + threads - 1) / threads;
   if (g > cap) g = cap;
@@ -505,6 +520,22 @@ cudaError_t div_scalar_launch(const double2* x, const double* d, double2* y, int
   if (n <= 0) return cudaSuccess;
   note_launch();
   div_scalar_kernel<<<(n + 255) / 256, 256, 0, s>>>(x, d, y, n);
+  return cudaGetLastError();
+}
+
+cudaError_t add_diag_shift_launch(double2* a, long long lda, int n, const double* fro, double coef,
+                                  cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  note_launch();
+  add_diag_shift_kernel<<<(n + 255) / 256, 256, 0, s>>>(a, lda, n, fro, coef);
+  return cudaGetLastError();
+}
+
+cudaError_t diag_accumulate_launch(const double2* r, long long ldr, int n, double* acc, bool first,
+                                   cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  note_launch();
+  diag_accumulate_kernel<<<(n + 255) / 256, 256, 0, s>>>(r, ldr, n, acc, first ? 1 : 0);
   return cudaGetLastError();
 }
 

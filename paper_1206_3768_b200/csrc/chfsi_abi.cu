@@ -36,6 +36,7 @@ struct chfsi_ctx {
   LanczosState* lstate = nullptr;
   chfsi::StepTiling tiling{0, 0, 0};  // K1 tile override (bm == 0: automatic)
   chfsi::StepWorkspace step_ws{nullptr, nullptr, nullptr, 0};
+  int qr_mode = 0;  // 0: shifted Cholesky-QR3 with Householder fallback; 1: Householder
   unsigned step_epoch = 0;
 };
 
@@ -355,25 +356,17 @@ int chfsi_cgs_project_z(chfsi_ctx* ctx, int n, int nlocked, int w, const void* l
   return CHFSI_OK;
 }
 
-int chfsi_qr_orthonormalize_z(chfsi_ctx* ctx, int m, int n, void* Y, long long ldy, int* dead,
-                              int* ndead) {
-  CK_ARG(ctx, "ctx is NULL");
-  CK_ARG(m >= n && n >= 0, "need rows >= cols");
-  CK_ARG(ndead && dead, "NULL output");
-  *ndead = 0;
-  if (n == 0) return CHFSI_OK;
-  CK_ARG(ldy == m, "QR needs a packed block (ldy == m)");
+}  // extern "C"
+
+namespace {
+
+// Householder QR (cuSOLVER geqrf/ungqr) with the reference's rank test and
+// positive-real R diagonal (linalg.py:152-178). y holds Y on entry, Q on
+// success; on rank deficiency y is restored from `backup`.
+int qr_householder(chfsi_ctx* ctx, int m, int n, double2* y, const double2* backup, double2* tau,
+                   double2* rdiag, const double* fro, int* dead, int* ndead) {
   cudaStream_t s = ctx->stream;
-  double2* y = static_cast<double2*>(Y);
-  // scratch: backup copy of Y (m*n), tau (n), rdiag (n)
   const size_t blk = (size_t)m * n * sizeof(double2);
-  CK(ensure_scratch(ctx, blk + 2 * (size_t)n * sizeof(double2)));
-  double2* backup = static_cast<double2*>(ctx->scratch);
-  double2* tau = backup + (size_t)m * n;
-  double2* rdiag = tau + n;
-  double* fro = ctx->scalars + 1;
-  CK_CUDA(cudaMemcpyAsync(backup, y, blk, cudaMemcpyDeviceToDevice, s));
-  CK_CUDA(chfsi::norm2_launch(y, (long long)m * n, ctx->partial, fro, nullptr, s));
   int lwork = 0, lwork2 = 0;
   CK_SOLVER(cusolverDnZgeqrf_bufferSize(ctx->solver, m, n, reinterpret_cast<cuDoubleComplex*>(y),
                                         m, &lwork));
@@ -404,6 +397,100 @@ int chfsi_qr_orthonormalize_z(chfsi_ctx* ctx, int m, int n, void* Y, long long l
                              reinterpret_cast<cuDoubleComplex*>(tau),
                              static_cast<cuDoubleComplex*>(ctx->ws), lwork, ctx->dinfo));
   CK_CUDA(chfsi::phase_fix_launch(y, m, m, n, rdiag, s));
+  return CHFSI_OK;
+}
+
+// Shifted Cholesky-QR3 (Fukaya et al.): three passes of Gram (ZGEMM),
+// Cholesky (potrf) and triangular solve, the first with a shift that keeps
+// the Gram matrix definite up to cond(Y) ~ 1/u. Q is the unique QR factor
+// with positive-real R diagonal, i.e. the one linalg.py:152-178 returns.
+// Returns 1 ("use Householder") when the decision of the reference's rank
+// test could be affected by Cholesky rounding: a pivot failed, or some
+// |R_ii| < 1e-11 ||Y||_F (100x above the 1e-13 threshold).
+int qr_cholqr3(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdiag_acc,
+               const double* fro, bool* fallback) {
+  cudaStream_t s = ctx->stream;
+  *fallback = false;
+  int lwork = 0;
+  CK_SOLVER(cusolverDnZpotrf_bufferSize(ctx->solver, CUBLAS_FILL_MODE_UPPER, n,
+                                        reinterpret_cast<cuDoubleComplex*>(g), n, &lwork));
+  CK(ensure_ws(ctx, (size_t)lwork * sizeof(cuDoubleComplex)));
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+  // unit roundoff 2^-53; Fukaya's shift 11 (mn + n(n+1)) u ||Y||_2^2 with ||Y||_F >= ||Y||_2
+  const double shift_coef = 11.0 * ((double)m * n + (double)n * (n + 1)) * 1.1102230246251565e-16;
+  for (int pass = 0; pass < 3; ++pass) {
+    CK_BLAS(cublasZgemm(ctx->blas, CUBLAS_OP_C, CUBLAS_OP_N, n, n, m, &one,
+                        reinterpret_cast<const cuDoubleComplex*>(y), m,
+                        reinterpret_cast<const cuDoubleComplex*>(y), m, &zero,
+                        reinterpret_cast<cuDoubleComplex*>(g), n));
+    if (pass == 0) CK_CUDA(chfsi::add_diag_shift_launch(g, n, n, fro, shift_coef, s));
+    CK_SOLVER(cusolverDnZpotrf(ctx->solver, CUBLAS_FILL_MODE_UPPER, n,
+                               reinterpret_cast<cuDoubleComplex*>(g), n,
+                               static_cast<cuDoubleComplex*>(ctx->ws), lwork, ctx->dinfo + pass));
+    CK_CUDA(chfsi::diag_accumulate_launch(g, n, n, rdiag_acc, pass == 0, s));
+    CK_BLAS(cublasZtrsm(ctx->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
+                        CUBLAS_DIAG_NON_UNIT, m, n, &one, reinterpret_cast<const cuDoubleComplex*>(g),
+                        n, reinterpret_cast<cuDoubleComplex*>(y), m));
+  }
+  std::vector<double> hd(n);
+  int info[3] = {0, 0, 0};
+  double hfro = 0.0;
+  CK_CUDA(cudaMemcpyAsync(hd.data(), rdiag_acc, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK_CUDA(cudaMemcpyAsync(info, ctx->dinfo, sizeof(info), cudaMemcpyDeviceToHost, s));
+  CK_CUDA(cudaMemcpyAsync(&hfro, fro, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK_CUDA(cudaStreamSynchronize(s));
+  if (info[0] || info[1] || info[2] || !std::isfinite(hfro)) {
+    *fallback = true;
+    return CHFSI_OK;
+  }
+  const double safe = 1e-11 * hfro;
+  for (int j = 0; j < n; ++j)
+    if (!(hd[j] >= safe)) {  // also catches NaN
+      *fallback = true;
+      return CHFSI_OK;
+    }
+  return CHFSI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int chfsi_qr_orthonormalize_z(chfsi_ctx* ctx, int m, int n, void* Y, long long ldy, int* dead,
+                              int* ndead) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(m >= n && n >= 0, "need rows >= cols");
+  CK_ARG(ndead && dead, "NULL output");
+  *ndead = 0;
+  if (n == 0) return CHFSI_OK;
+  CK_ARG(ldy == m, "QR needs a packed block (ldy == m)");
+  cudaStream_t s = ctx->stream;
+  double2* y = static_cast<double2*>(Y);
+  // scratch: backup copy of Y (m*n), tau (n), rdiag (n), Gram (n*n), diag accumulator (n)
+  const size_t blk = (size_t)m * n * sizeof(double2);
+  CK(ensure_scratch(ctx, blk + 2 * (size_t)n * sizeof(double2) + (size_t)n * n * sizeof(double2) +
+                             (size_t)n * sizeof(double)));
+  double2* backup = static_cast<double2*>(ctx->scratch);
+  double2* tau = backup + (size_t)m * n;
+  double2* rdiag = tau + n;
+  double2* g = rdiag + n;
+  double* racc = reinterpret_cast<double*>(g + (size_t)n * n);
+  double* fro = ctx->scalars + 1;
+  CK_CUDA(cudaMemcpyAsync(backup, y, blk, cudaMemcpyDeviceToDevice, s));
+  CK_CUDA(chfsi::norm2_launch(y, (long long)m * n, ctx->partial, fro, nullptr, s));
+  if (ctx->qr_mode != 1) {  // 0: Cholesky-QR3 first, 1: Householder only
+    bool fallback = false;
+    CK(qr_cholqr3(ctx, m, n, y, g, racc, fro, &fallback));
+    if (!fallback) return CHFSI_OK;
+    CK_CUDA(cudaMemcpyAsync(y, backup, blk, cudaMemcpyDeviceToDevice, s));
+  }
+  return qr_householder(ctx, m, n, y, backup, tau, rdiag, fro, dead, ndead);
+}
+
+int chfsi_ctx_set_qr_mode(chfsi_ctx* ctx, int mode) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(mode == 0 || mode == 1, "qr mode must be 0 (Cholesky-QR3 + fallback) or 1 (Householder)");
+  ctx->qr_mode = mode;
   return CHFSI_OK;
 }
 

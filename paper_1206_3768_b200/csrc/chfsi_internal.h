@@ -89,6 +89,12 @@ cudaError_t phase_fix_launch(double2* q, long long ldq, int m, int n, const doub
 // diag[j] = A[j, j]
 cudaError_t extract_diag_launch(const double2* a, long long lda, int n, double2* diag,
                                 cudaStream_t s);
+// A[i,i] += coef * (*fro)^2  (shifted Cholesky-QR)
+cudaError_t add_diag_shift_launch(double2* a, long long lda, int n, const double* fro, double coef,
+                                  cudaStream_t s);
+// acc[i] = (first ? 1 : acc[i]) * Re(R[i,i])
+cudaError_t diag_accumulate_launch(const double2* r, long long ldr, int n, double* acc, bool first,
+                                   cudaStream_t s);
 // y = x / *d (complex / real, round-to-nearest division)
 cudaError_t div_scalar_launch(const double2* x, const double* d, double2* y, int n, cudaStream_t s);
 // Y[:, j] = X[:, j]

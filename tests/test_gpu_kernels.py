@@ -186,6 +186,38 @@ def test_qr_matches_reference_golden(pkg, small_golden, name):
         np.testing.assert_allclose(q, small_golden[f"qr/{name}/q"], rtol=0, atol=1e-12)
 
 
+def set_qr_mode(mode):
+    L = _lib()
+    L.check(L.lib().chfsi_ctx_set_qr_mode(L.ctx(), mode))
+
+
+@pytest.mark.parametrize("kind", ["random", "graded", "near_dependent", "tall"])
+def test_cholqr3_matches_householder(pkg, kind):
+    """Shifted Cholesky-QR3 (default) vs Householder: the same unique Q
+    (positive-real R diagonal) to rounding x cond, orthonormal to 1e-13."""
+    rng = np.random.default_rng(31)
+    m, n = (4000, 24) if kind == "tall" else (300, 40)
+    y = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
+    cond = 1.0
+    if kind == "graded":  # filtered-panel-like column scales down to 1e-9
+        y = y * np.logspace(0, -9, n)
+        cond = 1e9
+    elif kind == "near_dependent":
+        y[:, 7] = y[:, 3] + 1e-8 * y[:, 7]
+        cond = 1e8
+    try:
+        set_qr_mode(1)
+        qh = pkg.qr_orthonormalize(y).cpu().numpy()
+        set_qr_mode(0)
+        qc = pkg.qr_orthonormalize(y).cpu().numpy()
+    finally:
+        set_qr_mode(0)
+    assert np.abs(qc.conj().T @ qc - np.eye(n)).max() <= 1e-13
+    assert np.abs(qc - qh).max() <= 1e-13 * cond * 10
+    ref = orc.qr_orthonormalize(y)
+    assert np.abs(qc - ref).max() <= 1e-13 * cond * 10
+
+
 def test_qr_idempotent_on_orthonormal_input(pkg):
     rng = np.random.default_rng(17)
     q0 = orc.qr_orthonormalize(rng.standard_normal((90, 12)) + 1j * rng.standard_normal((90, 12)))
