@@ -35,6 +35,7 @@
 #include <cuda.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "chfsi_internal.h"
 #include "common.cuh"
@@ -67,6 +68,7 @@ struct StepParams {
   double* partials;    // [grid][ACC][THREADS]
   unsigned* flags;     // [grid]
   unsigned epoch;
+  int dbg;             // diagnostics (CHFSI_K1_DEBUG): 1 = block barrier before each refill
 };
 
 // ------------------------------------------------------------ PTX helpers ---
@@ -316,9 +318,15 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
         }
       }
     }
-    // release the stage; the elected thread refills it once every warp has
+    // Release the stage; the elected thread refills it once every warp has.
+    // The fragments were read through the generic proxy (LDS) and the refill
+    // is an async-proxy (TMA) write of the same bytes: the proxy fence makes
+    // the reads complete before the release (without it ptxas schedules the
+    // arrive ahead of the last LDS and a slow warp can read refilled data).
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * stage);
+    if (p.dbg & 1) __syncthreads();
     if (tid == 0 && lc.j < total) {
       mbar_wait(empty0 + 8 * stage, phase);
       issue(lc, stage);
@@ -336,6 +344,7 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
     const bool tile_end = cc.kk == kiters - 1;
     const bool pub_end = pub > 0 && j == pub - 1;
     if (tile_end || pub_end) {
+      if (p.dbg & 4) __syncthreads();
       if (pub_end) {
         // non-owner: publish the partial head of this CTA's last tile
         double* dst = p.partials + (size_t)cta * ACC * THREADS + tid;
@@ -514,7 +523,14 @@ cudaError_t cheb_step_launch(const double2* h, long long ldh, bool conj_h, const
   const int tiles_m = (n + v.bm - 1) / v.bm;
   const long long tiles = (long long)tiles_m * p.tiles_n;
   p.kiters = (n + BK - 1) / BK;
+  static const int dbg = [] {
+    const char* e = getenv("CHFSI_K1_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  p.dbg = dbg;
+  if ((dbg & 2) && tiles <= grid) grid = (int)tiles;  // one whole tile per CTA, no stream-K
   p.dp_waves = tiles >= 2LL * grid ? (int)(tiles / grid) - 1 : 0;
+  if ((dbg & 2) && tiles == grid) p.dp_waves = 1;
   p.sk_first = p.dp_waves * grid;
   p.sk_iters = (tiles - p.sk_first) * p.kiters;
   p.sk_ctas = (int)(p.sk_iters < grid ? p.sk_iters : grid);
