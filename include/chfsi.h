@@ -96,6 +96,10 @@ CHFSI_API int chfsi_lanczos_z(chfsi_ctx* ctx, int n, int k, const void* H, long 
                     const void* q0, void* basis, double* alphas, double* betas,
                     double* beta_last, int* steps);
 
+/* Lanczos implementation (tests/tuning): 0 = one cooperative persistent
+ * kernel for all k steps (default); 1 = one launch per operation. */
+CHFSI_API int chfsi_ctx_set_lanczos_mode(chfsi_ctx* ctx, int mode);
+
 /* ------------------------------------------------------- K3 / K4 (RR) ---
  * Plain ZGEMM C = alpha op(A) op(B) + beta C (cuBLAS; trans 'N','T','C'). */
 CHFSI_API int chfsi_gemm_z(chfsi_ctx* ctx, char transa, char transb, int m, int n, int k, double alpha_re,

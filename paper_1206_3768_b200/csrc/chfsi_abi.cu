@@ -37,6 +37,7 @@ struct chfsi_ctx {
   chfsi::StepTiling tiling{0, 0, 0};  // K1 tile override (bm == 0: automatic)
   chfsi::StepWorkspace step_ws{nullptr, nullptr, nullptr, 0};
   int qr_mode = 0;  // 0: shifted Cholesky-QR3 with Householder fallback; 1: Householder
+  int lanczos_mode = 0;  // 0: cooperative single kernel; 1: one launch per operation
   unsigned step_epoch = 0;
 };
 
@@ -283,7 +284,27 @@ int chfsi_lanczos_z(chfsi_ctx* ctx, int n, int k, const void* H, long long ldh, 
   CK_ARG(ctx, "ctx is NULL");
   CK_ARG(n >= 1 && k >= 1 && k <= n, "need 1 <= k <= n");
   CK_ARG(H && q0 && basis && alphas && betas && beta_last && steps, "NULL argument");
-  // scratch: u, r (n each), coef (k), alphas_d, betas_d (k doubles each)
+  if (ctx->lanczos_mode == 0) {  // one cooperative persistent kernel (lanczos.cu)
+    const size_t ws = chfsi::lanczos_coop_workspace_bytes(n, k);
+    CK(ensure_scratch(ctx, ws + 2 * (size_t)k * sizeof(double) + 256));
+    double* al_d = reinterpret_cast<double*>(static_cast<char*>(ctx->scratch) + ws);
+    double* be_d = al_d + k;
+    cudaStream_t s = ctx->stream;
+    CK_CUDA(cudaMemsetAsync(ctx->lstate, 0, sizeof(LanczosState), s));
+    CK_CUDA(cudaMemsetAsync(be_d, 0, (size_t)k * sizeof(double), s));
+    CK_CUDA(chfsi::lanczos_coop_launch(static_cast<const double2*>(H), ldh, conj_h != 0, n, k,
+                                       static_cast<const double2*>(q0), static_cast<double2*>(basis),
+                                       ctx->scratch, al_d, be_d, ctx->lstate, s));
+    LanczosState hst;
+    CK_CUDA(cudaMemcpyAsync(&hst, ctx->lstate, sizeof(hst), cudaMemcpyDeviceToHost, s));
+    CK_CUDA(cudaMemcpyAsync(alphas, al_d, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK_CUDA(cudaMemcpyAsync(betas, be_d, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK_CUDA(cudaStreamSynchronize(s));
+    *steps = hst.steps;
+    *beta_last = hst.beta_last;
+    return CHFSI_OK;
+  }
+  // multi-kernel path (reference for tests): u, r (n each), coef (k), alphas_d, betas_d (k)
   const size_t vec = (size_t)n * sizeof(double2);
   CK(ensure_scratch(ctx, 2 * vec + (size_t)k * sizeof(double2) + 2 * (size_t)k * sizeof(double) + 256));
   char* base = static_cast<char*>(ctx->scratch);
@@ -485,6 +506,13 @@ int chfsi_qr_orthonormalize_z(chfsi_ctx* ctx, int m, int n, void* Y, long long l
     CK_CUDA(cudaMemcpyAsync(y, backup, blk, cudaMemcpyDeviceToDevice, s));
   }
   return qr_householder(ctx, m, n, y, backup, tau, rdiag, fro, dead, ndead);
+}
+
+int chfsi_ctx_set_lanczos_mode(chfsi_ctx* ctx, int mode) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(mode == 0 || mode == 1, "lanczos mode must be 0 (cooperative) or 1 (multi-kernel)");
+  ctx->lanczos_mode = mode;
+  return CHFSI_OK;
 }
 
 int chfsi_ctx_set_qr_mode(chfsi_ctx* ctx, int mode) {

@@ -61,6 +61,12 @@ struct LanczosState {
   int steps;
   double beta_last;
 };
+// whole k-step Lanczos in one cooperative kernel (lanczos.cu)
+int lanczos_coop_grid();
+size_t lanczos_coop_workspace_bytes(int n, int k);
+cudaError_t lanczos_coop_launch(const double2* h, long long ldh, bool conj_h, int n, int k,
+                                const double2* q0, double2* V, void* ws, double* alphas,
+                                double* betas, LanczosState* st, cudaStream_t s);
 cudaError_t lanczos_residual_launch(const double2* u, const double2* q, const double2* qprev,
                                     const double* alpha_i, const double* beta_prev, double2* r,
                                     int n, const int* done, cudaStream_t s);

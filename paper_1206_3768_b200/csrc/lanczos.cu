@@ -1,0 +1,269 @@
+// K2 — the whole k-step Lanczos bound (reference chfsi.py:125-162) as ONE
+// cooperative persistent kernel.
+//
+// Per step: u = H q (HBM-bound GEMV, each block its own row range),
+// alpha = Re(q^H u), r = u - alpha q - beta q_prev, full reorthogonalisation
+// r -= V (V^H r), beta = ||r||, q_next = r / beta, with the breakdown test
+// beta < 1e-14 of chfsi.py:152. Five grid-wide barriers per step replace the
+// nine kernel launches of the multi-kernel version (launch latency dominated
+// it below n ~ 5000). Every reduction uses a fixed partition and a fixed
+// combining order (block partials summed in block order), so alphas/betas are
+// bitwise reproducible run to run.
+#include <cooperative_groups.h>
+
+#include "chfsi_internal.h"
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace chfsi {
+
+namespace {
+
+constexpr int LZ_THREADS = 256;
+constexpr int LZ_WARPS = LZ_THREADS / 32;
+
+struct LanczosParams {
+  const double2* h;
+  long long ldh;
+  int n, k;
+  const double2* q0;  // raw start vector (normalised here)
+  double2* V;         // n x k basis, column-major, ld n
+  double2* u;         // n
+  double2* r;         // n
+  double* part;       // [grid] scalar partials
+  double2* cpart;     // [grid][k] reorthogonalisation partials
+  double2* coef;      // [k]
+  double* alphas;     // [k]
+  double* betas;      // [k]
+  LanczosState* st;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// fixed-tree block sum, result broadcast to every thread
+__device__ double block_sum_all(double v, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (wid == 0) {
+    r = lane < LZ_WARPS ? sh[lane] : 0.0;
+    r = warp_sum(r);
+    if (lane == 0) sh[LZ_WARPS] = r;
+  }
+  __syncthreads();
+  r = sh[LZ_WARPS];
+  __syncthreads();
+  return r;
+}
+
+// sum of the G block partials in block order (every block gets the same bits)
+__device__ double grid_total(const double* part, int G, double* sh) {
+  double v = 0.0;
+  for (int b = threadIdx.x; b < G; b += LZ_THREADS) v += __ldcg(part + b);
+  return block_sum_all(v, sh);
+}
+
+template <bool CONJ>
+__global__ void __launch_bounds__(LZ_THREADS) lanczos_coop_kernel(const LanczosParams p) {
+  __shared__ double sh[LZ_WARPS + 1];
+  cg::grid_group grid = cg::this_grid();
+  const int G = gridDim.x, b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = p.n;
+  const int r0 = (int)((long long)n * b / G), r1 = (int)((long long)n * (b + 1) / G);
+
+  // ---- q = q0 / ||q0||  (chfsi.py:137-138)
+  double s = 0.0;
+  for (int i = r0 + tid; i < r1; i += LZ_THREADS) {
+    const double2 x = p.q0[i];
+    s = fma(x.x, x.x, fma(x.y, x.y, s));
+  }
+  s = block_sum_all(s, sh);
+  if (tid == 0) p.part[b] = s;
+  grid.sync();
+  const double nq = sqrt(grid_total(p.part, G, sh));
+  for (int i = r0 + tid; i < r1; i += LZ_THREADS) {
+    const double2 x = p.q0[i];
+    p.V[i] = make_double2(__ddiv_rn(x.x, nq), __ddiv_rn(x.y, nq));
+  }
+  grid.sync();
+
+  double beta_prev = 0.0;
+  for (int it = 0; it < p.k; ++it) {
+    const double2* q = p.V + (long long)it * n;
+    // ---- u = H q on this block's rows (warp per row), alpha partial
+    double ap = 0.0;
+    for (int row = r0 + warp; row < r1; row += LZ_WARPS) {
+      const double2* hr = p.h + (long long)row * p.ldh;
+      double sr = 0.0, si = 0.0;
+      int c = lane;
+      for (; c + 96 < n; c += 128) {
+        const double2 a0 = hr[c], a1 = hr[c + 32], a2 = hr[c + 64], a3 = hr[c + 96];
+        const double2 b0 = q[c], b1 = q[c + 32], b2 = q[c + 64], b3 = q[c + 96];
+        const double sg = CONJ ? -1.0 : 1.0;
+        sr = fma(a0.x, b0.x, fma(-sg * a0.y, b0.y, sr));
+        si = fma(a0.x, b0.y, fma(sg * a0.y, b0.x, si));
+        sr = fma(a1.x, b1.x, fma(-sg * a1.y, b1.y, sr));
+        si = fma(a1.x, b1.y, fma(sg * a1.y, b1.x, si));
+        sr = fma(a2.x, b2.x, fma(-sg * a2.y, b2.y, sr));
+        si = fma(a2.x, b2.y, fma(sg * a2.y, b2.x, si));
+        sr = fma(a3.x, b3.x, fma(-sg * a3.y, b3.y, sr));
+        si = fma(a3.x, b3.y, fma(sg * a3.y, b3.x, si));
+      }
+      for (; c < n; c += 32) {
+        const double2 a = hr[c], bb = q[c];
+        const double sg = CONJ ? -1.0 : 1.0;
+        sr = fma(a.x, bb.x, fma(-sg * a.y, bb.y, sr));
+        si = fma(a.x, bb.y, fma(sg * a.y, bb.x, si));
+      }
+      sr = warp_sum(sr);
+      si = warp_sum(si);
+      if (lane == 0) {
+        p.u[row] = make_double2(sr, si);
+        const double2 qv = q[row];
+        ap = fma(qv.x, sr, fma(qv.y, si, ap));  // Re(conj(q) u)
+      }
+    }
+    ap = block_sum_all(ap, sh);
+    if (tid == 0) p.part[b] = ap;
+    grid.sync();  // (1) alpha partials
+
+    const double alpha = grid_total(p.part, G, sh);
+    if (b == 0 && tid == 0) p.alphas[it] = alpha;
+    // ---- r = (u - alpha q) - beta_prev q_prev on own rows
+    const double2* qp = it ? p.V + (long long)(it - 1) * n : nullptr;
+    for (int i = r0 + tid; i < r1; i += LZ_THREADS) {
+      const double2 uu = p.u[i], qq = q[i];
+      double rr = dsub(uu.x, dmul(alpha, qq.x)), ri = dsub(uu.y, dmul(alpha, qq.y));
+      if (qp) {
+        const double2 pp = qp[i];
+        rr = dsub(rr, dmul(beta_prev, pp.x));
+        ri = dsub(ri, dmul(beta_prev, pp.y));
+      }
+      p.r[i] = make_double2(rr, ri);
+    }
+    __syncthreads();
+    // ---- reorthogonalisation partials: cpart[b][j] = V[own rows, j]^H r
+    for (int j = warp; j <= it; j += LZ_WARPS) {
+      const double2* vj = p.V + (long long)j * n;
+      double cr = 0.0, ci = 0.0;
+      for (int i = r0 + lane; i < r1; i += 32) {
+        const double2 a = vj[i], rv = p.r[i];
+        cr = fma(a.x, rv.x, fma(a.y, rv.y, cr));
+        ci = fma(a.x, rv.y, fma(-a.y, rv.x, ci));
+      }
+      cr = warp_sum(cr);
+      ci = warp_sum(ci);
+      if (lane == 0) p.cpart[(long long)b * p.k + j] = make_double2(cr, ci);
+    }
+    grid.sync();  // (2) partials complete
+
+    // ---- coef[j] = sum_b cpart[b][j] (block order), j spread over warps
+    for (int j = b * LZ_WARPS + warp; j <= it; j += G * LZ_WARPS) {
+      double cr = 0.0, ci = 0.0;
+      for (int bb = lane; bb < G; bb += 32) {
+        const double2 v = __ldcg(p.cpart + (long long)bb * p.k + j);
+        cr += v.x;
+        ci += v.y;
+      }
+      cr = warp_sum(cr);
+      ci = warp_sum(ci);
+      if (lane == 0) p.coef[j] = make_double2(cr, ci);
+    }
+    grid.sync();  // (3) coefficients complete
+
+    // ---- r -= V coef (fixed j order), beta partial
+    double bp = 0.0;
+    for (int i = r0 + tid; i < r1; i += LZ_THREADS) {
+      double sr = 0.0, si = 0.0;
+      for (int j = 0; j <= it; ++j) {
+        const double2 a = p.V[(long long)j * n + i], c = __ldcg(p.coef + j);
+        sr = fma(a.x, c.x, fma(-a.y, c.y, sr));
+        si = fma(a.x, c.y, fma(a.y, c.x, si));
+      }
+      const double2 rv = p.r[i];
+      const double2 nr = make_double2(rv.x - sr, rv.y - si);
+      p.r[i] = nr;
+      bp = fma(nr.x, nr.x, fma(nr.y, nr.y, bp));
+    }
+    bp = block_sum_all(bp, sh);
+    if (tid == 0) p.part[b] = bp;
+    grid.sync();  // (4) beta partials
+
+    const double beta = sqrt(grid_total(p.part, G, sh));
+    const bool stop = (beta < 1e-14) || (it == p.k - 1);  // chfsi.py:152
+    if (b == 0 && tid == 0) {
+      p.st->steps = it + 1;
+      p.st->beta_last = beta;
+      if (stop) p.st->done = 1;
+      else p.betas[it] = beta;
+    }
+    if (stop) break;
+    double2* qn = p.V + (long long)(it + 1) * n;
+    for (int i = r0 + tid; i < r1; i += LZ_THREADS) {
+      const double2 x = p.r[i];
+      qn[i] = make_double2(__ddiv_rn(x.x, beta), __ddiv_rn(x.y, beta));
+    }
+    beta_prev = beta;
+    grid.sync();  // (5) q_next complete before the next GEMV
+  }
+}
+
+}  // namespace
+
+size_t lanczos_coop_workspace_bytes(int n, int k) {
+  const int G = lanczos_coop_grid();
+  return 2 * (size_t)n * sizeof(double2) + (size_t)G * sizeof(double) +
+         (size_t)G * k * sizeof(double2) + (size_t)k * sizeof(double2) + 256;
+}
+
+int lanczos_coop_grid() {
+  static int grid = [] {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lanczos_coop_kernel<false>, LZ_THREADS, 0);
+    int occ2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, lanczos_coop_kernel<true>, LZ_THREADS, 0);
+    if (occ2 < occ) occ = occ2;
+    if (occ > 2) occ = 2;  // enough bytes in flight for the GEMV; fewer partials
+    return (occ > 0 ? occ : 1) * kNumSMs;
+  }();
+  return grid;
+}
+
+cudaError_t lanczos_coop_launch(const double2* h, long long ldh, bool conj_h, int n, int k,
+                                const double2* q0, double2* V, void* ws, double* alphas,
+                                double* betas, LanczosState* st, cudaStream_t s) {
+  const int G = lanczos_coop_grid();
+  LanczosParams p{};
+  p.h = h;
+  p.ldh = ldh;
+  p.n = n;
+  p.k = k;
+  p.q0 = q0;
+  p.V = V;
+  char* base = static_cast<char*>(ws);
+  p.u = reinterpret_cast<double2*>(base);
+  p.r = p.u + n;
+  p.cpart = p.r + n;
+  p.coef = p.cpart + (size_t)G * k;
+  p.part = reinterpret_cast<double*>(p.coef + k);
+  p.alphas = alphas;
+  p.betas = betas;
+  p.st = st;
+  void* args[] = {&p};
+  note_launch();
+  if (conj_h)
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(lanczos_coop_kernel<true>),
+                                       dim3(G), dim3(LZ_THREADS), args, 0, s);
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(lanczos_coop_kernel<false>),
+                                     dim3(G), dim3(LZ_THREADS), args, 0, s);
+}
+
+}  // namespace chfsi

@@ -171,6 +171,34 @@ def test_lanczos_matches_reference_golden(pkg, small_golden, name):
     assert abs(bound - float(small_golden[f"lanczos/{name}/bound"])) <= 1e-10
 
 
+@pytest.mark.parametrize("n,k", [(2048, 204), (777, 60), (300, 300)])
+def test_lanczos_cooperative_matches_multikernel(pkg, n, k):
+    """The single cooperative kernel and the one-launch-per-operation path
+    run the same algorithm: same step count, Ritz values to rounding."""
+    from paper_1206_3768_b200.chfsi import _lanczos_estimates
+    from paper_1206_3768_b200._device import Operator
+
+    L = _lib()
+    h = random_hermitian(np.random.default_rng(n), n)
+    op = Operator(h)
+    runs = {}
+    try:
+        for mode in (1, 0, 0):
+            L.check(L.lib().chfsi_ctx_set_lanczos_mode(L.ctx(), mode))
+            runs.setdefault(mode, []).append(_lanczos_estimates(op, k, np.random.default_rng(9)))
+    finally:
+        L.check(L.lib().chfsi_ctx_set_lanczos_mode(L.ctx(), 0))
+    (r1, b1, s1), = runs[1]
+    (r0, b0, s0), (r0b, b0b, s0b) = runs[0]
+    assert s0 == s1 == s0b
+    np.testing.assert_allclose(r0, r1, rtol=0, atol=1e-11)
+    assert abs(b0 - b1) <= 1e-11
+    assert np.array_equal(r0, r0b) and b0 == b0b  # bitwise run to run
+    ritz_np, last_np, steps_np = orc.lanczos(h, k, np.random.default_rng(9))
+    assert steps_np == s0
+    np.testing.assert_allclose(r0, ritz_np, rtol=0, atol=1e-10)
+
+
 def test_lanczos_rejects_too_few_steps(pkg):
     with pytest.raises(ValueError):
         pkg.lanczos_upper_bound(np.eye(3, dtype=complex), 1)
