@@ -130,6 +130,15 @@ CHFSI_API int chfsi_ctx_set_qr_mode(chfsi_ctx* ctx, int mode);
  * DEVICE array w, eigenvectors overwrite A. */
 CHFSI_API int chfsi_heevd_z(chfsi_ctx* ctx, int n, void* A, long long lda, double* w);
 
+/* Rayleigh-Ritz eigensolver (chfsi.py:347): when G is near-diagonal (max
+ * |G_ij| / |G_jj - G_ii| <= 0.25, the regime of every ChFSI loop after the
+ * first few) it runs simultaneous first-order Jacobi steps (ZGEMM +
+ * Newton-Schulz) until max|G_ij| <= tol * max(1, max|G_ii|) and sets
+ * *used_fast = 1; otherwise, or if that fails, it is exactly chfsi_heevd_z.
+ * tol <= 0 forces zheevd. Same outputs as chfsi_heevd_z. */
+CHFSI_API int chfsi_heev_rr_z(chfsi_ctx* ctx, int n, void* A, long long lda, double* w, double tol,
+                              int* used_fast);
+
 /* res[j] = || HP[:,j] - lambda[j] P[:,j] ||_2 (chfsi.py:350); device arrays.
  * P and lambda may be NULL (plain column norms). */
 CHFSI_API int chfsi_colnorm_residual_z(chfsi_ctx* ctx, int n, int w, const void* HP, long long ldhp,

@@ -71,6 +71,7 @@ _SIGNATURES = {
     "chfsi_ctx_set_qr_mode": [_vp, _i],
     "chfsi_ctx_set_lanczos_mode": [_vp, _i],
     "chfsi_heevd_z": [_vp, _i, _vp, _ll, _vp],
+    "chfsi_heev_rr_z": [_vp, _i, _vp, _ll, _vp, _d, _pi],
     "chfsi_colnorm_residual_z": [_vp, _i, _i, _vp, _ll, _vp, _ll, _vp, _vp],
     "chfsi_symmetrize_z": [_vp, _i, _vp, _ll],
     "chfsi_herm_defect_z": [_vp, _i, _vp, _ll, _pd, _pd],

@@ -142,6 +142,7 @@ class SolveReport:
     t_rr: float = 0.0
     filter_flops: float = 0.0
     filter_launches: int = 0
+    rr_fast_eigs: int = 0
     tail_vectors: object = None
     lambda_blk_plus_1: float = float("nan")
 
@@ -279,18 +280,29 @@ def _gemm(ta, tb, m, n, k, a, b, c, alpha=1.0, beta=0.0):
                              ld_of(b), beta, 0.0, dptr(c), ld_of(c)), "zgemm")
 
 
-def _rr_core(op, panel, hp, g, rot_p, rot_hp, ritz_d, res_d):
-    """HP = H P; G = P^H HP, symmetrized; zheevd; P W, HP W; residual norms
-    (chfsi.py:341-350). All device; returns nothing (results in buffers)."""
+# Off-diagonal target of the near-diagonal Rayleigh-Ritz eigensolver, relative
+# to max|G_ii|: its remainder enters the Ritz residuals directly, so it must sit
+# far below the locking tolerance (1e-13 * ||G|| vs tol = 1e-10 at BASELINE).
+RR_FAST_TOL = 1e-13
+
+
+def _rr_core(op, panel, hp, g, rot_p, rot_hp, ritz_d, res_d, eig_tol=0.0):
+    """HP = H P; G = P^H HP, symmetrized; eigendecomposition; P W, HP W;
+    residual norms (chfsi.py:341-350). All device. With ``eig_tol > 0`` the
+    near-diagonal Jacobi/ZGEMM eigensolver is tried before zheevd. Returns
+    True when it was used."""
     n, w = panel.shape
     _apply_h(op, panel, hp)
     _gemm(b"C", b"N", w, w, n, panel, hp, g)
     check(lib().chfsi_symmetrize_z(ctx(), w, dptr(g), ld_of(g)), "symmetrize")
-    check(lib().chfsi_heevd_z(ctx(), w, dptr(g), ld_of(g), dptr(ritz_d)), "hermitian_eig")
+    used = ctypes.c_int(0)
+    check(lib().chfsi_heev_rr_z(ctx(), w, dptr(g), ld_of(g), dptr(ritz_d), float(eig_tol),
+                                ctypes.byref(used)), "hermitian_eig")
     _gemm(b"N", b"N", n, w, w, panel, g, rot_p)
     _gemm(b"N", b"N", n, w, w, hp, g, rot_hp)
     check(lib().chfsi_colnorm_residual_z(ctx(), n, w, dptr(rot_hp), ld_of(rot_hp), dptr(rot_p),
                                          ld_of(rot_p), dptr(ritz_d), dptr(res_d)), "residuals")
+    return bool(used.value)
 
 
 def rayleigh_ritz(h, y):
@@ -396,6 +408,7 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1):
     locked_res: list[float] = []
     nlocked = 0
     pb, off, width = 0, 0, blk   # panel = bufs[pb][:, off:off+width]
+    try_fast = guess is not None  # warm panels give near-diagonal projections
     ritz_vals = np.zeros(0)
     rot_p = None
     n_lock = 0
@@ -420,8 +433,14 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1):
         t_r.start()
         rot_buf = bufs[pb] if q_in_other else bufs[1 - pb]
         rot_p = rot_buf[:, :width]  # free: disjoint from Q by construction
-        _rr_core(op, filtered, hp_buf[:, :width], g_buf[:width, :width], rot_p,
-                 hp_rot[:, :width], ritz_d[:width], res_d[:width])
+        # near-diagonal eigensolver once the panel is close to invariant (warm
+        # starts, or after the first locking); zheevd otherwise
+        fast = _rr_core(op, filtered, hp_buf[:, :width], g_buf[:width, :width], rot_p,
+                        hp_rot[:, :width], ritz_d[:width], res_d[:width],
+                        eig_tol=RR_FAST_TOL if (try_fast and tol >= 1e-11) else 0.0)
+        report.rr_fast_eigs += int(fast)
+        if try_fast and not fast:
+            try_fast = False
         report.residual_check_matvecs += width
         report.matvecs += width
         host = torch.cat([ritz_d[:width], res_d[:width]]).cpu().numpy()
@@ -432,6 +451,7 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1):
         while n_lock < width and nlocked + n_lock < cfg.nev and res[n_lock] < tol:
             n_lock += 1
         if n_lock:
+            try_fast = True
             locked_vals.extend(float(v) for v in ritz_vals[:n_lock])
             locked_res.extend(float(r) for r in res[:n_lock])
             locked[:, nlocked:nlocked + n_lock].copy_(rot_p[:, :n_lock])

@@ -5,6 +5,7 @@
 #include <cusolverDn.h>
 
 #include <atomic>
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -29,6 +30,8 @@ struct chfsi_ctx {
   void* ws = nullptr;  // cuSOLVER workspace (grown on demand)
   size_t ws_bytes = 0;
   void* scratch = nullptr;  // n-sized vectors (grown on demand)
+  void* eig_ws = nullptr;   // near-diagonal eigensolver work (grown on demand)
+  size_t eig_ws_bytes = 0;
   size_t scratch_bytes = 0;
   double* partial = nullptr;  // kRedBlocks doubles
   double* scalars = nullptr;  // 16 doubles
@@ -164,6 +167,7 @@ int chfsi_ctx_destroy(chfsi_ctx* ctx) {
   if (ctx->solver) cusolverDnDestroy(ctx->solver);
   cudaFree(ctx->ws);
   cudaFree(ctx->scratch);
+  cudaFree(ctx->eig_ws);
   cudaFree(ctx->partial);
   cudaFree(ctx->scalars);
   cudaFree(ctx->dinfo);
@@ -520,6 +524,110 @@ int chfsi_ctx_set_qr_mode(chfsi_ctx* ctx, int mode) {
   CK_ARG(mode == 0 || mode == 1, "qr mode must be 0 (Cholesky-QR3 + fallback) or 1 (Householder)");
   ctx->qr_mode = mode;
   return CHFSI_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Near-diagonal Hermitian eigensolver (nd_eig.cu): simultaneous first-order
+// Jacobi steps X = I + S, S_ij = G_ij / (d_j - d_i), made unitary by two
+// Newton-Schulz polar iterations, G <- X^H G X, W <- W X. Converges
+// quadratically in max|G_ij| / gap. *done = false (A untouched) when G is not
+// in that regime or does not reach max|G_ij| <= tol * max(1, max|G_ii|).
+int heev_near_diag(chfsi_ctx* ctx, int n, double2* a, long long lda, double* w, double tol,
+                   bool* done) {
+  *done = false;
+  cudaStream_t s = ctx->stream;
+  const size_t mat = (size_t)n * n * sizeof(double2);
+  constexpr int kMaxIt = 6;
+  const size_t need = 5 * mat + (kMaxIt + 1) * 4 * sizeof(double) + (size_t)n * sizeof(int) + 1024;
+  if (need > ctx->eig_ws_bytes) {
+    CK_CUDA(cudaStreamSynchronize(s));
+    if (ctx->eig_ws) CK_CUDA(cudaFree(ctx->eig_ws));
+    ctx->eig_ws = nullptr;
+    ctx->eig_ws_bytes = 0;
+    CK_CUDA(cudaMalloc(&ctx->eig_ws, need));
+    ctx->eig_ws_bytes = need;
+  }
+  double2* G = reinterpret_cast<double2*>(ctx->eig_ws);  // working copy, ld n
+  double2* X = G + (size_t)n * n;
+  double2* T = X + (size_t)n * n;
+  double2* Y = T + (size_t)n * n;
+  double2* W = Y + (size_t)n * n;
+  double* stats = reinterpret_cast<double*>(W + (size_t)n * n);  // [it][4]
+  int* perm = reinterpret_cast<int*>(stats + (kMaxIt + 1) * 4);
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+  auto gemm = [&](cublasOperation_t ta, const double2* A_, const double2* B_, double2* C_) -> int {
+    CK_BLAS(cublasZgemm(ctx->blas, ta, CUBLAS_OP_N, n, n, n, &one,
+                        reinterpret_cast<const cuDoubleComplex*>(A_), n,
+                        reinterpret_cast<const cuDoubleComplex*>(B_), n, &zero,
+                        reinterpret_cast<cuDoubleComplex*>(C_), n));
+    return CHFSI_OK;
+  };
+  CK_CUDA(cudaMemcpy2DAsync(G, (size_t)n * sizeof(double2), a, (size_t)lda * sizeof(double2),
+                            (size_t)n * sizeof(double2), n, cudaMemcpyDeviceToDevice, s));
+  CK_CUDA(cudaMemsetAsync(stats, 0, (kMaxIt + 1) * 4 * sizeof(double), s));
+  int it = 0;
+  int checked = 0;
+  std::vector<double> hs((kMaxIt + 1) * 4);
+  for (;;) {
+    // one simultaneous Jacobi step
+    CK_CUDA(chfsi::nd_build_step_launch(G, n, n, X, n, stats + 4 * it, s));
+    for (int ns = 0; ns < 2; ++ns) {  // X <- X (3I - X^H X) / 2
+      CK(gemm(CUBLAS_OP_C, X, X, T));
+      CK_CUDA(chfsi::nd_ns_matrix_launch(T, n, n, s));
+      CK(gemm(CUBLAS_OP_N, X, T, Y));
+      std::swap(X, Y);
+    }
+    CK(gemm(CUBLAS_OP_N, G, X, Y));  // Y = G X
+    CK(gemm(CUBLAS_OP_C, X, Y, G));  // G = X^H G X
+    CK_CUDA(chfsi::symmetrize_launch(G, n, n, s));
+    if (it == 0) {
+      std::swap(W, X);  // W = X
+    } else {
+      CK(gemm(CUBLAS_OP_N, W, X, Y));
+      std::swap(W, Y);
+    }
+    ++it;
+    if (it < 3 && it < kMaxIt) continue;
+    // measure the remaining off-diagonal (stats[it]) and decide
+    CK_CUDA(chfsi::nd_build_step_launch(G, n, n, X, n, stats + 4 * it, s));
+    CK_CUDA(cudaMemcpyAsync(hs.data(), stats, hs.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK_CUDA(cudaStreamSynchronize(s));
+    ++checked;
+    const double rmax0 = hs[0], emax = hs[4 * it + 1], dmax = hs[4 * it + 2];
+    if (!(rmax0 <= 0.25)) return CHFSI_OK;  // not near-diagonal: caller uses zheevd
+    if (emax <= tol * std::max(1.0, dmax)) break;
+    if (it >= kMaxIt || !(hs[4 * it] < hs[4 * (it - 1)])) return CHFSI_OK;  // stalled
+  }
+  // ascending eigenvalues, eigenvectors permuted accordingly, back into A
+  CK_CUDA(chfsi::nd_sort_launch(G, n, n, w, perm, s));
+  CK_CUDA(chfsi::nd_gather_cols_launch(W, n, n, n, perm, a, lda, s));
+  *done = true;
+  return CHFSI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int chfsi_heev_rr_z(chfsi_ctx* ctx, int n, void* A, long long lda, double* w, double tol,
+                    int* used_fast) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(used_fast, "used_fast is NULL");
+  *used_fast = 0;
+  if (n == 0) return CHFSI_OK;
+  CK_ARG(A && w && lda >= n, "bad argument");
+  if (tol > 0.0 && n > 1) {
+    bool done = false;
+    CK(heev_near_diag(ctx, n, static_cast<double2*>(A), lda, w, tol, &done));
+    if (done) {
+      *used_fast = 1;
+      return CHFSI_OK;
+    }
+  }
+  return chfsi_heevd_z(ctx, n, A, lda, w);
 }
 
 int chfsi_heevd_z(chfsi_ctx* ctx, int n, void* A, long long lda, double* w) {

@@ -101,6 +101,14 @@ cudaError_t add_diag_shift_launch(double2* a, long long lda, int n, const double
 // acc[i] = (first ? 1 : acc[i]) * Re(R[i,i])
 cudaError_t diag_accumulate_launch(const double2* r, long long ldr, int n, double* acc, bool first,
                                    cudaStream_t s);
+// near-diagonal Hermitian eigensolver pieces (nd_eig.cu)
+cudaError_t nd_build_step_launch(const double2* g, long long ldg, int n, double2* x, long long ldx,
+                                 double* stats, cudaStream_t s);
+cudaError_t nd_ns_matrix_launch(double2* t, long long ldt, int n, cudaStream_t s);
+cudaError_t nd_sort_launch(const double2* g, long long ldg, int n, double* w, int* perm,
+                           cudaStream_t s);
+cudaError_t nd_gather_cols_launch(const double2* src, long long lds, int m, int n, const int* perm,
+                                  double2* out, long long ldo, cudaStream_t s);
 // y = x / *d (complex / real, round-to-nearest division)
 cudaError_t div_scalar_launch(const double2* x, const double* d, double2* y, int n, cudaStream_t s);
 // Y[:, j] = X[:, j]

@@ -267,6 +267,33 @@ def test_hermitian_eig(pkg, n):
     assert np.abs(g @ v - v * vals).max() <= 1e-11 * max(1, n)
 
 
+@pytest.mark.parametrize("n,off", [(48, 1e-4), (160, 1e-6), (301, 1e-5), (160, 0.3)])
+def test_near_diagonal_eigensolver(pkg, n, off):
+    """chfsi_heev_rr_z: near-diagonal G (the RR regime after the first loops)
+    goes through the Jacobi/ZGEMM path; a far-from-diagonal G must fall back
+    to zheevd. Either way: ascending values and an orthonormal eigenbasis
+    matching numpy to rounding."""
+    from paper_1206_3768_b200._device import to_fblock, ld_of
+
+    L = _lib()
+    rng = np.random.default_rng(n)
+    d = np.sort(rng.uniform(-1, 9, n))
+    e = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) * off
+    g = np.diag(d) + (e + e.conj().T) / 2
+    gd = to_fblock(g, copy=True)
+    w = torch.empty(n, dtype=torch.float64, device="cuda")
+    used = ctypes.c_int()
+    L.check(L.lib().chfsi_heev_rr_z(L.ctx(), n, L.dptr(gd), ld_of(gd), L.dptr(w), 1e-13,
+                                    ctypes.byref(used)))
+    assert used.value == (1 if off < 0.01 else 0)
+    vals, v = w.cpu().numpy(), gd.cpu().numpy()
+    ref = np.linalg.eigvalsh(g)
+    assert np.all(np.diff(vals) >= 0)
+    np.testing.assert_allclose(vals, ref, rtol=0, atol=1e-12 * np.abs(ref).max())
+    assert np.abs(v.conj().T @ v - np.eye(n)).max() <= 1e-12
+    assert np.abs(g @ v - v * vals).max() <= 1e-12 * np.abs(ref).max()
+
+
 def test_hermitian_view_rejects_asymmetric(pkg):
     rng = np.random.default_rng(5)
     m = rng.standard_normal((6, 6)) + 1j * rng.standard_normal((6, 6))
