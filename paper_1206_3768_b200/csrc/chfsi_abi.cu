@@ -542,6 +542,7 @@ int heev_near_diag(chfsi_ctx* ctx, int n, double2* a, long long lda, double* w, 
   const size_t mat = (size_t)n * n * sizeof(double2);
   constexpr int kMaxIt = 6;
   const size_t need = 5 * mat + (kMaxIt + 1) * 4 * sizeof(double) + (size_t)n * sizeof(int) + 1024;
+  static_assert(kMaxIt >= 5, "two rounds of steps plus measurements");
   if (need > ctx->eig_ws_bytes) {
     CK_CUDA(cudaStreamSynchronize(s));
     if (ctx->eig_ws) CK_CUDA(cudaFree(ctx->eig_ws));
@@ -550,12 +551,12 @@ int heev_near_diag(chfsi_ctx* ctx, int n, double2* a, long long lda, double* w, 
     CK_CUDA(cudaMalloc(&ctx->eig_ws, need));
     ctx->eig_ws_bytes = need;
   }
-  double2* G = reinterpret_cast<double2*>(ctx->eig_ws);  // working copy, ld n
+  double2* G0 = reinterpret_cast<double2*>(ctx->eig_ws);  // the input, kept for the exact projection
+  double2* G = G0 + (size_t)n * n;                          // working iterate
   double2* X = G + (size_t)n * n;
-  double2* T = X + (size_t)n * n;
-  double2* Y = T + (size_t)n * n;
-  double2* W = Y + (size_t)n * n;
-  double* stats = reinterpret_cast<double*>(W + (size_t)n * n);  // [it][4]
+  double2* Y = X + (size_t)n * n;
+  double2* W = Y + (size_t)n * n;                           // accumulated eigenvector basis
+  double* stats = reinterpret_cast<double*>(W + (size_t)n * n);  // [step][4]
   int* perm = reinterpret_cast<int*>(stats + (kMaxIt + 1) * 4);
   const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
   auto gemm = [&](cublasOperation_t ta, const double2* A_, const double2* B_, double2* C_) -> int {
@@ -565,41 +566,46 @@ int heev_near_diag(chfsi_ctx* ctx, int n, double2* a, long long lda, double* w, 
                         reinterpret_cast<cuDoubleComplex*>(C_), n));
     return CHFSI_OK;
   };
-  CK_CUDA(cudaMemcpy2DAsync(G, (size_t)n * sizeof(double2), a, (size_t)lda * sizeof(double2),
+  CK_CUDA(cudaMemcpy2DAsync(G0, (size_t)n * sizeof(double2), a, (size_t)lda * sizeof(double2),
                             (size_t)n * sizeof(double2), n, cudaMemcpyDeviceToDevice, s));
+  CK_CUDA(cudaMemcpyAsync(G, G0, mat, cudaMemcpyDeviceToDevice, s));
   CK_CUDA(cudaMemsetAsync(stats, 0, (kMaxIt + 1) * 4 * sizeof(double), s));
-  int it = 0;
-  int checked = 0;
   std::vector<double> hs((kMaxIt + 1) * 4);
-  for (;;) {
-    // one simultaneous Jacobi step
-    CK_CUDA(chfsi::nd_build_step_launch(G, n, n, X, n, stats + 4 * it, s));
-    for (int ns = 0; ns < 2; ++ns) {  // X <- X (3I - X^H X) / 2
-      CK(gemm(CUBLAS_OP_C, X, X, T));
-      CK_CUDA(chfsi::nd_ns_matrix_launch(T, n, n, s));
-      CK(gemm(CUBLAS_OP_N, X, T, Y));
-      std::swap(X, Y);
+  int it = 0;
+  for (int round = 0; round < 2; ++round) {
+    // Jacobi steps: X = I + S (first order, not exactly unitary), G <- X^H G X,
+    // W <- W X. The max G_ij/gap ratio is squared per step either way.
+    const int steps = round == 0 ? 3 : 1;
+    for (int k = 0; k < steps; ++k, ++it) {
+      CK_CUDA(chfsi::nd_build_step_launch(G, n, n, X, n, stats + 4 * it, s));
+      CK(gemm(CUBLAS_OP_N, G, X, Y));  // Y = G X
+      CK(gemm(CUBLAS_OP_C, X, Y, G));  // G = X^H G X
+      if (it == 0) {
+        std::swap(W, X);               // W = X
+      } else {
+        CK(gemm(CUBLAS_OP_N, W, X, Y));
+        std::swap(W, Y);               // W = W X
+      }
     }
-    CK(gemm(CUBLAS_OP_N, G, X, Y));  // Y = G X
-    CK(gemm(CUBLAS_OP_C, X, Y, G));  // G = X^H G X
+    // W unitary to rounding: 3 Newton-Schulz polar steps (error squared per
+    // step from ~||S||^2), then the exact projection of the ORIGINAL matrix,
+    // G = W^H G0 W: the eigen-pairs come from this unitary similarity.
+    for (int ns = 0; ns < 3; ++ns) {   // W <- W (3I - W^H W) / 2
+      CK(gemm(CUBLAS_OP_C, W, W, Y));
+      CK_CUDA(chfsi::nd_ns_matrix_launch(Y, n, n, s));
+      CK(gemm(CUBLAS_OP_N, W, Y, X));
+      std::swap(W, X);
+    }
+    CK(gemm(CUBLAS_OP_N, G0, W, X));   // X = G0 W
+    CK(gemm(CUBLAS_OP_C, W, X, G));    // G = W^H G0 W
     CK_CUDA(chfsi::symmetrize_launch(G, n, n, s));
-    if (it == 0) {
-      std::swap(W, X);  // W = X
-    } else {
-      CK(gemm(CUBLAS_OP_N, W, X, Y));
-      std::swap(W, Y);
-    }
-    ++it;
-    if (it < 3 && it < kMaxIt) continue;
-    // measure the remaining off-diagonal (stats[it]) and decide
-    CK_CUDA(chfsi::nd_build_step_launch(G, n, n, X, n, stats + 4 * it, s));
+    CK_CUDA(chfsi::nd_build_step_launch(G, n, n, X, n, stats + 4 * it, s));  // measure only
     CK_CUDA(cudaMemcpyAsync(hs.data(), stats, hs.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK_CUDA(cudaStreamSynchronize(s));
-    ++checked;
     const double rmax0 = hs[0], emax = hs[4 * it + 1], dmax = hs[4 * it + 2];
-    if (!(rmax0 <= 0.25)) return CHFSI_OK;  // not near-diagonal: caller uses zheevd
+    if (!(rmax0 <= 0.1)) return CHFSI_OK;  // not near-diagonal: caller uses zheevd
     if (emax <= tol * std::max(1.0, dmax)) break;
-    if (it >= kMaxIt || !(hs[4 * it] < hs[4 * (it - 1)])) return CHFSI_OK;  // stalled
+    if (round == 1 || !(hs[4 * it] < 0.01)) return CHFSI_OK;  // not converging fast enough
   }
   // ascending eigenvalues, eigenvectors permuted accordingly, back into A
   CK_CUDA(chfsi::nd_sort_launch(G, n, n, w, perm, s));
