@@ -571,25 +571,19 @@ int heev_near_diag(chfsi_ctx* ctx, int n, double2* a, long long lda, double* w, 
   CK_CUDA(cudaMemcpyAsync(G, G0, mat, cudaMemcpyDeviceToDevice, s));
   CK_CUDA(cudaMemsetAsync(stats, 0, (kMaxIt + 1) * 4 * sizeof(double), s));
   std::vector<double> hs((kMaxIt + 1) * 4);
-  int it = 0;
-  for (int round = 0; round < 2; ++round) {
-    // Jacobi steps: X = I + S (first order, not exactly unitary), G <- X^H G X,
-    // W <- W X. The max G_ij/gap ratio is squared per step either way.
-    const int steps = round == 0 ? 3 : 1;
-    for (int k = 0; k < steps; ++k, ++it) {
-      CK_CUDA(chfsi::nd_build_step_launch(G, n, n, X, n, stats + 4 * it, s));
-      CK(gemm(CUBLAS_OP_N, G, X, Y));  // Y = G X
-      CK(gemm(CUBLAS_OP_C, X, Y, G));  // G = X^H G X
-      if (it == 0) {
-        std::swap(W, X);               // W = X
-      } else {
-        CK(gemm(CUBLAS_OP_N, W, X, Y));
-        std::swap(W, Y);               // W = W X
-      }
+  // Each step: X = I + S from the current G; W <- W X made unitary to
+  // rounding by Newton-Schulz polar steps (X^H X = I - S^2, so 3 steps take
+  // ||S||^2 ~ 1e-3 below 1e-16); G = W^H G0 W projected exactly, so G stays
+  // unitarily similar to the input and the off-diagonal/gap ratio squares.
+  constexpr int kSteps = 3;
+  for (int it = 0; it < kSteps; ++it) {
+    CK_CUDA(chfsi::nd_build_step_launch(G, n, n, X, n, stats + 4 * it, s));
+    if (it == 0) {
+      std::swap(W, X);                 // W = X
+    } else {
+      CK(gemm(CUBLAS_OP_N, W, X, Y));
+      std::swap(W, Y);                 // W = W X
     }
-    // W unitary to rounding: 3 Newton-Schulz polar steps (error squared per
-    // step from ~||S||^2), then the exact projection of the ORIGINAL matrix,
-    // G = W^H G0 W: the eigen-pairs come from this unitary similarity.
     for (int ns = 0; ns < 3; ++ns) {   // W <- W (3I - W^H W) / 2
       CK(gemm(CUBLAS_OP_C, W, W, Y));
       CK_CUDA(chfsi::nd_ns_matrix_launch(Y, n, n, s));
@@ -599,14 +593,13 @@ int heev_near_diag(chfsi_ctx* ctx, int n, double2* a, long long lda, double* w, 
     CK(gemm(CUBLAS_OP_N, G0, W, X));   // X = G0 W
     CK(gemm(CUBLAS_OP_C, W, X, G));    // G = W^H G0 W
     CK_CUDA(chfsi::symmetrize_launch(G, n, n, s));
-    CK_CUDA(chfsi::nd_build_step_launch(G, n, n, X, n, stats + 4 * it, s));  // measure only
-    CK_CUDA(cudaMemcpyAsync(hs.data(), stats, hs.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK_CUDA(cudaStreamSynchronize(s));
-    const double rmax0 = hs[0], emax = hs[4 * it + 1], dmax = hs[4 * it + 2];
-    if (!(rmax0 <= 0.1)) return CHFSI_OK;  // not near-diagonal: caller uses zheevd
-    if (emax <= tol * std::max(1.0, dmax)) break;
-    if (round == 1 || !(hs[4 * it] < 0.01)) return CHFSI_OK;  // not converging fast enough
   }
+  CK_CUDA(chfsi::nd_build_step_launch(G, n, n, X, n, stats + 4 * kSteps, s));  // measure only
+  CK_CUDA(cudaMemcpyAsync(hs.data(), stats, hs.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK_CUDA(cudaStreamSynchronize(s));
+  const double rmax0 = hs[0], emax = hs[4 * kSteps + 1], dmax = hs[4 * kSteps + 2];
+  if (!(rmax0 <= 0.1)) return CHFSI_OK;                     // not near-diagonal: zheevd
+  if (!(emax <= tol * std::max(1.0, dmax))) return CHFSI_OK;  // not converged: zheevd
   // ascending eigenvalues, eigenvectors permuted accordingly, back into A
   CK_CUDA(chfsi::nd_sort_launch(G, n, n, w, perm, s));
   CK_CUDA(chfsi::nd_gather_cols_launch(W, n, n, n, perm, a, lda, s));
