@@ -157,18 +157,24 @@ _ctxs = threading.local()
 
 
 def ctx(device=None):
-    """Per-thread, per-device libchfsi context bound to torch's current stream."""
+    """libchfsi context for (this thread, device, torch's current stream).
+
+    One context per stream: contexts own cuBLAS/cuSOLVER handles and
+    workspaces, so work issued concurrently on two streams (the sequence
+    driver reduces problem l+1 while solving problem l) never shares them.
+    """
     import torch
 
     if not torch.cuda.is_available():
         raise BackendUnavailable("no CUDA device visible: the ChFSI path runs only on the GPU")
     dev = torch.cuda.current_device() if device is None else int(device)
+    stream = torch.cuda.current_stream(dev).cuda_stream
     table = getattr(_ctxs, "table", None)
     if table is None:
         table = _ctxs.table = {}
-    c = table.get(dev)
+    c = table.get((dev, stream))
     if c is None:
-        c = table[dev] = _Ctx(dev)
+        c = table[(dev, stream)] = _Ctx(dev)
     return c.bind_stream()
 
 

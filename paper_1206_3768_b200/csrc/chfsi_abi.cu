@@ -579,6 +579,11 @@ int heev_near_diag(chfsi_ctx* ctx, int n, double2* a, long long lda, double* w, 
   for (int it = 0; it < kSteps; ++it) {
     CK_CUDA(chfsi::nd_build_step_launch(G, n, n, X, n, stats + 4 * it, s));
     if (it == 0) {
+      // regime check before spending the ZGEMMs: bail out to zheevd early
+      double r0 = 0.0;
+      CK_CUDA(cudaMemcpyAsync(&r0, stats, sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK_CUDA(cudaStreamSynchronize(s));
+      if (!(r0 <= 0.1)) return CHFSI_OK;
       std::swap(W, X);                 // W = X
     } else {
       CK(gemm(CUBLAS_OP_N, W, X, Y));

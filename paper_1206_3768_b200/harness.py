@@ -84,33 +84,61 @@ def _as_pencil(p):
     return EigenPencil(a=a, b=b, label=label)
 
 
-def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on_problem=None):
+def _stage(item, side):
+    """Upload/validate and reduce one pencil on the side stream; returns
+    (pencil, StandardProblem, ready event)."""
+    with torch.cuda.stream(side):
+        pencil = _as_pencil(item)
+        sp = to_standard(pencil)
+        ev = torch.cuda.Event()
+        ev.record(side)
+    return pencil, sp, ev
+
+
+def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on_problem=None,
+                   overlap=True):
     """Solve a correlated sequence on the device.
 
     ``pencils`` yields EigenPencil or ``(label, A, B)`` (numpy or torch).
     ``cfg`` is a ChfsiConfig (``nex`` accepted). Returns a list of
     ProblemResult; ``on_problem(result)`` is called after each problem.
+
+    With ``overlap`` the upload + reduction to standard form of problem l+1
+    runs on a side stream while problem l is being solved (the reduction
+    does not depend on the previous solve), hiding it behind the solver's
+    latency-bound phases. Results are identical either way.
     """
     if mode not in ("chained", "harness"):
         raise ValueError(f"unknown mode {mode!r}")
     out = []
     guess = None
-    for item in pencils:
-        pencil = _as_pencil(item)
+    main = torch.cuda.current_stream()
+    side = torch.cuda.Stream() if overlap else main
+    if side is not main:
+        side.wait_stream(main)  # inputs produced on the caller's stream are visible
+    it = iter(pencils)
+    first = next(it, None)
+    staged = _stage(first, side) if first is not None else None
+    while staged is not None:
+        t0 = time.perf_counter()
+        pencil, sp, ev = staged
+        main.wait_event(ev)
+        if side is not main:
+            for t in (sp.h, sp.cholesky_factor, pencil.a, pencil.b):
+                t.record_stream(main)
+        t1 = time.perf_counter()
+        nxt = next(it, None)
+        staged = _stage(nxt, side) if nxt is not None else None
         n = pencil.n
         blk = cfg.resolve(n)[0]
         if mode == "harness" and blk >= n:
             raise ValueError(f"chfsi warm starts need blk < n (blk={blk}, n={n})")
-        t0 = time.perf_counter()
-        sp = to_standard(pencil)
-        torch.cuda.current_stream().synchronize()
-        t1 = time.perf_counter()
         start = 0 if guess is None else 1
         rng = np.random.default_rng((seed, pencil.label, start))
         sol, rep = chfsi_solve(sp.h, cfg, guess=guess, rng=rng, label=pencil.label)
         t2 = time.perf_counter()
         gsol = back_transform(sp.cholesky_factor, sol)
-        torch.cuda.current_stream().synchronize()
+        main.synchronize()
         t3 = time.perf_counter()
         res = ProblemResult(label=pencil.label, values=sol.values, solution=gsol,
                             standard_vectors=sol.vectors if keep_standard else None, report=rep,
@@ -130,6 +158,7 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
         if on_problem is not None:
             on_problem(res)
         del sp
+    main.wait_stream(side)
     return out
 
 
