@@ -72,6 +72,20 @@ CHFSI_API int chfsi_cheb_step_z(chfsi_ctx* ctx, int n, int w, const void* H, lon
                       const void* ycur, long long ldc, const void* yprev, long long ldp,
                       void* ynext, long long ldn, double alpha, double c, double beta);
 
+/* Row shard of one Chebyshev step for the multi-GPU filter:
+ * computes rows [r0, r0+rows) of Ynext = alpha*(H Ycur - c Ycur) - beta Yprev
+ * where H_rows points at row r0 of H (row-major read, ld ldh, n columns).
+ * Ycur is the FULL block, either column-major (kblk = 0, ld ldc) or in the
+ * rank-blocked layout the NCCL all-gather produces (kblk rows per block,
+ * nblk blocks; block q holds rows [q*kblk, (q+1)*kblk), column-major inside,
+ * padding rows zero). ycur_rows / yprev / ynext address the shard's own rows
+ * (ld ldcr / ldp / ldn); yprev may alias ynext. */
+CHFSI_API int chfsi_cheb_step_rows_z(chfsi_ctx* ctx, int n, int rows, int w, const void* H_rows,
+                                     long long ldh, int conj_h, const void* ycur, long long ldc,
+                                     int kblk, int nblk, const void* ycur_rows, long long ldcr,
+                                     const void* yprev, long long ldp, void* ynext, long long ldn,
+                                     double alpha, double c, double beta);
+
 /* Host-only: the filter's shift c and per-step (alpha_j, beta_j) exactly as
  * chebyshev_filter computes them (chfsi.py:198-207). alphas/betas hold deg. */
 CHFSI_API int chfsi_filter_coeffs(int deg, double a, double b, double scale_ref, double* c,

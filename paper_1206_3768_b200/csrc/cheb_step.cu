@@ -50,13 +50,15 @@ constexpr int kMaxThreads = 256;
 constexpr int kMaxAcc = 32;        // doubles per thread in a partial tile (upper bound)
 
 struct StepParams {
-  const double2* ycur;
+  const double2* ycur;  // rows of Ycur matching the output rows (epilogue c*Ycur term)
   long long ldc;
   const double2* yprev;
   long long ldp;
   double2* ynext;
   long long ldn;
-  int n, w;
+  int n, w;            // contraction length (== rows of H), columns of Y
+  int m;               // output rows computed by this launch (row shard of H)
+  int kblk_slabs;      // > 0: B operand in rank-blocked layout, K slabs per block
   int tiles_n;
   int kiters;          // K slabs per tile
   int dp_waves;        // whole tiles per CTA before the stream-K part
@@ -100,6 +102,14 @@ __device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(unsigned dst, const CUtensorMap* map, unsigned bar,
+                                            int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y), "r"(z)
       : "memory");
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
@@ -222,8 +232,14 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
     mbar_expect_tx(bar, STAGE_BYTES);
     tma_load_2d(dst, &tmA, bar, x, c.m0);
     tma_load_2d(dst + A_BYTES, &tmA, bar, x + BK, c.m0);
-    tma_load_2d(dst + 2 * A_BYTES, &tmB, bar, x, c.n0);
-    tma_load_2d(dst + 2 * A_BYTES + B_BYTES, &tmB, bar, x + BK, c.n0);
+    if (p.kblk_slabs > 0) {  // rank-blocked Y: block q holds rows [q*kblk, (q+1)*kblk)
+      const int q = c.kk / p.kblk_slabs, xl = (c.kk - q * p.kblk_slabs) * (2 * BK);
+      tma_load_3d(dst + 2 * A_BYTES, &tmB, bar, xl, c.n0, q);
+      tma_load_3d(dst + 2 * A_BYTES + B_BYTES, &tmB, bar, xl + BK, c.n0, q);
+    } else {
+      tma_load_2d(dst + 2 * A_BYTES, &tmB, bar, x, c.n0);
+      tma_load_2d(dst + 2 * A_BYTES + B_BYTES, &tmB, bar, x + BK, c.n0);
+    }
   };
 
   if (tid == 0) {
@@ -264,7 +280,7 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
         for (int e = 0; e < 2; ++e) {
           const int row = c.m0 + wm * TM + i * 8 + sg;
           const int col = c.n0 + wn * TN + j * 8 + sigma(2 * t + e);
-          if (row < p.n && col < p.w) epilogue_store(p, row, col, acc[i][j][e], acc[i][j][2 + e]);
+          if (row < p.m && col < p.w) epilogue_store(p, row, col, acc[i][j][e], acc[i][j][2 + e]);
         }
   };
 
@@ -431,6 +447,21 @@ bool encode_map(CUtensorMap* map, const void* base, long long len, long long cou
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D map over the rank-blocked layout: block q, column j, row r at
+// base + (q*count + j)*len + r (complex); box = 16 doubles x rows x 1.
+bool encode_map_blocked(CUtensorMap* map, const void* base, long long len, long long count,
+                        long long blocks, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)(2 * len), (cuuint64_t)count, (cuuint64_t)blocks};
+  const cuuint64_t strides[2] = {(cuuint64_t)(len * 16), (cuuint64_t)(len * count * 16)};
+  const cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)box_rows, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 struct Variant {
   const void* fn;
   int bm, bn, threads, smem;
@@ -497,7 +528,18 @@ cudaError_t cheb_step_launch(const double2* h, long long ldh, bool conj_h, const
                              long long ldc, const double2* yprev, long long ldp, double2* ynext,
                              long long ldn, int n, int w, double alpha, double c, double beta,
                              StepTiling tiling, const StepWorkspace& ws, cudaStream_t stream) {
-  if (n <= 0 || w <= 0) return cudaSuccess;
+  const RowShard whole{n, 0, 0, nullptr, 0};
+  return cheb_step_rows_launch(h, ldh, conj_h, ycur, ldc, yprev, ldp, ynext, ldn, n, w, alpha, c,
+                               beta, whole, tiling, ws, stream);
+}
+
+cudaError_t cheb_step_rows_launch(const double2* h, long long ldh, bool conj_h, const double2* ycur,
+                                  long long ldc, const double2* yprev, long long ldp, double2* ynext,
+                                  long long ldn, int n, int w, double alpha, double c, double beta,
+                                  const RowShard& shard, StepTiling tiling, const StepWorkspace& ws,
+                                  cudaStream_t stream) {
+  const int m = shard.rows;
+  if (n <= 0 || w <= 0 || m <= 0) return cudaSuccess;
   if (tiling.bm == 0) tiling = choose_step_tiling(n, w);
   const Variant* vp = variant(tiling.bm, tiling.bn, conj_h);
   if (vp == nullptr) return cudaErrorInvalidValue;
@@ -506,13 +548,22 @@ cudaError_t cheb_step_launch(const double2* h, long long ldh, bool conj_h, const
   if (tiling.split > 0 && tiling.split < grid) grid = tiling.split;  // test/tuning override
   if (grid > ws.max_grid) return cudaErrorInvalidValue;
 
+  // A: the shard's rows of H (m rows, contraction n). B: Ycur, either plain
+  // column-major (ld ldc) or rank-blocked (kblk rows per block, nblk blocks).
   alignas(64) CUtensorMap tmA, tmB;
-  if (!encode_map(&tmA, h, n, n, ldh, v.bm) || !encode_map(&tmB, ycur, n, w, ldc, v.bn))
+  const bool blocked = shard.kblk > 0;
+  if (blocked && (shard.kblk % BK != 0 || (long long)shard.kblk * shard.nblk < n))
+    return cudaErrorInvalidValue;
+  if (!encode_map(&tmA, h, n, m, ldh, v.bm)) return cudaErrorInvalidValue;
+  if (blocked ? !encode_map_blocked(&tmB, ycur, shard.kblk, w, shard.nblk, v.bn)
+              : !encode_map(&tmB, ycur, n, w, ldc, v.bn))
     return cudaErrorInvalidValue;
 
   StepParams p{};
-  p.ycur = ycur;
-  p.ldc = ldc;
+  p.ycur = shard.ycur_rows ? shard.ycur_rows : ycur;
+  p.ldc = shard.ycur_rows ? shard.ldcr : ldc;
+  p.m = m;
+  p.kblk_slabs = blocked ? shard.kblk / BK : 0;
   p.yprev = yprev ? yprev : ynext;
   p.ldp = yprev ? ldp : ldn;
   p.ynext = ynext;
@@ -520,9 +571,9 @@ cudaError_t cheb_step_launch(const double2* h, long long ldh, bool conj_h, const
   p.n = n;
   p.w = w;
   p.tiles_n = (w + v.bn - 1) / v.bn;
-  const int tiles_m = (n + v.bm - 1) / v.bm;
+  const int tiles_m = (m + v.bm - 1) / v.bm;
   const long long tiles = (long long)tiles_m * p.tiles_n;
-  p.kiters = (n + BK - 1) / BK;
+  p.kiters = blocked ? shard.nblk * (shard.kblk / BK) : (n + BK - 1) / BK;
   static const int dbg = [] {
     const char* e = getenv("CHFSI_K1_DEBUG");
     return e ? atoi(e) : 0;

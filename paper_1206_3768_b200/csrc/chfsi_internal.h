@@ -36,6 +36,24 @@ cudaError_t cheb_step_launch(const double2* h, long long ldh, bool conj_h, const
                              long long ldn, int n, int w, double alpha, double c, double beta,
                              StepTiling tiling, const StepWorkspace& ws, cudaStream_t stream);
 
+// Row shard of K1 for the multi-GPU filter: compute `rows` output rows
+// (H points at the shard's first row); Ycur may be in the rank-blocked
+// layout (kblk rows per block, nblk blocks, block q = rows [q*kblk, ...)),
+// and the epilogue's c*Ycur term then reads the shard's own rows at
+// ycur_rows (ld ldcr).
+struct RowShard {
+  int rows;
+  int kblk;   // 0: Ycur is plain column-major
+  int nblk;
+  const double2* ycur_rows;
+  long long ldcr;
+};
+cudaError_t cheb_step_rows_launch(const double2* h, long long ldh, bool conj_h, const double2* ycur,
+                                  long long ldc, const double2* yprev, long long ldp, double2* ynext,
+                                  long long ldn, int n, int w, double alpha, double c, double beta,
+                                  const RowShard& shard, StepTiling tiling, const StepWorkspace& ws,
+                                  cudaStream_t stream);
+
 // ---- auxiliary kernels (aux_kernels.cu) ----
 // u = op(H) q for a row-major H (conj_h: conj(H)).
 cudaError_t gemv_rows_launch(const double2* h, long long ldh, bool conj_h, const double2* q,

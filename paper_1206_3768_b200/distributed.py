@@ -1,0 +1,173 @@
+"""Row-sharded Chebyshev filter across GPUs (`north_star` (4)).
+
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch). Rank p
+owns rows [p*kblk, (p+1)*kblk) of the filter output; every step
+
+    Y_next[rows_p] = alpha (H[rows_p, :] Y_cur - c Y_cur[rows_p]) - beta Y_prev[rows_p]
+
+is one K1 launch over the shard (`chfsi_cheb_step_rows_z`), followed by an
+in-place NCCL all-gather of the row slabs so every rank holds the full
+Y_next for the next step. The full block lives in a *rank-blocked* layout
+— block q = rows [q*kblk, (q+1)*kblk), column-major inside, zero padding
+rows — which is exactly what an in-place all-gather of the per-rank slabs
+produces, and K1 reads it directly through a 3-D TMA map: no pack/unpack
+between steps. The step is column-chunked (`chunks`): the all-gather of
+chunk c runs on a communication stream while K1 computes chunk c+1, so the
+NVLink transfer overlaps the tensor-core work.
+
+The reference has no parallel code (one process, BLAS threads);
+the result is identical to the single-GPU filter up to the summation order
+of the GEMM (the K split differs), i.e. rounding.
+
+The local step and the collective are injectable so the host logic
+(partition, ping-pong, coefficients, chunking, all-gather order) is tested
+with the gloo backend on CPU (tests/test_distributed_cpu.py).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from ._lib import check, ctx, dptr, filter_coeffs, lib
+
+__all__ = ["RowPartition", "RowShardedFilter", "gpu_row_step"]
+
+BK = 16  # K1 slab: blocked rows per rank are a multiple of it
+
+
+class RowPartition:
+    """Uniform 1-D row blocks: rank p owns [p*kblk, min(n, (p+1)*kblk))."""
+
+    def __init__(self, n, world, rank):
+        if world < 1 or not 0 <= rank < world:
+            raise ValueError("bad world/rank")
+        self.n, self.world, self.rank = n, world, rank
+        self.kblk = max(BK, int(math.ceil(math.ceil(n / world) / BK)) * BK)
+        self.r0 = min(n, rank * self.kblk)
+        self.rows = max(0, min(n, self.r0 + self.kblk) - self.r0)
+
+    def block_range(self, q):
+        r0 = min(self.n, q * self.kblk)
+        return r0, max(0, min(self.n, r0 + self.kblk) - r0)
+
+
+def blocked_empty(part, w, device, dtype=torch.complex128):
+    """Zero-initialised rank-blocked buffer [world][w][kblk] (padding rows stay 0)."""
+    return torch.zeros((part.world, w, part.kblk), dtype=dtype, device=device)
+
+
+def to_blocked(part, y, out):
+    """Full column-major n x w -> rank-blocked buffer."""
+    for q in range(part.world):
+        r0, rows = part.block_range(q)
+        if rows:
+            out[q, :, :rows].copy_(y[r0:r0 + rows, :].t())
+    return out
+
+
+def from_blocked(part, buf, out):
+    """Rank-blocked buffer -> full column-major n x w (out is an F-block view)."""
+    for q in range(part.world):
+        r0, rows = part.block_range(q)
+        if rows:
+            out[r0:r0 + rows, :].copy_(buf[q, :, :rows].t())
+    return out
+
+
+def gpu_row_step(op, part, ycur_blk, yprev_slab, ynext_slab, w, alpha, c, beta):
+    """K1 over this rank's rows (libchfsi); slabs are [w][kblk] views of
+    the rank's block (column-major, ld kblk)."""
+    if part.rows == 0:
+        return
+    h_rows = op.tensor.data_ptr() + part.r0 * op.ld * 16
+    ycur_rows = ycur_blk[part.rank]
+    check(lib().chfsi_cheb_step_rows_z(
+        ctx(), part.n, part.rows, w, ctypes_ptr(h_rows), op.ld, op.conj, dptr(ycur_blk), 0,
+        part.kblk, part.world, dptr(ycur_rows), part.kblk,
+        None if yprev_slab is None else dptr(yprev_slab), part.kblk, dptr(ynext_slab),
+        part.kblk, alpha, c, beta), "sharded chebyshev step")
+
+
+def ctypes_ptr(addr):
+    import ctypes
+
+    return ctypes.c_void_p(addr)
+
+
+def nccl_allgather(buf, part, group=None, async_op=False):
+    """In-place all-gather of the rank slabs of a blocked buffer [world][w][kblk]."""
+    if part.world == 1:
+        return None
+    flat = buf.view(-1)
+    chunk = flat.numel() // part.world
+    mine = flat[part.rank * chunk:(part.rank + 1) * chunk]
+    if dist.get_backend(group) != "nccl":  # in-place aliasing is an NCCL guarantee only
+        mine = mine.clone()
+    return dist.all_gather_into_tensor(flat, mine, group=group, async_op=async_op)
+
+
+class RowShardedFilter:
+    """Degree-`deg` filter (chfsi.py:179-208) with the row-sharded step.
+
+    Columns are independent through the whole recurrence (chfsi.py:203-206),
+    so the block is split into `chunks` column groups, each with its own pair
+    of blocked buffers: the all-gather of group c (asynchronous, on the
+    collective stream) overlaps K1 on group c+1, and step j+1 of group c only
+    waits for group c's all-gather of step j.
+
+    `step(ycur_blk, yprev_slab, ynext_slab, w, alpha, c, beta)` computes this
+    rank's rows; `allgather(buf, async_op)` makes the blocked buffer full on
+    every rank and may return a handle with `.wait()`. Defaults: K1 through
+    libchfsi and NCCL.
+    """
+
+    def __init__(self, op, n, group=None, step=None, allgather=None, chunks=1):
+        self.group = group
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.part = RowPartition(n, world, rank)
+        self.op = op
+        self.chunks = max(1, int(chunks))
+        self.step = step or (lambda yc, yp, yn, w, a, c, b: gpu_row_step(op, self.part, yc, yp, yn,
+                                                                        w, a, c, b))
+        self.allgather = allgather or (lambda buf, async_op=False: nccl_allgather(
+            buf, self.part, self.group, async_op))
+
+    def apply(self, y, deg, window, out=None):
+        """Filter the full block y (n x w, replicated on all ranks); returns
+        the full filtered block (replicated), column-major."""
+        part = self.part
+        n, w = y.shape
+        if n != part.n:
+            raise ValueError("operator/block shapes do not conform")
+        c, al, be = filter_coeffs(deg, float(window.a), float(window.b), float(window.scale_ref))
+        dev = y.device
+        edges = np.linspace(0, w, min(self.chunks, w) + 1).astype(int)
+        groups = [(int(edges[k]), int(edges[k + 1])) for k in range(len(edges) - 1)
+                  if edges[k + 1] > edges[k]]
+        bufs = [[to_blocked(part, y[:, j0:j1], blocked_empty(part, j1 - j0, dev)),
+                 blocked_empty(part, j1 - j0, dev)] for j0, j1 in groups]
+        pending = [None] * len(groups)
+        cur = 0
+        for j in range(deg):
+            nxt = 1 - cur
+            for g, (j0, j1) in enumerate(groups):
+                if pending[g] is not None:
+                    pending[g].wait()  # step j of group g needs its step j-1 all-gather
+                    pending[g] = None
+                yprev = bufs[g][nxt][part.rank] if j > 0 else None
+                self.step(bufs[g][cur], yprev, bufs[g][nxt][part.rank], j1 - j0, al[j], c, be[j])
+                pending[g] = self.allgather(bufs[g][nxt], async_op=True)
+            cur = nxt
+        for h in pending:
+            if h is not None:
+                h.wait()
+        if out is None:
+            out = torch.empty((w, n), dtype=y.dtype, device=dev).t()
+        for g, (j0, j1) in enumerate(groups):
+            from_blocked(part, bufs[g][cur], out[:, j0:j1])
+        return out

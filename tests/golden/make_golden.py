@@ -113,7 +113,7 @@ def small_cases():
     save("small_cases.npz", **out)
 
 
-def sequence_case(cfg_name, vector_labels):
+def sequence_case(cfg_name, vector_labels, limit=None):
     """Reference harness protocol on the BASELINE generator (harness.py:188-289).
 
     For every problem: the dense oracle (to_standard + eigh), a cold ChFSI
@@ -126,6 +126,8 @@ def sequence_case(cfg_name, vector_labels):
     prev = None
     timings = {}
     for label, a, b in iter_baseline_sequence(cfg.n, cfg.length, seed=0):
+        if limit is not None and label > limit:
+            break
         out[f"{label}/a_sha"] = np.bytes_(sha(a))
         out[f"{label}/b_sha"] = np.bytes_(sha(b))
         # host-BLAS-independent fingerprint (the QR/GEMM of the generator
@@ -170,12 +172,15 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--c2", action="store_true")
     p.add_argument("--skip-small", action="store_true")
+    p.add_argument("--c3", action="store_true", help="C3 problems 1-3 (~10 min)")
     args = p.parse_args()
     if not args.skip_small:
         small_cases()
         sequence_case("C1", vector_labels={1, 2})
     if args.c2:
         sequence_case("C2", vector_labels=set())
+    if args.c3:
+        sequence_case("C3", vector_labels=set(), limit=3)
 
 
 if __name__ == "__main__":
