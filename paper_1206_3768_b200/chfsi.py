@@ -352,10 +352,17 @@ def _safe_window(scale_ref, a, b):
 
 # ----------------------------------------------------------------- solver ---
 
-def chfsi_solve(h, cfg, guess=None, rng=None, label=1):
+def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     """Compute the ``cfg.nev`` lowest eigenpairs of the Hermitian ``h``
     (chfsi.py:274-384). ``h`` may be a numpy array (uploaded once) or a CUDA
     tensor in either row- or column-major layout (used in place).
+
+    ``shard`` (multi-GPU): ``True`` or a torch.distributed process
+    group row-shards the filter across the group's ranks (one GPU each; every
+    rank calls chfsi_solve with the same arguments); ``shard=k`` (int) also
+    sets the number of overlapped column groups. Everything else is computed
+    redundantly and bit-identically on every rank, so no other exchange is
+    needed and every rank returns the same solution.
 
     Returns ``(EigenSolution(form="standard"), SolveReport)``; the solution
     vectors stay on the device.
@@ -368,6 +375,13 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1):
     report = SolveReport()
     dev = op.tensor.device
     t_lz, t_f, t_o, t_r = _PhaseTimer(), _PhaseTimer(), _PhaseTimer(), _PhaseTimer()
+    sharded = None
+    if shard is not None and shard is not False:
+        from .distributed import RowShardedFilter
+
+        group = shard if not isinstance(shard, (bool, int)) else None
+        chunks = shard if isinstance(shard, int) and not isinstance(shard, bool) else 2
+        sharded = RowShardedFilter(op, n, group=group, chunks=chunks)
 
     # HBM workspace: two panel buffers (filter ping-pong / rotation target),
     # two H*panel buffers, the locked block, the projected matrix.
@@ -418,7 +432,10 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1):
         panel = bufs[pb][:, off:off + width]
         other = bufs[1 - pb][:, :width]
         t_f.start()
-        filtered = _filter_into(op, panel, other, panel, deg, window)
+        if sharded is not None:
+            filtered = sharded.apply(panel, deg, window, out=other)
+        else:
+            filtered = _filter_into(op, panel, other, panel, deg, window)
         t_f.stop()
         report.filter_launches += deg
         report.filtered_vectors += width

@@ -96,7 +96,7 @@ def _stage(item, side):
 
 
 def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on_problem=None,
-                   overlap=True):
+                   overlap=True, shard=None):
     """Solve a correlated sequence on the device.
 
     ``pencils`` yields EigenPencil or ``(label, A, B)`` (numpy or torch).
@@ -106,7 +106,8 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
     With ``overlap`` the upload + reduction to standard form of problem l+1
     runs on a side stream while problem l is being solved (the reduction
     does not depend on the previous solve), hiding it behind the solver's
-    latency-bound phases. Results are identical either way.
+    latency-bound phases. Results are identical either way. ``shard`` is
+    passed to chfsi_solve (row-sharded multi-GPU filter).
     """
     if mode not in ("chained", "harness"):
         raise ValueError(f"unknown mode {mode!r}")
@@ -135,7 +136,7 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
             raise ValueError(f"chfsi warm starts need blk < n (blk={blk}, n={n})")
         start = 0 if guess is None else 1
         rng = np.random.default_rng((seed, pencil.label, start))
-        sol, rep = chfsi_solve(sp.h, cfg, guess=guess, rng=rng, label=pencil.label)
+        sol, rep = chfsi_solve(sp.h, cfg, guess=guess, rng=rng, label=pencil.label, shard=shard)
         t2 = time.perf_counter()
         gsol = back_transform(sp.cholesky_factor, sol)
         main.synchronize()
