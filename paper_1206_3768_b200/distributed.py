@@ -146,7 +146,8 @@ class RowShardedFilter:
             raise ValueError("operator/block shapes do not conform")
         c, al, be = filter_coeffs(deg, float(window.a), float(window.b), float(window.scale_ref))
         dev = y.device
-        edges = np.linspace(0, w, min(self.chunks, w) + 1).astype(int)
+        nchunks = 1 if part.world == 1 else min(self.chunks, w)  # nothing to overlap alone
+        edges = np.linspace(0, w, nchunks + 1).astype(int)
         groups = [(int(edges[k]), int(edges[k + 1])) for k in range(len(edges) - 1)
                   if edges[k + 1] > edges[k]]
         bufs = [[to_blocked(part, y[:, j0:j1], blocked_empty(part, j1 - j0, dev)),

@@ -84,6 +84,19 @@ def _as_pencil(p):
     return EigenPencil(a=a, b=b, label=label)
 
 
+_SIDE_STREAMS = {}
+
+
+def side_stream(device=None):
+    """One persistent side stream per device (and so one libchfsi context for
+    it): creating a stream per call would create a context per call."""
+    dev = torch.cuda.current_device() if device is None else device
+    st = _SIDE_STREAMS.get(dev)
+    if st is None:
+        st = _SIDE_STREAMS[dev] = torch.cuda.Stream(device=dev)
+    return st
+
+
 def _stage(item, side):
     """Upload/validate and reduce one pencil on the side stream; returns
     (pencil, StandardProblem, ready event)."""
@@ -114,7 +127,7 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
     out = []
     guess = None
     main = torch.cuda.current_stream()
-    side = torch.cuda.Stream() if overlap else main
+    side = side_stream() if overlap else main
     if side is not main:
         side.wait_stream(main)  # inputs produced on the caller's stream are visible
     it = iter(pencils)
