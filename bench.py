@@ -60,6 +60,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=2, help="problems in the CPU sample")
     ap.add_argument("--no-clocks", action="store_true", help="diagnostics: no clock sampler")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="diagnostics: no side-stream reduction of the next problem")
     ap.add_argument("--shard", action="store_true",
                     help="row-shard the filter across the ranks (strong scaling, C3-C5)")
     return ap.parse_args()
@@ -231,7 +233,8 @@ def run_ours(args):
     shard = True if args.shard else None
 
     def device_step():
-        return solve_sequence(dev_pencils, cfg, seed=0, mode=args.mode, shard=shard)
+        return solve_sequence(dev_pencils, cfg, seed=0, mode=args.mode, shard=shard,
+                              overlap=not args.no_overlap)
 
     for _ in range(args.warmup):
         device_step()
@@ -265,7 +268,7 @@ def run_ours(args):
 
         def e2e_step():
             out = solve_sequence(((lab, a, b) for lab, a, b in pinned), cfg, seed=0,
-                                 mode=args.mode, shard=shard)
+                                 mode=args.mode, shard=shard, overlap=not args.no_overlap)
             host = [(r.values, r.solution.vectors.cpu()) for r in out]
             return out, host
 
