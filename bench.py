@@ -69,11 +69,29 @@ def parse_args():
 
 # ------------------------------------------------------------------ clocks ---
 
+_SAMPLER_SRC = r"""
+import sys, time, pynvml as nv
+nv.nvmlInit()
+h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+period = float(sys.argv[2])
+while True:
+    try:
+        print(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), smax,
+              nv.nvmlDeviceGetPowerUsage(h) / 1000.0,
+              nv.nvmlDeviceGetCurrentClocksEventReasons(h), flush=True)
+    except Exception:
+        pass
+    time.sleep(period)
+"""
+
+
 class ClockSampler:
     """SM clock / throttle-reason sampling during the timed region (the
-    nvidia-smi clocks line of B200_PROFILING.md, read through NVML from a
-    background thread every 200 ms — the same counters without spawning
-    nvidia-smi, whose queries stall kernel launches)."""
+    nvidia-smi clocks line of B200_PROFILING.md, read through NVML every
+    200 ms). It runs in a separate process: an in-process sampler thread
+    measurably stalled the solver's host loop, and nvidia-smi itself stalls
+    kernel launches."""
 
     REASONS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
                "hw_thermal_slowdown": 0x40, "hw_power_brake": 0x80}
@@ -81,48 +99,44 @@ class ClockSampler:
     def __init__(self, index, period=0.2):
         self.index = index
         self.period = period
-        self.rows = []
-        self.thread = None
-        self.stop_evt = threading.Event()
-
-    def _run(self):
-        import pynvml as nv
-
-        h = nv.nvmlDeviceGetHandleByIndex(self.index)
-        smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-        while not self.stop_evt.is_set():
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.rows.append((sm, smax, pw, rs))
-            except Exception:  # noqa: BLE001 - sampling must never break the bench
-                pass
-            self.stop_evt.wait(self.period)
+        self.proc = None
+        self.path = None
 
     def start(self):
-        try:
-            import pynvml as nv
+        import subprocess
+        import tempfile
 
-            nv.nvmlInit()
-        except Exception:  # noqa: BLE001
-            return
-        self.thread = threading.Thread(target=self._run, daemon=True)
-        self.thread.start()
+        fd, self.path = tempfile.mkstemp(suffix=".clk")
+        try:
+            self.proc = subprocess.Popen(
+                [sys.executable, "-c", _SAMPLER_SRC, str(self.index), str(self.period)],
+                stdout=fd, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        os.close(fd)
+        time.sleep(0.3)  # first samples before the timed region starts
 
     def stop(self):
-        if self.thread is None:
+        if self.proc is None:
             return None
-        self.stop_evt.set()
-        self.thread.join(timeout=5)
-        rows = self.rows
+        self.proc.terminate()
+        self.proc.wait(timeout=10)
+        rows = []
+        for line in open(self.path):
+            parts = line.split()
+            if len(parts) == 4:
+                try:
+                    rows.append((float(parts[0]), float(parts[1]), float(parts[2]), int(parts[3])))
+                except ValueError:
+                    pass
+        os.unlink(self.path)
         if not rows:
             return None
         reasons = sorted({k for r in rows for k, bit in self.REASONS.items() if r[3] & bit})
         loaded = [r[0] for r in rows if r[2] > 250.0] or [r[0] for r in rows]
         return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(r[1] for r in rows),
                 "reasons": reasons, "samples": len(rows),
-                "power_w_max": max(r[2] for r in rows), "source": "NVML, 200 ms"}
+                "power_w_max": max(r[2] for r in rows), "source": "NVML subprocess, 200 ms"}
 
 
 # ------------------------------------------------------------------ inputs ---
