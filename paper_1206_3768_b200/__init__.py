@@ -44,6 +44,8 @@ from .chfsi import (
 )
 from .harness import OracleMismatchError, oracle_solve, solve_sequence
 from .sequence import BASELINE_CONFIGS, BaselineConfig, iter_baseline_sequence
+from .pencil_io import FormatError, load_sequence, read_pencil, save_sequence, write_pencil
+from .analysis import AngleReport, angle_report, match_eigenvectors
 from ._lib import BackendUnavailable
 
 __version__ = "0.1.0"

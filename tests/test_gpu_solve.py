@@ -191,3 +191,63 @@ def test_c2_harness_protocol_matches_reference(pkg, c2_golden):
             assert subspace_sines(dvec[:, : cfg_b.nev].cpu().numpy(), sol.vectors_host()).max() <= 1e-6
         prev = pkg.ChfsiGuess(vectors=dvec[:, : cfg_b.blk], lambda1=float(dv[0]),
                               lambda_blk_plus_1=float(dv[cfg_b.blk]))
+
+
+def test_angle_report_matches_reference_restatement(pkg):
+    """Device cross-Gram + greedy matching (sequence.py:187-257) on a solved
+    C1 sequence, checked against the numpy restatement of the reference."""
+    from tests.test_io_analysis_cpu import reference_greedy
+
+    cfg_b = pkg.BASELINE_CONFIGS["C1"]
+    cfg = pkg.ChfsiConfig(nev=cfg_b.nev, nex=cfg_b.nex, deg=cfg_b.deg, tol=cfg_b.tol)
+    seq = list(pkg.iter_baseline_sequence(cfg_b.n, 3, seed=0))
+    res = pkg.solve_sequence(seq, cfg, keep_standard=True)
+    pencils = [pkg.EigenPencil(a=a, b=b, label=l) for l, a, b in seq]
+    sols = [r.solution for r in res]  # generalized form: exercises L^H x
+    rep = pkg.angle_report(pencils, sols, fraction=0.5)
+    for k, r in enumerate(res[:-1]):
+        tracked = int(np.ceil(0.5 * cfg_b.nev))
+        ya = r.standard_vectors.cpu().numpy()[:, :tracked]
+        yb = res[k + 1].standard_vectors.cpu().numpy()[:, :tracked]
+        gram = np.abs(ya.conj().T @ yb)
+        sigma = reference_greedy(gram)
+        theta = np.arccos(np.minimum(1.0, gram[np.arange(tracked), sigma]))
+        assert np.array_equal(rep.matching[k + 1], sigma)
+        assert np.abs(rep.angles[k + 1] - theta).max() <= 1e-6
+        assert rep.median_angles[k + 1] < 0.1  # correlated problems: small deviation angles
+
+
+@pytest.mark.slow
+def test_c3_harness_protocol_matches_reference(pkg):
+    """BASELINE config 3 (n=5000, nev=500, nex=100, deg=20): problems 1-3 of
+    the reference harness protocol (golden from the reference, ~10 min of
+    CPU per run) — counts within one loop, eigenvalues 1e-9 relative,
+    residuals <= tol, angles to the dense device eigenspace <= 1e-6."""
+    import os
+
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "c3_harness.npz"))
+    cfg_b = pkg.BASELINE_CONFIGS["C3"]
+    cfg = pkg.ChfsiConfig(nev=cfg_b.nev, nex=cfg_b.nex, deg=cfg_b.deg, tol=cfg_b.tol)
+    prev = None
+    for label, a, b in pkg.iter_baseline_sequence(cfg_b.n, 3, seed=0):
+        assert_same_input(a, b, gold, label)
+        sp = pkg.to_standard(pkg.EigenPencil(a=a, b=b, label=label))
+        dv, dvec = pkg.hermitian_eig(sp.h)
+        np.testing.assert_allclose(dv[: cfg_b.blk + 1], gold[f"{label}/dense_values"], rtol=0,
+                                   atol=1e-11)
+        runs = [("cold", None, (0, label, 0))]
+        if prev is not None:
+            runs.append(("warm", prev, (0, label, 1)))
+        for kind, guess, seed in runs:
+            sol, rep = pkg.chfsi_solve(sp.h, cfg, guess=guess, rng=np.random.default_rng(seed))
+            pre = f"{label}/{kind}/"
+            assert rep.converged
+            assert_counts_close(rep, gold, pre, cfg_b.deg, cfg_b.blk)
+            assert_report_algebra(rep, cfg_b.deg)
+            ref = gold[pre + "values"]
+            assert np.abs(sol.values - ref).max() <= 1e-9 * np.abs(ref).max()
+            assert (rep.final_residuals <= cfg_b.tol).all()
+            v = sol.vectors_host()
+            assert subspace_sines(dvec[:, : cfg_b.nev].cpu().numpy(), v).max() <= 1e-6
+        prev = pkg.ChfsiGuess(vectors=dvec[:, : cfg_b.blk], lambda1=float(dv[0]),
+                              lambda_blk_plus_1=float(dv[cfg_b.blk]))
