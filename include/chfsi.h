@@ -182,6 +182,59 @@ CHFSI_API int chfsi_to_standard_z(chfsi_ctx* ctx, int n, void* A, long long lda,
 CHFSI_API int chfsi_back_transform_z(chfsi_ctx* ctx, int n, int nev, const void* L, long long ldl, void* Y,
                            long long ldy);
 
+/* --------------------------------------------------------------- driver ---
+ * The inner loop of chfsi_solve (chfsi.py:328-373) in native code: per pass
+ * filter -> CGS against the locked block + QR with rank repair -> Rayleigh-
+ * Ritz -> locking of leading converged Ritz pairs -> window refresh
+ * (chfsi.py:264-271), until nev pairs are locked or max_repeats passes ran.
+ * The caller sets up the start block (bufs[0], orthonormal), the window and
+ * the workspace; the loop leaves its state and counters in the struct.
+ * Optional host callbacks: `filter` replaces the single-GPU filter (the
+ * row-sharded multi-GPU filter), `fill` draws replacement columns for a
+ * rank-deficient panel (the caller's RNG, reference draw order). */
+typedef int (*chfsi_filter_cb)(void* user, const void* panel, void* other, long long ld, int width,
+                               int deg, double a, double b, double scale_ref, void** result);
+typedef int (*chfsi_fill_cb)(void* user, void* block, long long ld, int rows, const int* cols,
+                             int ncols);
+
+typedef struct chfsi_loop {
+  /* problem and device workspace (in) */
+  int n, blk, nev, deg, max_repeats;
+  double tol;
+  double rr_fast_tol;        /* > 0: near-diagonal RR eigensolver allowed (else zheevd only) */
+  const void* H;
+  long long ldh;
+  int conj_h;
+  void* bufs[2];             /* n x blk panels, ld n; bufs[0] holds the orthonormal start block */
+  void* hp;                  /* n x blk */
+  void* hp_rot;              /* n x blk */
+  void* locked;              /* n x nev, ld n */
+  void* g;                   /* blk x blk, ld blk */
+  void* coef;                /* nev x blk, ld nev */
+  double* ritz_d;            /* device, blk */
+  double* res_d;             /* device, blk */
+  chfsi_filter_cb filter;    /* NULL: chfsi_filter_z on this context */
+  chfsi_fill_cb fill;        /* NULL: rank deficiency is an error */
+  void* user;
+  /* window and loop state (in/out) */
+  double win_a, win_b, win_scale_ref;
+  int try_fast;
+  int inner_loops, nlocked, pb, off, width, converged;
+  int last_rot_pb, last_width, last_nlock; /* the final pass's rotated panel */
+  /* host outputs (caller-owned arrays) */
+  double* locked_vals;       /* nev, in locking order */
+  double* locked_res;        /* nev */
+  int* locked_per_loop;      /* max_repeats */
+  double* ritz;              /* blk: the final pass's Ritz values */
+  double* res;               /* blk: and residual norms */
+  /* counters (SolveReport, chfsi.py:101-122) and device phase times */
+  long long filtered_vectors, matvecs, residual_check_matvecs, filter_launches, rr_fast_eigs;
+  double filter_flops;
+  double t_filter, t_ortho, t_rr; /* seconds */
+} chfsi_loop;
+
+CHFSI_API int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* loop);
+
 #ifdef __cplusplus
 }
 #endif

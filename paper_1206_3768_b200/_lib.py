@@ -83,6 +83,37 @@ _SIGNATURES = {
     "chfsi_to_standard_z": [_vp, _i, _vp, _ll, _vp, _ll, _i, _pi],
     "chfsi_back_transform_z": [_vp, _i, _i, _vp, _ll, _vp, _ll],
 }
+
+FILTER_CB = ctypes.CFUNCTYPE(_i, _vp, _vp, _vp, _ll, _i, _i, _d, _d, _d, ctypes.POINTER(_vp))
+FILL_CB = ctypes.CFUNCTYPE(_i, _vp, _vp, _ll, _i, _pi, _i)
+
+
+class LoopState(ctypes.Structure):
+    """Mirror of `chfsi_loop` (include/chfsi.h): native ChFSI inner loop."""
+
+    _fields_ = [
+        ("n", _i), ("blk", _i), ("nev", _i), ("deg", _i), ("max_repeats", _i),
+        ("tol", _d), ("rr_fast_tol", _d),
+        ("H", _vp), ("ldh", _ll), ("conj_h", _i),
+        ("bufs", _vp * 2), ("hp", _vp), ("hp_rot", _vp), ("locked", _vp), ("g", _vp),
+        ("coef", _vp), ("ritz_d", _vp), ("res_d", _vp),
+        ("filter", FILTER_CB), ("fill", FILL_CB), ("user", _vp),
+        ("win_a", _d), ("win_b", _d), ("win_scale_ref", _d),
+        ("try_fast", _i),
+        ("inner_loops", _i), ("nlocked", _i), ("pb", _i), ("off", _i), ("width", _i),
+        ("converged", _i),
+        ("last_rot_pb", _i), ("last_width", _i), ("last_nlock", _i),
+        ("locked_vals", _pd), ("locked_res", _pd), ("locked_per_loop", _pi),
+        ("ritz", _pd), ("res", _pd),
+        ("filtered_vectors", _ll), ("matvecs", _ll), ("residual_check_matvecs", _ll),
+        ("filter_launches", _ll), ("rr_fast_eigs", _ll),
+        ("filter_flops", _d),
+        ("t_filter", _d), ("t_ortho", _d), ("t_rr", _d),
+    ]
+
+
+_SIGNATURES["chfsi_solve_loop_z"] = [_vp, ctypes.POINTER(LoopState)]
+
 _RESTYPES = {"chfsi_last_error": ctypes.c_char_p, "chfsi_launch_count": ctypes.c_longlong}
 
 

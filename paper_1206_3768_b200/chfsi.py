@@ -29,9 +29,8 @@ import scipy.linalg
 import torch
 
 from ._device import C128, Operator, fblock, ld_of, to_fblock
-from ._lib import check, ctx, dptr, lib
+from ._lib import FILL_CB, FILTER_CB, LoopState, check, ctx, dptr, lib
 from .linalg import qr_orthonormalize_inplace
-from .linalg_errors import RankDeficientError
 from .reduction import EigenSolution
 
 __all__ = [
@@ -321,24 +320,52 @@ def rayleigh_ritz(h, y):
 
 # ------------------------------------------------------------ orthonormal ---
 
-def _orthonormalize_panel(work, locked, nlocked, coef, rng, retries=3):
-    """Two CGS passes against the locked block, then Householder QR with
-    rank repair (chfsi.py:242-261). ``work`` is overwritten by Q."""
-    n, w = work.shape
-    for attempt in range(retries + 1):
-        if nlocked:
-            check(lib().chfsi_cgs_project_z(ctx(), n, nlocked, w, dptr(locked), ld_of(locked),
-                                            dptr(work), ld_of(work), dptr(coef)), "cgs")
+class _LoopCallbacks:
+    """Host callbacks of the native loop: rank-repair draws from the
+    caller's Generator (reference order, chfsi.py:255-259) and, for the
+    row-sharded multi-GPU filter, the filter itself. Exceptions raised in a
+    callback are re-raised after the loop returns."""
+
+    def __init__(self, bufs, n, rng, sharded):
+        self.bufs, self.n, self.rng, self.sharded = bufs, n, rng, sharded
+        self.error = None
+        self.fill_cb = FILL_CB(self._fill)
+        self.filter_cb = FILTER_CB(self._filter)
+
+    def _view(self, ptr, width):
+        for b in self.bufs:
+            off = (ptr - b.data_ptr()) // (16 * self.n)
+            if 0 <= off < b.shape[1] and b.data_ptr() + off * 16 * self.n == ptr:
+                return b[:, off:off + width]
+        raise ValueError("pointer outside the panel buffers")
+
+    def _fill(self, user, block, ld, rows, cols, ncols):
         try:
-            return qr_orthonormalize_inplace(work)
-        except RankDeficientError as err:
-            if attempt == retries:
-                raise
-            idx = list(err.indices)
-            fresh = random_block(rng, n, len(idx))
-            for j, col in enumerate(idx):
-                work[:, col].copy_(fresh[:, j])
-    raise AssertionError("unreachable")
+            idx = [cols[j] for j in range(ncols)]
+            work = self._view(block, max(idx) + 1)
+            fresh = random_block(self.rng, self.n, ncols)
+            for j, c in enumerate(idx):
+                work[:, c].copy_(fresh[:, j])
+            return 0
+        except BaseException as exc:  # noqa: BLE001 - re-raised by reraise()
+            self.error = exc
+            return -1
+
+    def _filter(self, user, panel, other, ld, width, deg, a, b, scale_ref, result):
+        try:
+            out = self.sharded.apply(self._view(panel, width), deg,
+                                     FilterWindow(a=a, b=b, scale_ref=scale_ref),
+                                     out=self._view(other, width))
+            result[0] = out.data_ptr()
+            return 0
+        except BaseException as exc:  # noqa: BLE001
+            self.error = exc
+            return -1
+
+    def reraise(self):
+        if self.error is not None:
+            err, self.error = self.error, None
+            raise err
 
 
 def _safe_window(scale_ref, a, b):
@@ -374,7 +401,7 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     blk, deg, tol, lancz_k, max_repeats = cfg.resolve(n)
     report = SolveReport()
     dev = op.tensor.device
-    t_lz, t_f, t_o, t_r = _PhaseTimer(), _PhaseTimer(), _PhaseTimer(), _PhaseTimer()
+    t_lz = _PhaseTimer()
     sharded = None
     if shard is not None and shard is not False:
         from .distributed import RowShardedFilter
@@ -418,78 +445,59 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     report.matvecs += steps
     report.operator_norm_estimate = float(max(abs(ritz[0]), abs(ritz[-1])) + beta_last)
 
-    locked_vals: list[float] = []
-    locked_res: list[float] = []
-    nlocked = 0
-    pb, off, width = 0, 0, blk   # panel = bufs[pb][:, off:off+width]
-    try_fast = guess is not None  # warm panels give near-diagonal projections
-    ritz_vals = np.zeros(0)
-    rot_p = None
-    n_lock = 0
+    # ---- the inner loop runs natively (chfsi_solve_loop_z, chfsi_loop.cu)
+    st = LoopState()
+    st.n, st.blk, st.nev, st.deg, st.max_repeats = n, blk, cfg.nev, deg, max_repeats
+    st.tol = tol
+    # near-diagonal eigensolver once the panel is close to invariant (warm
+    # starts, or after the first locking); zheevd otherwise
+    st.rr_fast_tol = RR_FAST_TOL if tol >= 1e-11 else 0.0
+    st.H, st.ldh, st.conj_h = op.tensor.data_ptr(), op.ld, int(op.conj)
+    st.bufs[0], st.bufs[1] = bufs[0].data_ptr(), bufs[1].data_ptr()
+    st.hp, st.hp_rot, st.locked = hp_buf.data_ptr(), hp_rot.data_ptr(), locked.data_ptr()
+    st.g, st.coef = g_buf.data_ptr(), coef.data_ptr()
+    st.ritz_d, st.res_d = ritz_d.data_ptr(), res_d.data_ptr()
+    st.win_a, st.win_b, st.win_scale_ref = window.a, window.b, window.scale_ref
+    st.try_fast = int(guess is not None)  # warm panels give near-diagonal projections
+    st.pb, st.off, st.width = 0, 0, blk
+    host_f = np.zeros((4, blk))
+    locked_per_loop = np.zeros(max(max_repeats, 1), dtype=np.int32)
+    pd_, pi_ = ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)
+    st.locked_vals = host_f[0].ctypes.data_as(pd_)
+    st.locked_res = host_f[1].ctypes.data_as(pd_)
+    st.ritz = host_f[2].ctypes.data_as(pd_)
+    st.res = host_f[3].ctypes.data_as(pd_)
+    st.locked_per_loop = locked_per_loop.ctypes.data_as(pi_)
+    callbacks = _LoopCallbacks(bufs, n, rng, sharded)
+    st.fill = callbacks.fill_cb
+    if sharded is not None:
+        st.filter = callbacks.filter_cb
+    status = lib().chfsi_solve_loop_z(ctx(), ctypes.byref(st))
+    callbacks.reraise()
+    check(status, "chfsi inner loop")
 
-    for _ in range(max_repeats):
-        report.inner_loops += 1
-        panel = bufs[pb][:, off:off + width]
-        other = bufs[1 - pb][:, :width]
-        t_f.start()
-        if sharded is not None:
-            filtered = sharded.apply(panel, deg, window, out=other)
-        else:
-            filtered = _filter_into(op, panel, other, panel, deg, window)
-        t_f.stop()
-        report.filter_launches += deg
-        report.filtered_vectors += width
-        report.matvecs += deg * width
-        report.filter_flops += filter_flops(n, deg, width)
-        q_in_other = filtered.data_ptr() == other.data_ptr()
-
-        t_o.start()
-        _orthonormalize_panel(filtered, locked, nlocked, coef, rng)
-        t_o.stop()
-
-        t_r.start()
-        rot_buf = bufs[pb] if q_in_other else bufs[1 - pb]
-        rot_p = rot_buf[:, :width]  # free: disjoint from Q by construction
-        # near-diagonal eigensolver once the panel is close to invariant (warm
-        # starts, or after the first locking); zheevd otherwise
-        fast = _rr_core(op, filtered, hp_buf[:, :width], g_buf[:width, :width], rot_p,
-                        hp_rot[:, :width], ritz_d[:width], res_d[:width],
-                        eig_tol=RR_FAST_TOL if (try_fast and tol >= 1e-11) else 0.0)
-        report.rr_fast_eigs += int(fast)
-        if try_fast and not fast:
-            try_fast = False
-        report.residual_check_matvecs += width
-        report.matvecs += width
-        host = torch.cat([ritz_d[:width], res_d[:width]]).cpu().numpy()
-        t_r.stop()
-        ritz_vals, res = host[:width], host[width:]
-
-        n_lock = 0
-        while n_lock < width and nlocked + n_lock < cfg.nev and res[n_lock] < tol:
-            n_lock += 1
-        if n_lock:
-            try_fast = True
-            locked_vals.extend(float(v) for v in ritz_vals[:n_lock])
-            locked_res.extend(float(r) for r in res[:n_lock])
-            locked[:, nlocked:nlocked + n_lock].copy_(rot_p[:, :n_lock])
-            nlocked += n_lock
-        report.locked_per_loop.append(n_lock)
-
-        if len(locked_vals) >= cfg.nev:
-            report.converged = True
-            break
-
-        pb = 0 if rot_p.data_ptr() == bufs[0].data_ptr() else 1
-        off, width = n_lock, width - n_lock
-        window = _safe_window(float(ritz_vals[n_lock]), float(ritz_vals[-1]), window.b)
+    nlocked = st.nlocked
+    report.inner_loops = st.inner_loops
+    report.filtered_vectors = int(st.filtered_vectors)
+    report.matvecs += int(st.matvecs)
+    report.residual_check_matvecs = int(st.residual_check_matvecs)
+    report.filter_launches = int(st.filter_launches)
+    report.filter_flops = float(st.filter_flops)
+    report.rr_fast_eigs = int(st.rr_fast_eigs)
+    report.converged = bool(st.converged)
+    report.locked_per_loop = [int(x) for x in locked_per_loop[: st.inner_loops]]
+    locked_vals = host_f[0, :nlocked].tolist()
+    locked_res = host_f[1, :nlocked].tolist()
 
     # chained-mode tail: [locked | unlocked remainder of the final panel]
-    if rot_p is not None:
-        tail = fblock(n, nlocked + rot_p.shape[1] - n_lock)
+    if st.inner_loops:
+        rot_p = bufs[st.last_rot_pb][:, : st.last_width]
+        n_lock = st.last_nlock
+        tail = fblock(n, nlocked + st.last_width - n_lock)
         tail[:, :nlocked].copy_(locked[:, :nlocked])
         tail[:, nlocked:].copy_(rot_p[:, n_lock:])
         report.tail_vectors = tail
-        report.lambda_blk_plus_1 = float(ritz_vals[-1])
+        report.lambda_blk_plus_1 = float(host_f[2, st.last_width - 1])
 
     order = np.argsort(locked_vals, kind="stable")
     vecs = locked[:, :nlocked]
@@ -501,8 +509,8 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     report.final_residuals = np.asarray(locked_res)[order]
     torch.cuda.current_stream().synchronize()
     report.t_lanczos = t_lz.seconds()
-    report.t_filter = t_f.seconds()
-    report.t_ortho = t_o.seconds()
-    report.t_rr = t_r.seconds()
+    report.t_filter = st.t_filter
+    report.t_ortho = st.t_ortho
+    report.t_rr = st.t_rr
     report.wall_time = time.perf_counter() - t0
     return sol, report

@@ -1,0 +1,74 @@
+// Private to libchfsi's C-ABI translation units (chfsi_abi.cu,
+// chfsi_loop.cu): the context object and the status-returning check macros.
+#pragma once
+
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include <string>
+
+#include "../../include/chfsi.h"
+#include "chfsi_internal.h"
+
+struct chfsi_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cublasHandle_t blas = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  void* ws = nullptr;  // cuSOLVER workspace (grown on demand)
+  size_t ws_bytes = 0;
+  void* scratch = nullptr;  // n-sized vectors (grown on demand)
+  void* eig_ws = nullptr;   // near-diagonal eigensolver work (grown on demand)
+  size_t eig_ws_bytes = 0;
+  size_t scratch_bytes = 0;
+  double* partial = nullptr;  // kRedBlocks doubles
+  double* scalars = nullptr;  // 16 doubles
+  int* dinfo = nullptr;
+  chfsi::LanczosState* lstate = nullptr;
+  chfsi::StepTiling tiling{0, 0, 0};  // K1 tile override (bm == 0: automatic)
+  chfsi::StepWorkspace step_ws{nullptr, nullptr, nullptr, 0};
+  int qr_mode = 0;  // 0: shifted Cholesky-QR3 with Householder fallback; 1: Householder
+  int lanczos_mode = 0;  // 0: cooperative single kernel; 1: one launch per operation
+  unsigned step_epoch = 0;
+  cudaEvent_t loop_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // chfsi_solve_loop_z phase timers
+  void* pinned = nullptr;  // page-locked host staging for small readbacks (grown on demand)
+  size_t pinned_bytes = 0;
+};
+
+namespace chfsi {
+// Page-locked host buffer of at least `bytes` owned by the context (for the
+// small device->host readbacks that drive host decisions).
+int ensure_pinned(chfsi_ctx* ctx, size_t bytes);
+// Records `msg` as this thread's chfsi_last_error() and returns `code`.
+int fail(int code, const std::string& msg);
+}  // namespace chfsi
+
+#define CK_CUDA(expr)                                                                \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess)                                                           \
+      return chfsi::fail(CHFSI_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));  \
+  } while (0)
+#define CK_BLAS(expr)                                                                        \
+  do {                                                                                       \
+    cublasStatus_t _s = (expr);                                                              \
+    if (_s != CUBLAS_STATUS_SUCCESS)                                                         \
+      return chfsi::fail(CHFSI_ECUBLAS, std::string(#expr) + ": cublas status " + std::to_string(_s)); \
+  } while (0)
+#define CK_SOLVER(expr)                                                                     \
+  do {                                                                                      \
+    cusolverStatus_t _s = (expr);                                                           \
+    if (_s != CUSOLVER_STATUS_SUCCESS)                                                      \
+      return chfsi::fail(CHFSI_ECUSOLVER,                                                          \
+                  std::string(#expr) + ": cusolver status " + std::to_string(_s));          \
+  } while (0)
+#define CK_ARG(cond, msg) \
+  do {                    \
+    if (!(cond)) return chfsi::fail(CHFSI_EINVAL, msg); \
+  } while (0)
+#define CK(expr)              \
+  do {                        \
+    int _r = (expr);          \
+    if (_r != CHFSI_OK) return _r; \
+  } while (0)
+

@@ -12,8 +12,7 @@
 #include <string>
 #include <vector>
 
-#include "../../include/chfsi.h"
-#include "chfsi_internal.h"
+#include "abi_internal.h"
 
 using chfsi::LanczosState;
 
@@ -22,65 +21,29 @@ static std::atomic<long long> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 }  // namespace chfsi
 
-struct chfsi_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  cublasHandle_t blas = nullptr;
-  cusolverDnHandle_t solver = nullptr;
-  void* ws = nullptr;  // cuSOLVER workspace (grown on demand)
-  size_t ws_bytes = 0;
-  void* scratch = nullptr;  // n-sized vectors (grown on demand)
-  void* eig_ws = nullptr;   // near-diagonal eigensolver work (grown on demand)
-  size_t eig_ws_bytes = 0;
-  size_t scratch_bytes = 0;
-  double* partial = nullptr;  // kRedBlocks doubles
-  double* scalars = nullptr;  // 16 doubles
-  int* dinfo = nullptr;
-  LanczosState* lstate = nullptr;
-  chfsi::StepTiling tiling{0, 0, 0};  // K1 tile override (bm == 0: automatic)
-  chfsi::StepWorkspace step_ws{nullptr, nullptr, nullptr, 0};
-  int qr_mode = 0;  // 0: shifted Cholesky-QR3 with Householder fallback; 1: Householder
-  int lanczos_mode = 0;  // 0: cooperative single kernel; 1: one launch per operation
-  unsigned step_epoch = 0;
-};
-
-namespace {
-
-thread_local std::string g_last_error;
-
+namespace chfsi {
+static thread_local std::string g_last_error;
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
 
-#define CK_CUDA(expr)                                                                \
-  do {                                                                               \
-    cudaError_t _e = (expr);                                                         \
-    if (_e != cudaSuccess)                                                           \
-      return fail(CHFSI_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));  \
-  } while (0)
-#define CK_BLAS(expr)                                                                        \
-  do {                                                                                       \
-    cublasStatus_t _s = (expr);                                                              \
-    if (_s != CUBLAS_STATUS_SUCCESS)                                                         \
-      return fail(CHFSI_ECUBLAS, std::string(#expr) + ": cublas status " + std::to_string(_s)); \
-  } while (0)
-#define CK_SOLVER(expr)                                                                     \
-  do {                                                                                      \
-    cusolverStatus_t _s = (expr);                                                           \
-    if (_s != CUSOLVER_STATUS_SUCCESS)                                                      \
-      return fail(CHFSI_ECUSOLVER,                                                          \
-                  std::string(#expr) + ": cusolver status " + std::to_string(_s));          \
-  } while (0)
-#define CK_ARG(cond, msg) \
-  do {                    \
-    if (!(cond)) return fail(CHFSI_EINVAL, msg); \
-  } while (0)
-#define CK(expr)              \
-  do {                        \
-    int _r = (expr);          \
-    if (_r != CHFSI_OK) return _r; \
-  } while (0)
+int ensure_pinned(chfsi_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->pinned_bytes) return CHFSI_OK;
+  CK_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->pinned) CK_CUDA(cudaFreeHost(ctx->pinned));
+  ctx->pinned = nullptr;
+  ctx->pinned_bytes = 0;
+  bytes = std::max<size_t>(bytes, 4096);
+  CK_CUDA(cudaMallocHost(&ctx->pinned, bytes));
+  ctx->pinned_bytes = bytes;
+  return CHFSI_OK;
+}
+}  // namespace chfsi
+
+namespace {
+
+using chfsi::fail;
 
 int ensure_ws(chfsi_ctx* ctx, size_t bytes) {
   if (bytes <= ctx->ws_bytes) return CHFSI_OK;
@@ -122,7 +85,7 @@ int chfsi_version(void) { return 1; }
 
 long long chfsi_launch_count(void) { return chfsi::g_launches.load(std::memory_order_relaxed); }
 
-const char* chfsi_last_error(void) { return g_last_error.c_str(); }
+const char* chfsi_last_error(void) { return chfsi::g_last_error.c_str(); }
 
 int chfsi_ctx_create(int device, chfsi_ctx** out) {
   CK_ARG(out != nullptr, "out is NULL");
@@ -174,6 +137,9 @@ int chfsi_ctx_destroy(chfsi_ctx* ctx) {
   cudaFree(ctx->lstate);
   cudaFree(ctx->step_ws.partials);
   cudaFree(ctx->step_ws.flags);
+  for (cudaEvent_t e : ctx->loop_ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;
   return CHFSI_OK;
 }
@@ -478,13 +444,14 @@ int qr_cholqr3(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdi
                         CUBLAS_DIAG_NON_UNIT, m, n, &one, reinterpret_cast<const cuDoubleComplex*>(g),
                         n, reinterpret_cast<cuDoubleComplex*>(y), m));
   }
-  std::vector<double> hd(n);
-  int info[3] = {0, 0, 0};
-  double hfro = 0.0;
-  CK_CUDA(cudaMemcpyAsync(hd.data(), rdiag_acc, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK_CUDA(cudaMemcpyAsync(info, ctx->dinfo, sizeof(info), cudaMemcpyDeviceToHost, s));
-  CK_CUDA(cudaMemcpyAsync(&hfro, fro, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(chfsi::ensure_pinned(ctx, (size_t)(n + 1) * sizeof(double) + 4 * sizeof(int)));
+  double* hd = static_cast<double*>(ctx->pinned);
+  int* info = reinterpret_cast<int*>(hd + n + 1);
+  CK_CUDA(cudaMemcpyAsync(hd, rdiag_acc, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK_CUDA(cudaMemcpyAsync(hd + n, fro, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK_CUDA(cudaMemcpyAsync(info, ctx->dinfo, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
   CK_CUDA(cudaStreamSynchronize(s));
+  const double hfro = hd[n];
   if (info[0] || info[1] || info[2] || !std::isfinite(hfro)) {
     *fallback = true;
     return CHFSI_OK;
@@ -552,18 +519,23 @@ int chfsi_ctx_set_qr_mode(chfsi_ctx* ctx, int mode) {
 namespace {
 
 // Near-diagonal Hermitian eigensolver (nd_eig.cu): simultaneous first-order
-// Jacobi steps X = I + S, S_ij = G_ij / (d_j - d_i), made unitary by two
-// Newton-Schulz polar iterations, G <- X^H G X, W <- W X. Converges
-// quadratically in max|G_ij| / gap. *done = false (A untouched) when G is not
-// in that regime or does not reach max|G_ij| <= tol * max(1, max|G_ii|).
+// Jacobi steps X = I + S, S_ij = G_ij / (d_j - d_i); W <- W X made unitary by
+// Newton-Schulz polar iterations; G = W^H G0 W projected exactly from the
+// input, so G stays unitarily similar to it and the off-diagonal/gap ratio r
+// squares every step. Adaptive: after each step's O(w^2) measurement the host
+// stops as soon as max|G_ij| <= tol * max(1, max|G_ii|), and the number of
+// NS iterations follows r (the unitarity defect of W X is ~|S|^2 and squares
+// per NS iteration). *done = false (A untouched) when G is not in that regime
+// (r > 0.1), does not converge within kMaxSteps, or W is not unitary to
+// rounding (defect at the last NS input > 1e-8): the caller uses zheevd.
 int heev_near_diag(chfsi_ctx* ctx, int n, double2* a, long long lda, double* w, double tol,
                    bool* done) {
   *done = false;
   cudaStream_t s = ctx->stream;
   const size_t mat = (size_t)n * n * sizeof(double2);
-  constexpr int kMaxIt = 6;
-  const size_t need = 5 * mat + (kMaxIt + 1) * 4 * sizeof(double) + (size_t)n * sizeof(int) + 1024;
-  static_assert(kMaxIt >= 5, "two rounds of steps plus measurements");
+  constexpr int kMaxSteps = 4;
+  constexpr int kSlots = 4 * (kMaxSteps + 1) + kMaxSteps;  // build stats + NS defects
+  const size_t need = 5 * mat + kSlots * sizeof(double) + (size_t)n * sizeof(int) + 1024;
   if (need > ctx->eig_ws_bytes) {
     CK_CUDA(cudaStreamSynchronize(s));
     if (ctx->eig_ws) CK_CUDA(cudaFree(ctx->eig_ws));
@@ -572,13 +544,16 @@ int heev_near_diag(chfsi_ctx* ctx, int n, double2* a, long long lda, double* w, 
     CK_CUDA(cudaMalloc(&ctx->eig_ws, need));
     ctx->eig_ws_bytes = need;
   }
+  CK(chfsi::ensure_pinned(ctx, kSlots * sizeof(double)));
   double2* G0 = reinterpret_cast<double2*>(ctx->eig_ws);  // the input, kept for the exact projection
   double2* G = G0 + (size_t)n * n;                          // working iterate
   double2* X = G + (size_t)n * n;
   double2* Y = X + (size_t)n * n;
   double2* W = Y + (size_t)n * n;                           // accumulated eigenvector basis
-  double* stats = reinterpret_cast<double*>(W + (size_t)n * n);  // [step][4]
-  int* perm = reinterpret_cast<int*>(stats + (kMaxIt + 1) * 4);
+  double* stats = reinterpret_cast<double*>(W + (size_t)n * n);  // [step][4], then [step] NS defect
+  double* defect = stats + 4 * (kMaxSteps + 1);
+  int* perm = reinterpret_cast<int*>(stats + kSlots);
+  double* hs = static_cast<double*>(ctx->pinned);
   const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
   auto gemm = [&](cublasOperation_t ta, const double2* A_, const double2* B_, double2* C_) -> int {
     CK_BLAS(cublasZgemm(ctx->blas, ta, CUBLAS_OP_N, n, n, n, &one,
@@ -587,45 +562,43 @@ int heev_near_diag(chfsi_ctx* ctx, int n, double2* a, long long lda, double* w, 
                         reinterpret_cast<cuDoubleComplex*>(C_), n));
     return CHFSI_OK;
   };
-  CK_CUDA(cudaMemcpy2DAsync(G0, (size_t)n * sizeof(double2), a, (size_t)lda * sizeof(double2),
-                            (size_t)n * sizeof(double2), n, cudaMemcpyDeviceToDevice, s));
-  CK_CUDA(cudaMemcpyAsync(G, G0, mat, cudaMemcpyDeviceToDevice, s));
-  CK_CUDA(cudaMemsetAsync(stats, 0, (kMaxIt + 1) * 4 * sizeof(double), s));
-  std::vector<double> hs((kMaxIt + 1) * 4);
-  // Each step: X = I + S from the current G; W <- W X made unitary to
-  // rounding by Newton-Schulz polar steps (X^H X = I - S^2, so 3 steps take
-  // ||S||^2 ~ 1e-3 below 1e-16); G = W^H G0 W projected exactly, so G stays
-  // unitarily similar to the input and the off-diagonal/gap ratio squares.
-  constexpr int kSteps = 3;
-  for (int it = 0; it < kSteps; ++it) {
-    CK_CUDA(chfsi::nd_build_step_launch(G, n, n, X, n, stats + 4 * it, s));
+  CK_CUDA(cudaMemsetAsync(stats, 0, kSlots * sizeof(double), s));
+  CK_CUDA(chfsi::copy_cols_launch(a, lda, G0, n, n, n, s));
+  const double2* Gcur = G0;  // step 0 measures the input directly
+  double last_defect = 0.0;
+  for (int it = 0;; ++it) {
+    CK_CUDA(chfsi::nd_build_step_launch(Gcur, n, n, X, n, stats + 4 * it, s));
+    CK_CUDA(cudaMemcpyAsync(hs, stats + 4 * it, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (it > 0)
+      CK_CUDA(cudaMemcpyAsync(hs + 4, defect + it - 1, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK_CUDA(cudaStreamSynchronize(s));
+    const double rmax = hs[0], emax = hs[1], dmax = hs[2];
+    if (it > 0) last_defect = hs[4];
+    if (it > 0 && emax <= tol * std::max(1.0, dmax)) {
+      if (!(last_defect <= 1e-8)) return CHFSI_OK;  // W not unitary to rounding: zheevd
+      break;
+    }
+    if (it == kMaxSteps || !(rmax <= 0.1)) return CHFSI_OK;  // not near-diagonal / not converging
     if (it == 0) {
-      // regime check before spending the ZGEMMs: bail out to zheevd early
-      double r0 = 0.0;
-      CK_CUDA(cudaMemcpyAsync(&r0, stats, sizeof(double), cudaMemcpyDeviceToHost, s));
-      CK_CUDA(cudaStreamSynchronize(s));
-      if (!(r0 <= 0.1)) return CHFSI_OK;
-      std::swap(W, X);                 // W = X
+      std::swap(W, X);  // W = X
     } else {
       CK(gemm(CUBLAS_OP_N, W, X, Y));
-      std::swap(W, Y);                 // W = W X
+      std::swap(W, Y);  // W = W X
     }
-    for (int ns = 0; ns < 3; ++ns) {   // W <- W (3I - W^H W) / 2
+    // unitarity defect of W X ~ |S|^2 <~ (sqrt(n) r)^2, squared by each NS step
+    const double sr = std::sqrt((double)n) * rmax;
+    const int ns = sr <= 5e-5 ? 1 : (sr <= 7e-3 ? 2 : 3);
+    for (int k = 0; k < ns; ++k) {  // W <- W (3I - W^H W) / 2
       CK(gemm(CUBLAS_OP_C, W, W, Y));
-      CK_CUDA(chfsi::nd_ns_matrix_launch(Y, n, n, s));
+      CK_CUDA(chfsi::nd_ns_matrix_launch(Y, n, n, k == ns - 1 ? defect + it : nullptr, s));
       CK(gemm(CUBLAS_OP_N, W, Y, X));
       std::swap(W, X);
     }
-    CK(gemm(CUBLAS_OP_N, G0, W, X));   // X = G0 W
-    CK(gemm(CUBLAS_OP_C, W, X, G));    // G = W^H G0 W
+    CK(gemm(CUBLAS_OP_N, G0, W, X));  // X = G0 W
+    CK(gemm(CUBLAS_OP_C, W, X, G));   // G = W^H G0 W
     CK_CUDA(chfsi::symmetrize_launch(G, n, n, s));
+    Gcur = G;
   }
-  CK_CUDA(chfsi::nd_build_step_launch(G, n, n, X, n, stats + 4 * kSteps, s));  // measure only
-  CK_CUDA(cudaMemcpyAsync(hs.data(), stats, hs.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK_CUDA(cudaStreamSynchronize(s));
-  const double rmax0 = hs[0], emax = hs[4 * kSteps + 1], dmax = hs[4 * kSteps + 2];
-  if (!(rmax0 <= 0.1)) return CHFSI_OK;                     // not near-diagonal: zheevd
-  if (!(emax <= tol * std::max(1.0, dmax))) return CHFSI_OK;  // not converged: zheevd
   // ascending eigenvalues, eigenvectors permuted accordingly, back into A
   CK_CUDA(chfsi::nd_sort_launch(G, n, n, w, perm, s));
   CK_CUDA(chfsi::nd_gather_cols_launch(W, n, n, n, perm, a, lda, s));

@@ -122,7 +122,7 @@ cudaError_t diag_accumulate_launch(const double2* r, long long ldr, int n, doubl
 // near-diagonal Hermitian eigensolver pieces (nd_eig.cu)
 cudaError_t nd_build_step_launch(const double2* g, long long ldg, int n, double2* x, long long ldx,
                                  double* stats, cudaStream_t s);
-cudaError_t nd_ns_matrix_launch(double2* t, long long ldt, int n, cudaStream_t s);
+cudaError_t nd_ns_matrix_launch(double2* t, long long ldt, int n, double* defect, cudaStream_t s);
 cudaError_t nd_sort_launch(const double2* g, long long ldg, int n, double* w, int* perm,
                            cudaStream_t s);
 cudaError_t nd_gather_cols_launch(const double2* src, long long lds, int m, int n, const int* perm,

@@ -1,0 +1,190 @@
+// Native ChFSI inner loop (chfsi_solve_loop_z, include/chfsi.h).
+//
+// Restates the pass structure of the reference solver loop
+// (spectral_chain/chfsi.py:328-373) on top of libchfsi's own entry points:
+//
+//   filter (K1 x deg)                                   chfsi.py:331-334
+//   2x CGS vs the locked block + QR, rank repair        chfsi.py:242-261
+//   Rayleigh-Ritz on the panel, residual norms          chfsi.py:337-350
+//   lock the leading Ritz pairs with res < tol          chfsi.py:352-366
+//   refresh the window [ritz[n_lock], ritz[-1]]         chfsi.py:367-373
+//
+// Host work per pass is a few dozen scalar operations; the only host<->device
+// traffic is the blk Ritz values and residuals the locking test needs (one
+// stream synchronisation per pass, plus the near-diagonal eigensolver's
+// regime checks). Device phase times are taken with events on the stream.
+#include <cmath>
+#include <vector>
+
+#include "abi_internal.h"
+
+namespace {
+
+using chfsi::fail;
+
+// chfsi.py:264-271: clamp the refreshed window back to scale_ref < a < b.
+void safe_window(double scale_ref, double a, double b, double* out_a, double* out_b) {
+  if (!std::isfinite(scale_ref) || !std::isfinite(a) || !std::isfinite(b) || !(scale_ref < b)) {
+    *out_a = scale_ref + 0.5;
+    *out_b = scale_ref + 1.0;
+    return;
+  }
+  if (!(scale_ref < a && a < b)) a = scale_ref + 0.5 * (b - scale_ref);
+  *out_a = a;
+  *out_b = b;
+}
+
+double2* col(void* base, long long ld, int j) { return static_cast<double2*>(base) + (long long)j * ld; }
+
+int ensure_events(chfsi_ctx* ctx) {
+  for (cudaEvent_t& e : ctx->loop_ev)
+    if (!e) CK_CUDA(cudaEventCreate(&e));
+  return CHFSI_OK;
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  return cudaEventElapsedTime(&ms, a, b) == cudaSuccess ? ms : 0.f;
+}
+
+// Two CGS passes against the locked block, then QR; rank-deficient columns
+// are replaced through the fill callback and the whole panel is redone,
+// at most `retries` times (chfsi.py:242-261).
+int orthonormalize(chfsi_ctx* ctx, chfsi_loop* L, void* work, int width) {
+  const int n = L->n;
+  constexpr int retries = 3;
+  std::vector<int> dead(width);
+  for (int attempt = 0;; ++attempt) {
+    if (L->nlocked)
+      CK(chfsi_cgs_project_z(ctx, n, L->nlocked, width, L->locked, n, work, n, L->coef));
+    int ndead = 0;
+    const int rc = chfsi_qr_orthonormalize_z(ctx, n, width, work, n, dead.data(), &ndead);
+    if (rc != CHFSI_ERANK) return rc;
+    if (attempt == retries || !L->fill) return rc;
+    if (L->fill(L->user, work, n, n, dead.data(), ndead) != 0)
+      return fail(CHFSI_EINVAL, "rank-repair fill callback failed");
+  }
+}
+
+// HP = H P; G = P^H HP symmetrised; eigenpairs (near-diagonal solver when
+// allowed, else zheevd); P W, HP W; residual norms (chfsi.py:337-350).
+int rayleigh_ritz(chfsi_ctx* ctx, chfsi_loop* L, const void* q, void* rot_p, int width, double eig_tol,
+                  int* used_fast) {
+  const int n = L->n;
+  const long long ldg = L->blk;
+  CK(chfsi_cheb_step_z(ctx, n, width, L->H, L->ldh, L->conj_h, q, n, nullptr, 0, L->hp, n, 1.0, 0.0,
+                       0.0));
+  CK(chfsi_gemm_z(ctx, 'C', 'N', width, width, n, 1.0, 0.0, q, n, L->hp, n, 0.0, 0.0, L->g, ldg));
+  CK(chfsi_symmetrize_z(ctx, width, L->g, ldg));
+  CK(chfsi_heev_rr_z(ctx, width, L->g, ldg, L->ritz_d, eig_tol, used_fast));
+  CK(chfsi_gemm_z(ctx, 'N', 'N', n, width, width, 1.0, 0.0, q, n, L->g, ldg, 0.0, 0.0, rot_p, n));
+  CK(chfsi_gemm_z(ctx, 'N', 'N', n, width, width, 1.0, 0.0, L->hp, n, L->g, ldg, 0.0, 0.0,
+                  L->hp_rot, n));
+  CK(chfsi_colnorm_residual_z(ctx, n, width, L->hp_rot, n, rot_p, n, L->ritz_d, L->res_d));
+  return CHFSI_OK;
+}
+
+}  // namespace
+
+extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
+  CK_ARG(ctx && L, "NULL argument");
+  CK_ARG(L->n >= 1 && 1 <= L->nev && L->nev <= L->blk && L->blk <= L->n, "need 1 <= nev <= blk <= n");
+  CK_ARG(L->deg >= 1 && L->max_repeats >= 0 && L->tol > 0, "bad degree / repeats / tolerance");
+  CK_ARG(L->H && L->bufs[0] && L->bufs[1] && L->hp && L->hp_rot && L->locked && L->g && L->coef &&
+             L->ritz_d && L->res_d,
+         "NULL device buffer");
+  CK_ARG(L->locked_vals && L->locked_res && L->locked_per_loop && L->ritz && L->res,
+         "NULL host output");
+  CK_ARG(L->pb == 0 || L->pb == 1, "bad panel buffer index");
+  CK_ARG(L->off >= 0 && L->width >= 1 && L->off + L->width <= L->blk, "bad panel window");
+  CK(ensure_events(ctx));
+  cudaStream_t s = ctx->stream;
+  cudaEvent_t* ev = ctx->loop_ev;
+  const int n = L->n;
+  CK(chfsi::ensure_pinned(ctx, 2 * (size_t)L->blk * sizeof(double)));
+
+  while (L->inner_loops < L->max_repeats) {
+    L->inner_loops += 1;
+    const int width = L->width;
+    void* panel = col(L->bufs[L->pb], n, L->off);
+    void* other = L->bufs[1 - L->pb];
+
+    // ---- filter (chfsi.py:331-334)
+    CK_CUDA(cudaEventRecord(ev[0], s));
+    void* result = nullptr;
+    if (L->filter) {
+      if (L->filter(L->user, panel, other, n, width, L->deg, L->win_a, L->win_b, L->win_scale_ref,
+                    &result) != 0 || !result)
+        return fail(CHFSI_EINVAL, "filter callback failed");
+    } else {
+      CK(chfsi_filter_z(ctx, n, width, L->H, L->ldh, L->conj_h, panel, n, other, panel, n, L->deg,
+                        L->win_a, L->win_b, L->win_scale_ref, &result));
+    }
+    CK_CUDA(cudaEventRecord(ev[1], s));
+    L->filter_launches += L->deg;
+    L->filtered_vectors += width;
+    L->matvecs += (long long)L->deg * width;
+    L->filter_flops += 8.0 * (double)n * (double)n * (double)L->deg * (double)width;
+    const bool q_in_other = result == other;
+
+    // ---- orthonormalize (chfsi.py:335-336)
+    CK(orthonormalize(ctx, L, result, width));
+    CK_CUDA(cudaEventRecord(ev[2], s));
+
+    // ---- Rayleigh-Ritz into the buffer the filter left free (chfsi.py:337-350)
+    const int rot_pb = q_in_other ? L->pb : 1 - L->pb;
+    void* rot_p = L->bufs[rot_pb];
+    const double eig_tol = (L->try_fast && L->rr_fast_tol > 0.0) ? L->rr_fast_tol : 0.0;
+    int used_fast = 0;
+    CK(rayleigh_ritz(ctx, L, result, rot_p, width, eig_tol, &used_fast));
+    CK_CUDA(cudaEventRecord(ev[3], s));
+    L->rr_fast_eigs += used_fast;
+    if (L->try_fast && !used_fast) L->try_fast = 0;
+    L->residual_check_matvecs += width;
+    L->matvecs += width;
+    double* host = static_cast<double*>(ctx->pinned);  // (re-read: RR may have grown it)
+    CK_CUDA(cudaMemcpyAsync(host, L->ritz_d, (size_t)width * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK_CUDA(cudaMemcpyAsync(host + width, L->res_d, (size_t)width * sizeof(double),
+                            cudaMemcpyDeviceToHost, s));
+    CK_CUDA(cudaStreamSynchronize(s));
+    L->t_filter += 1e-3 * elapsed(ev[0], ev[1]);
+    L->t_ortho += 1e-3 * elapsed(ev[1], ev[2]);
+    L->t_rr += 1e-3 * elapsed(ev[2], ev[3]);
+    const double* ritz = host;
+    const double* res = host + width;
+    for (int j = 0; j < width; ++j) {
+      L->ritz[j] = ritz[j];
+      L->res[j] = res[j];
+    }
+
+    // ---- locking (chfsi.py:352-366)
+    int n_lock = 0;
+    while (n_lock < width && L->nlocked + n_lock < L->nev && res[n_lock] < L->tol) ++n_lock;
+    if (n_lock) {
+      L->try_fast = 1;
+      for (int j = 0; j < n_lock; ++j) {
+        L->locked_vals[L->nlocked + j] = ritz[j];
+        L->locked_res[L->nlocked + j] = res[j];
+      }
+      CK_CUDA(cudaMemcpyAsync(col(L->locked, n, L->nlocked), rot_p,
+                              (size_t)n * n_lock * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+      L->nlocked += n_lock;
+    }
+    L->locked_per_loop[L->inner_loops - 1] = n_lock;
+    L->last_rot_pb = rot_pb;
+    L->last_width = width;
+    L->last_nlock = n_lock;
+    if (L->nlocked >= L->nev) {
+      L->converged = 1;
+      break;
+    }
+
+    // ---- next panel and window (chfsi.py:367-373)
+    L->pb = rot_pb;
+    L->off = n_lock;
+    L->width = width - n_lock;
+    L->win_scale_ref = ritz[n_lock];
+    safe_window(ritz[n_lock], ritz[width - 1], L->win_b, &L->win_a, &L->win_b);
+  }
+  return CHFSI_OK;
+}

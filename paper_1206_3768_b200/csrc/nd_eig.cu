@@ -21,6 +21,9 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
   atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
 }
 
+// max that propagates NaN (fmax drops it): a NaN anywhere must fail the checks
+__device__ __forceinline__ double pmax(double a, double b) { return (b > a || isnan(b)) ? b : a; }
+
 // X = I + S with S_ij = G_ij / (d_j - d_i); stats[0] = max_ij |G_ij| / |d_j - d_i|,
 // stats[1] = max_ij |G_ij| (i != j), stats[2] = max_i |d_i|.
 __global__ void nd_build_step_kernel(const double2* __restrict__ g, long long ldg, int n,
@@ -33,17 +36,17 @@ __global__ void nd_build_step_kernel(const double2* __restrict__ g, long long ld
     double2 out;
     if (i == j) {
       out = make_double2(1.0, 0.0);
-      dmax = fmax(dmax, fabs(g[(long long)i * ldg + i].x));
+      dmax = pmax(dmax, fabs(g[(long long)i * ldg + i].x));
     } else {
       const double2 e = g[(long long)j * ldg + i];
       const double gap = g[(long long)j * ldg + j].x - g[(long long)i * ldg + i].x;
       const double ae = hypot(e.x, e.y);
-      emax = fmax(emax, ae);
+      emax = pmax(emax, ae);
       if (ae == 0.0) {
         out = make_double2(0.0, 0.0);
       } else {
         const double ag = fabs(gap);
-        rmax = fmax(rmax, ag > 0.0 ? ae / ag : INFINITY);
+        rmax = pmax(rmax, ag > 0.0 ? ae / ag : INFINITY);
         out = make_double2(e.x / gap, e.y / gap);
       }
     }
@@ -54,9 +57,9 @@ __global__ void nd_build_step_kernel(const double2* __restrict__ g, long long ld
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    rmax = fmax(rmax, __shfl_down_sync(0xffffffffu, rmax, o));
-    emax = fmax(emax, __shfl_down_sync(0xffffffffu, emax, o));
-    dmax = fmax(dmax, __shfl_down_sync(0xffffffffu, dmax, o));
+    rmax = pmax(rmax, __shfl_down_sync(0xffffffffu, rmax, o));
+    emax = pmax(emax, __shfl_down_sync(0xffffffffu, emax, o));
+    dmax = pmax(dmax, __shfl_down_sync(0xffffffffu, dmax, o));
   }
   if (lane == 0) {
     sh[0][wid] = rmax;
@@ -66,9 +69,9 @@ __global__ void nd_build_step_kernel(const double2* __restrict__ g, long long ld
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-      rmax = fmax(rmax, sh[0][w]);
-      emax = fmax(emax, sh[1][w]);
-      dmax = fmax(dmax, sh[2][w]);
+      rmax = pmax(rmax, sh[0][w]);
+      emax = pmax(emax, sh[1][w]);
+      dmax = pmax(dmax, sh[2][w]);
     }
     if (!(rmax <= 1e300)) rmax = 1e300;  // inf / nan: "not near-diagonal"
     atomic_max_nonneg(stats + 0, rmax);
@@ -78,14 +81,29 @@ __global__ void nd_build_step_kernel(const double2* __restrict__ g, long long ld
 }
 
 // M = 1.5 I - 0.5 T   (Newton-Schulz polar step X <- X M with T = X^H X)
-__global__ void nd_ns_matrix_kernel(double2* t, long long ldt, int n) {
+__global__ void nd_ns_matrix_kernel(double2* t, long long ldt, int n, double* defect) {
   const long long total = (long long)n * n;
+  double dmax = 0.0;  // max |T - I|: the unitarity defect of the NS input
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     const int j = (int)(idx / n), i = (int)(idx % n);
     double2* p = t + (long long)j * ldt + i;
     const double2 v = *p;
+    dmax = pmax(dmax, hypot(v.x - (i == j ? 1.0 : 0.0), v.y));
     *p = make_double2((i == j ? 1.5 : 0.0) - 0.5 * v.x, -0.5 * v.y);
+  }
+  if (defect == nullptr) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dmax = pmax(dmax, __shfl_down_sync(0xffffffffu, dmax, o));
+  __shared__ double sh[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) sh[wid] = dmax;
+  __syncthreads();
+  if (wid == 0) {
+    dmax = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dmax = pmax(dmax, __shfl_down_sync(0xffffffffu, dmax, o));
+    if (lane == 0) atomic_max_nonneg(defect, dmax);
   }
 }
 
@@ -131,9 +149,9 @@ cudaError_t nd_build_step_launch(const double2* g, long long ldg, int n, double2
   return cudaGetLastError();
 }
 
-cudaError_t nd_ns_matrix_launch(double2* t, long long ldt, int n, cudaStream_t s) {
+cudaError_t nd_ns_matrix_launch(double2* t, long long ldt, int n, double* defect, cudaStream_t s) {
   note_launch();
-  nd_ns_matrix_kernel<<<grid_for((long long)n * n), 256, 0, s>>>(t, ldt, n);
+  nd_ns_matrix_kernel<<<grid_for((long long)n * n), 256, 0, s>>>(t, ldt, n, defect);
   return cudaGetLastError();
 }
 
