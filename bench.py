@@ -330,6 +330,7 @@ def run_ours(args):
                     "t_reduce_ms": round(r.t_reduce * 1e3, 3),
                     "t_back_ms": round(r.t_back * 1e3, 3),
                     "rr_fast_eigs": r.report.rr_fast_eigs,
+                    "host_ms": {k: round(v * 1e3, 3) for k, v in r.report.host_phases.items()},
                     "dev_ms": {k: round(getattr(r.report, "t_" + k) * 1e3, 3)
                                for k in ("lanczos", "filter", "ortho", "rr")}}
                    for r in results[-1]]

@@ -57,8 +57,9 @@ CHFSI_API long long chfsi_launch_count(void);
 CHFSI_API int chfsi_ctx_create(int device, chfsi_ctx** out);
 CHFSI_API int chfsi_ctx_destroy(chfsi_ctx* ctx);
 CHFSI_API int chfsi_ctx_set_stream(chfsi_ctx* ctx, void* cuda_stream);
-/* Force the K1 tiling for tests and tuning: bm = 64, bn = 16|32|64 columns
- * per CTA tile, grid = number of persistent CTAs (0 = all resident CTAs;
+/* Force the K1 tiling for tests and tuning: (bm, bn) = 64x16 | 64x32 |
+ * 64x64 (8 warps, two CTAs per SM) or 128x16 | 128x32 (16 warps, one CTA per
+ * SM), plus 32x32 | 32x64, grid = number of persistent CTAs (0 = all resident CTAs;
  * fewer CTAs exercise other stream-K splits). bm = 0 restores automatic. */
 CHFSI_API int chfsi_ctx_set_tiling(chfsi_ctx* ctx, int bm, int bn, int grid);
 
@@ -97,6 +98,12 @@ CHFSI_API int chfsi_filter_coeffs(int deg, double a, double b, double scale_ref,
 CHFSI_API int chfsi_filter_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, int conj_h,
                    const void* y0, long long ldy0, void* buf_a, void* buf_b, long long ldb,
                    int deg, double a, double b, double scale_ref, void** result);
+
+/* Diagnostics: with CHFSI_K1_DEBUG=8 in the environment every K1 launch
+ * records per-CTA [start, owner-wait begin, owner-wait end, end]
+ * (%globaltimer ns) and the SM id; this copies the last launch's records
+ * (5 values per CTA) and returns the number of CTAs (0: tracing off). */
+CHFSI_API int chfsi_debug_k1_trace(unsigned long long* host, int max_ctas);
 
 /* Introspection of the K1 tile choice for an (n, w) step. */
 CHFSI_API int chfsi_step_tiling(int n, int w, int* bm, int* bn, int* split);

@@ -66,6 +66,7 @@ _SIGNATURES = {
     "chfsi_filter_z": [_vp, _i, _i, _vp, _ll, _i, _vp, _ll, _vp, _vp, _ll, _i, _d, _d, _d,
                        ctypes.POINTER(_vp)],
     "chfsi_step_tiling": [_i, _i, _pi, _pi, _pi],
+    "chfsi_debug_k1_trace": [ctypes.POINTER(ctypes.c_ulonglong), _i],
     "chfsi_lanczos_z": [_vp, _i, _i, _vp, _ll, _i, _vp, _vp, _pd, _pd, _pd, _pi],
     "chfsi_gemm_z": [_vp, _c, _c, _i, _i, _i, _d, _d, _vp, _ll, _vp, _ll, _d, _d, _vp, _ll],
     "chfsi_cgs_project_z": [_vp, _i, _i, _i, _vp, _ll, _vp, _ll, _vp],

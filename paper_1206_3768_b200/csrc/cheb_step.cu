@@ -46,8 +46,8 @@ namespace {
 
 constexpr int BK = 16;             // complex elements per K slab (two 128-byte halves)
 constexpr int HALF = 128;          // bytes per row per half-slab (one TMA box row)
-constexpr int kMaxThreads = 256;
-constexpr int kMaxAcc = 32;        // doubles per thread in a partial tile (upper bound)
+constexpr int kMaxThreads = 512;
+constexpr int kSlotDoubles = 8192; // partial-tile slot per CTA: ACC * THREADS <= this
 
 struct StepParams {
   const double2* ycur;  // rows of Ycur matching the output rows (epilogue c*Ycur term)
@@ -71,6 +71,7 @@ struct StepParams {
   unsigned* flags;     // [grid]
   unsigned epoch;
   int dbg;             // diagnostics (CHFSI_K1_DEBUG): 1 = block barrier before each refill
+  unsigned long long* trace;  // dbg & 8: per CTA [start, owner wait begin, wait end, end, smid]
 };
 
 // ------------------------------------------------------------ PTX helpers ---
@@ -115,6 +116,16 @@ __device__ __forceinline__ void tma_load_3d(unsigned dst, const CUtensorMap* map
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -128,6 +139,14 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 // g+1 (same LDS.128 phase) land 4 apart, i.e. in opposite 64-byte halves
 // of the 128B-swizzled row, so the 8 lanes of a phase hit 32 distinct banks.
 __device__ __forceinline__ int sigma(int g) { return ((g & 1) << 2) | (g >> 1); }
+
+// First stream-K iteration of CTA c: even split. (Measured: the warp
+// schedulers favour the older of two co-resident CTAs — the lower blockIdx
+// finishes first on every SM — but the pairing of CTAs on SMs is not fixed,
+// so weighting the split by blockIdx made the worst SM slower.)
+__device__ __forceinline__ int sk_begin(const StepParams& p, int c) {
+  return (int)((long long)c * p.sk_iters / p.sk_ctas);
+}
 
 __device__ __forceinline__ void epilogue_store(const StepParams& p, int row, int col, double ar,
                                                double ai) {
@@ -159,7 +178,7 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
   constexpr int A_BYTES = BM * HALF;  // one half-slab of A
   constexpr int B_BYTES = BN * HALF;
   constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
-  static_assert(THREADS <= kMaxThreads && ACC <= kMaxAcc, "workspace bound");
+  static_assert(THREADS <= kMaxThreads && ACC * THREADS <= kSlotDoubles, "workspace bound");
   static_assert(MI >= 1 && NI >= 1, "warp tile too small");
   static_assert(A_BYTES % 1024 == 0 && B_BYTES % 1024 == 0, "128B swizzle needs 1024B-aligned boxes");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -173,25 +192,46 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp / WN, wn = warp % WN;
-  const int G = gridDim.x, cta = blockIdx.x;
+  const int G = gridDim.x;
+  const int cta = (p.dbg & 16) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x;  // 16: reversed (diagnostic)
   const int kiters = p.kiters;
 
   // ---- this CTA's slice of the linearised iteration space (64-bit once)
   const int dp_iters = p.dp_waves * kiters;
   int sb = 0, se = 0;
   if (cta < p.sk_ctas) {
-    sb = (int)((long long)cta * p.sk_iters / p.sk_ctas);
-    se = (int)((long long)(cta + 1) * p.sk_iters / p.sk_ctas);
+    sb = sk_begin(p, cta);
+    se = sk_begin(p, cta + 1);
   }
   const int total = dp_iters + (se - sb);
   if (total == 0) return;
-  // Local order: [publish segment] [data-parallel tiles] [rest of stream-K]
-  int pub = 0;
-  if (se > sb && (se % kiters) != 0) {
-    const int head = ((se - 1) / kiters) * kiters;
-    pub = se - (head > sb ? head : sb);
+  const bool tr = (p.dbg & 8) && threadIdx.x == 0;
+  if (tr) {
+    p.trace[cta * 5 + 0] = gtimer();
+    p.trace[cta * 5 + 4] = smid() | ((unsigned long long)blockIdx.x << 16);
   }
-  const int sk_tile0 = p.sk_first + sb / kiters, sk_kk0 = sb % kiters;
+  // Local order: [publish] [data-parallel tiles] [middle] [owner tail].
+  //   publish: the head of the last SK tile when the range ends inside it —
+  //            done first, so peers' partials are ready early;
+  //   middle:  whole SK tiles (epilogue directly);
+  //   tail:    the end of the first SK tile when the range starts inside it
+  //            — the CTA owns that tile and folds the peers' partials, so it
+  //            comes last, after the peers had the most time to publish.
+  int pub_start = se, tail_end = sb;
+  if (se > sb) {
+    if (se % kiters != 0) {
+      const int head = ((se - 1) / kiters) * kiters;
+      pub_start = head > sb ? head : sb;
+    }
+    if (sb % kiters != 0) {
+      const int nb = (sb / kiters + 1) * kiters;
+      tail_end = nb < se ? nb : se;
+    }
+    if (tail_end > pub_start) tail_end = sb;  // range inside one tile, not at its end: all publish
+  }
+  const int pub = se - pub_start;
+  const int mid_start = tail_end > sb ? tail_end : sb;
+  const int e1 = pub, e2 = e1 + dp_iters, e3 = e2 + (pub_start - mid_start);
 
   struct Cursor {
     int j, tile, kk, m0, n0;
@@ -202,28 +242,22 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
     c.m0 = (tile / p.tiles_n) * BM;
     c.n0 = (tile % p.tiles_n) * BN;
   };
+  auto set_sk = [&](Cursor& c, int it) { set_tile(c, p.sk_first + it / kiters, it % kiters); };
+  auto enter = [&](Cursor& c) {  // first iteration of the phase holding c.j
+    if (c.j < e1) set_sk(c, pub_start + c.j);
+    else if (c.j < e2) set_tile(c, cta, 0);
+    else if (c.j < e3) set_sk(c, mid_start + (c.j - e2));
+    else set_sk(c, sb + (c.j - e3));
+  };
   auto start = [&](Cursor& c) {
     c.j = 0;
-    if (pub > 0) {
-      const int s0 = se - pub;
-      set_tile(c, p.sk_first + s0 / kiters, s0 % kiters);
-    } else if (dp_iters > 0) {
-      set_tile(c, cta, 0);
-    } else {
-      set_tile(c, sk_tile0, sk_kk0);
-    }
+    enter(c);
   };
   auto advance = [&](Cursor& c) {
     ++c.j;
     ++c.kk;
-    if (pub > 0 && c.j == pub) {
-      if (dp_iters > 0) set_tile(c, cta, 0);
-      else set_tile(c, sk_tile0, sk_kk0);
-    } else if (dp_iters > 0 && c.j == pub + dp_iters) {
-      set_tile(c, sk_tile0, sk_kk0);
-    } else if (c.kk == kiters) {
-      set_tile(c, c.tile + ((c.j < pub + dp_iters) ? G : 1), 0);
-    }
+    if (c.j == e1 || c.j == e2 || c.j == e3) enter(c);
+    else if (c.kk == kiters) set_tile(c, c.tile + ((c.j > e1 && c.j < e2) ? G : 1), 0);
   };
   // one elected thread: arm the stage's barrier and issue its four TMA boxes
   auto issue = [&](const Cursor& c, int stage) {
@@ -253,7 +287,7 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
   }
   __syncthreads();
 
-  Cursor lc;
+  Cursor lc;  // producer cursor (thread 0)
   start(lc);
   if (tid == 0) {
     for (int s = 0; s < STAGES && lc.j < total; ++s) {
@@ -339,6 +373,8 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
     // is an async-proxy (TMA) write of the same bytes: the proxy fence makes
     // the reads complete before the release (without it ptxas schedules the
     // arrive ahead of the last LDS and a slow warp can read refilled data).
+    // (Measured alternative: the last-arriving warp refills via a shared
+    // counter — no empty-barrier wait, but ~3 % slower at 2 CTAs/SM.)
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * stage);
@@ -381,11 +417,13 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
           epilogue(cc);
         } else {
           // owner: the peers are the CTAs whose ranges hold [tile_s0, sb)
-          const int first =
+          const int first =  // the CTA holding iteration tile_s0
               (int)(((long long)(tile_s0 + 1) * p.sk_ctas + p.sk_iters - 1) / p.sk_iters) - 1;
           if (tid == 0) {
+            if (tr) p.trace[cta * 5 + 1] = gtimer();
             for (int q = first; q < cta; ++q)
               while (ld_acquire(p.flags + q) != p.epoch) __nanosleep(64);
+            if (tr) p.trace[cta * 5 + 2] = gtimer();
           }
           __syncthreads();
           // fixed fold order: own partial, then peers first..cta-1
@@ -411,9 +449,13 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
     }
     advance(cc);
   }
+  if (tr) p.trace[cta * 5 + 3] = gtimer();
 }
 
 // --------------------------------------------------------------- host ---
+
+unsigned long long* g_trace = nullptr;  // CHFSI_K1_DEBUG & 8: last launch's per-CTA trace
+int g_trace_grid = 0;
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -498,7 +540,8 @@ const Variant* variant(int bm, int bn, bool conj) {
   CHFSI_V(64, 64, 4, 2, 3, 2)
   CHFSI_V(32, 32, 2, 2, 4, 3)
   CHFSI_V(32, 64, 2, 2, 3, 3)
-  CHFSI_V(128, 32, 4, 2, 3, 1)
+  CHFSI_V(128, 32, 8, 2, 5, 1)
+  CHFSI_V(128, 16, 8, 1, 6, 1)
 #undef CHFSI_V
   return nullptr;
 }
@@ -506,18 +549,31 @@ const Variant* variant(int bm, int bn, bool conj) {
 }  // namespace
 
 StepTiling choose_step_tiling(int n, int w) {
-  // Measured on B200 (profiles/r01_k1_variants.log): 64x32 is the best or
-  // within 2 % everywhere except very wide panels, where 64x64 gains ~4 %
-  // once there are enough whole tiles for data-parallel waves; 64x16 only
-  // pays when w <= 16 (padding).
+  // Measured on B200 (profiles/r01_k1_tiling.log, TFLOP/s per (n, w)):
+  //  * padding dominates at small w: 64x16 (8 warps x 8x16) runs at ~0.9x the
+  //    speed of 64x32 per padded column, so it wins when it pads >10 % less;
+  //  * n <= 4096: 64x32 otherwise (two CTAs per SM);
+  //  * large n: the 16-warp 128x32 CTA (one per SM, B tile reused by twice the
+  //    rows) reaches 33-35 TF/s (94 % of the DMMA peak at C4); 64x64 is
+  //    slightly ahead at n ~ 5000 when it pads no more than 64x32.
   if (w <= 16) return StepTiling{64, 16, 0};
-  const long long tiles64 = (long long)((n + 63) / 64) * ((w + 63) / 64);
-  const int pad32 = ((w + 31) / 32) * 32, pad64 = ((w + 63) / 64) * 64;
-  if (w >= 512 && tiles64 >= 4LL * kNumSMs && pad64 <= pad32) return StepTiling{64, 64, 0};
-  return StepTiling{64, 32, 0};
+  const int pad16 = ((w + 15) / 16) * 16, pad32 = ((w + 31) / 32) * 32, pad64 = ((w + 63) / 64) * 64;
+  if (pad16 * 10 < pad32 * 9) return StepTiling{64, 16, 0};
+  if (n <= 4096) return StepTiling{64, 32, 0};
+  if (n >= 8000 || w >= 400) return StepTiling{128, 32, 0};
+  return pad64 <= pad32 ? StepTiling{64, 64, 0} : StepTiling{64, 32, 0};
 }
 
-size_t step_workspace_doubles(int max_grid) { return (size_t)max_grid * kMaxAcc * kMaxThreads; }
+int step_trace_copy(unsigned long long* host, int max_ctas) {
+  if (!g_trace) return 0;
+  const int n = g_trace_grid < max_ctas ? g_trace_grid : max_ctas;
+  if (cudaMemcpy(host, g_trace, (size_t)n * 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) !=
+      cudaSuccess)
+    return -1;
+  return n;
+}
+
+size_t step_workspace_doubles(int max_grid) { return (size_t)max_grid * kSlotDoubles; }
 
 int step_grid_size(int bn, bool conj) {
   const Variant* v = variant(64, bn, conj);
@@ -545,6 +601,11 @@ cudaError_t cheb_step_rows_launch(const double2* h, long long ldh, bool conj_h, 
   if (vp == nullptr) return cudaErrorInvalidValue;
   const Variant& v = *vp;
   int grid = v.resident * kNumSMs;
+  static const int oversub = [] {
+    const char* e = getenv("CHFSI_K1_OVERSUB");  // tuning: CTAs per resident slot
+    return e ? atoi(e) : 1;
+  }();
+  if (oversub > 1) grid *= oversub;
   if (tiling.split > 0 && tiling.split < grid) grid = tiling.split;  // test/tuning override
   if (grid > ws.max_grid) return cudaErrorInvalidValue;
 
@@ -579,6 +640,15 @@ cudaError_t cheb_step_rows_launch(const double2* h, long long ldh, bool conj_h, 
     return e ? atoi(e) : 0;
   }();
   p.dbg = dbg;
+  if (dbg & 8) {
+    static unsigned long long* trace_buf = nullptr;
+    if (!trace_buf && cudaMalloc(&trace_buf, 4096 * 5 * sizeof(unsigned long long)) != cudaSuccess)
+      return cudaErrorMemoryAllocation;
+    g_trace = trace_buf;
+    g_trace_grid = grid;
+    cudaMemsetAsync(trace_buf, 0, (size_t)grid * 5 * sizeof(unsigned long long), stream);
+    p.trace = trace_buf;
+  }
   if ((dbg & 2) && tiles <= grid) grid = (int)tiles;  // one whole tile per CTA, no stream-K
   p.dp_waves = tiles >= 2LL * grid ? (int)(tiles / grid) - 1 : 0;
   if ((dbg & 2) && tiles == grid) p.dp_waves = 1;

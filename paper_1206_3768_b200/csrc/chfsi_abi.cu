@@ -111,7 +111,7 @@ int chfsi_ctx_create(int device, chfsi_ctx** out) {
   CK_CUDA(cudaMalloc(&ctx->dinfo, 4 * sizeof(int)));
   CK_CUDA(cudaMalloc(&ctx->lstate, sizeof(LanczosState)));
   // K1 stream-K scratch: partial tiles and ready flags for every resident CTA
-  ctx->step_ws.max_grid = chfsi::kNumSMs * 4;
+  ctx->step_ws.max_grid = chfsi::kNumSMs * 8;
   CK_CUDA(cudaMalloc(&ctx->step_ws.partials,
                      chfsi::step_workspace_doubles(ctx->step_ws.max_grid) * sizeof(double)));
   CK_CUDA(cudaMalloc(&ctx->step_ws.flags, ctx->step_ws.max_grid * sizeof(unsigned)));
@@ -256,6 +256,13 @@ int chfsi_filter_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, i
     ldcur = ldb;
   }
   return CHFSI_OK;
+}
+
+int chfsi_debug_k1_trace(unsigned long long* host, int max_ctas) {
+  CK_ARG(host && max_ctas >= 0, "bad argument");
+  const int n = chfsi::step_trace_copy(host, max_ctas);
+  if (n < 0) return fail(CHFSI_ECUDA, "trace copy failed");
+  return n;
 }
 
 int chfsi_step_tiling(int n, int w, int* bm, int* bn, int* split) {

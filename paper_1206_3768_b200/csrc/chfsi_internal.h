@@ -12,7 +12,7 @@ constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
 void note_launch();
 
 struct StepTiling {
-  int bm;     // 0 = choose automatically (bm is always 64)
+  int bm;     // 0 = choose automatically; 32, 64 or 128 rows per CTA tile
   int bn;     // 16, 32 or 64 columns per CTA tile
   int split;  // grid override for tests/tuning (0 = all resident CTAs)
 };
@@ -27,6 +27,9 @@ struct StepWorkspace {
 
 StepTiling choose_step_tiling(int n, int w);
 size_t step_workspace_doubles(int max_grid);
+// CHFSI_K1_DEBUG & 8 diagnostics: copy the last K1 launch's per-CTA trace
+// ([start, wait begin, wait end, end] globaltimer ns, smid) to host.
+int step_trace_copy(unsigned long long* host, int max_ctas);
 int step_grid_size(int bn, bool conj);
 
 // K1: Ynext = alpha*(op(H) Ycur - c Ycur) - beta Yprev; Yprev may alias Ynext
