@@ -259,7 +259,16 @@ def run_ours(args):
     lc0 = _lib.lib().chfsi_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    results = [device_step() for _ in range(args.steps)]
+    # keep only scalars of earlier steps: a caller that retained every
+    # step's solutions would grow the allocator (cudaMalloc) every step
+    step_stats = []
+    res = None
+    for _ in range(args.steps):
+        res = None  # release the previous step's solutions first
+        res = device_step()
+        step_stats.append([(r.report.t_filter, r.report.filter_flops, r.report.filter_launches)
+                           for r in res])
+    results = [res]
     e1.record()
     barrier()
     launches = _lib.lib().chfsi_launch_count() - lc0
@@ -267,9 +276,9 @@ def run_ours(args):
     t_dev = max_over_ranks(e0.elapsed_time(e1) / 1e3)
 
     flops_seq = sum(r.report.filter_flops for r in results[-1])
-    f_time = sum(r.report.t_filter for res in results for r in res)
-    f_flops = sum(r.report.filter_flops for res in results for r in res)
-    f_launch = sum(r.report.filter_launches for res in results for r in res)
+    f_time = sum(t for st in step_stats for t, _, _ in st)
+    f_flops = sum(f for st in step_stats for _, f, _ in st)
+    f_launch = sum(k for st in step_stats for _, _, k in st)
     replicas = 1 if args.shard else world  # sharded: all ranks solve ONE sequence together
     value = replicas * flops_seq * args.steps / t_dev / 1e9
 

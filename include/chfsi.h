@@ -208,7 +208,7 @@ typedef struct chfsi_loop {
   /* problem and device workspace (in) */
   int n, blk, nev, deg, max_repeats;
   double tol;
-  double rr_fast_tol;        /* > 0: near-diagonal RR eigensolver allowed (else zheevd only) */
+  double rr_fast_tol;        /* > 0: near-diagonal RR eigensolver tried first (else zheevd only) */
   const void* H;
   long long ldh;
   int conj_h;
@@ -225,7 +225,6 @@ typedef struct chfsi_loop {
   void* user;
   /* window and loop state (in/out) */
   double win_a, win_b, win_scale_ref;
-  int try_fast;
   int inner_loops, nlocked, pb, off, width, converged;
   int last_rot_pb, last_width, last_nlock; /* the final pass's rotated panel */
   /* host outputs (caller-owned arrays) */

@@ -100,7 +100,6 @@ class LoopState(ctypes.Structure):
         ("coef", _vp), ("ritz_d", _vp), ("res_d", _vp),
         ("filter", FILTER_CB), ("fill", FILL_CB), ("user", _vp),
         ("win_a", _d), ("win_b", _d), ("win_scale_ref", _d),
-        ("try_fast", _i),
         ("inner_loops", _i), ("nlocked", _i), ("pb", _i), ("off", _i), ("width", _i),
         ("converged", _i),
         ("last_rot_pb", _i), ("last_width", _i), ("last_nlock", _i),

@@ -466,8 +466,8 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     st = LoopState()
     st.n, st.blk, st.nev, st.deg, st.max_repeats = n, blk, cfg.nev, deg, max_repeats
     st.tol = tol
-    # near-diagonal eigensolver once the panel is close to invariant (warm
-    # starts, or after the first locking); zheevd otherwise
+    # near-diagonal Rayleigh-Ritz eigensolver first (bails out to zheevd when
+    # the projection is not close to diagonal)
     st.rr_fast_tol = RR_FAST_TOL if tol >= 1e-11 else 0.0
     st.H, st.ldh, st.conj_h = op.tensor.data_ptr(), op.ld, int(op.conj)
     st.bufs[0], st.bufs[1] = bufs[0].data_ptr(), bufs[1].data_ptr()
@@ -475,7 +475,6 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     st.g, st.coef = g_buf.data_ptr(), coef.data_ptr()
     st.ritz_d, st.res_d = ritz_d.data_ptr(), res_d.data_ptr()
     st.win_a, st.win_b, st.win_scale_ref = window.a, window.b, window.scale_ref
-    st.try_fast = int(guess is not None)  # warm panels give near-diagonal projections
     st.pb, st.off, st.width = 0, 0, blk
     host_f = np.zeros((4, blk))
     locked_per_loop = np.zeros(max(max_repeats, 1), dtype=np.int32)

@@ -142,8 +142,10 @@ __device__ __forceinline__ int sigma(int g) { return ((g & 1) << 2) | (g >> 1); 
 
 // First stream-K iteration of CTA c: even split. (Measured: the warp
 // schedulers favour the older of two co-resident CTAs — the lower blockIdx
-// finishes first on every SM — but the pairing of CTAs on SMs is not fixed,
-// so weighting the split by blockIdx made the worst SM slower.)
+// finishes first on every SM, ~40 % earlier — but neither a blockIdx-weighted
+// split (the SM pairing is not fixed) nor dynamically grabbed fixed-boundary
+// slices (owner folds then wait on slices queued behind a CTA's current work)
+// beat the even static split; oversubscribing the grid only helps n >= 4096.)
 __device__ __forceinline__ int sk_begin(const StepParams& p, int c) {
   return (int)((long long)c * p.sk_iters / p.sk_ctas);
 }
@@ -601,11 +603,6 @@ cudaError_t cheb_step_rows_launch(const double2* h, long long ldh, bool conj_h, 
   if (vp == nullptr) return cudaErrorInvalidValue;
   const Variant& v = *vp;
   int grid = v.resident * kNumSMs;
-  static const int oversub = [] {
-    const char* e = getenv("CHFSI_K1_OVERSUB");  // tuning: CTAs per resident slot
-    return e ? atoi(e) : 1;
-  }();
-  if (oversub > 1) grid *= oversub;
   if (tiling.split > 0 && tiling.split < grid) grid = tiling.split;  // test/tuning override
   if (grid > ws.max_grid) return cudaErrorInvalidValue;
 

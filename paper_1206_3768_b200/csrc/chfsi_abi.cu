@@ -111,7 +111,7 @@ int chfsi_ctx_create(int device, chfsi_ctx** out) {
   CK_CUDA(cudaMalloc(&ctx->dinfo, 4 * sizeof(int)));
   CK_CUDA(cudaMalloc(&ctx->lstate, sizeof(LanczosState)));
   // K1 stream-K scratch: partial tiles and ready flags for every resident CTA
-  ctx->step_ws.max_grid = chfsi::kNumSMs * 8;
+  ctx->step_ws.max_grid = chfsi::kNumSMs * 4;
   CK_CUDA(cudaMalloc(&ctx->step_ws.partials,
                      chfsi::step_workspace_doubles(ctx->step_ws.max_grid) * sizeof(double)));
   CK_CUDA(cudaMalloc(&ctx->step_ws.flags, ctx->step_ws.max_grid * sizeof(unsigned)));
