@@ -99,6 +99,16 @@ CHFSI_API int chfsi_filter_z(chfsi_ctx* ctx, int n, int w, const void* H, long l
                    const void* y0, long long ldy0, void* buf_a, void* buf_b, long long ldb,
                    int deg, double a, double b, double scale_ref, void** result);
 
+/* Per-column degrees (SURVEY G4, config C5's adaptive filter): column j of
+ * the result is the degree-degs[j] filter of Y0[:, j]; degs is a HOST array,
+ * non-decreasing, each >= 1 (sort the columns first). One recurrence runs
+ * for all columns and retires each as its degree is reached, so the work is
+ * 8 n^2 sum(degs). Same buffers and aliasing rules as chfsi_filter_z. */
+CHFSI_API int chfsi_filter_degrees_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh,
+                                     int conj_h, const void* y0, long long ldy0, void* buf_a,
+                                     void* buf_b, long long ldb, const int* degs, double a, double b,
+                                     double scale_ref, void** result);
+
 /* Diagnostics: with CHFSI_K1_DEBUG=8 in the environment every K1 launch
  * records per-CTA [start, owner-wait begin, owner-wait end, end]
  * (%globaltimer ns) and the SM id; this copies the last launch's records
@@ -197,16 +207,23 @@ CHFSI_API int chfsi_back_transform_z(chfsi_ctx* ctx, int n, int nev, const void*
  * The caller sets up the start block (bufs[0], orthonormal), the window and
  * the workspace; the loop leaves its state and counters in the struct.
  * Optional host callbacks: `filter` replaces the single-GPU filter (the
- * row-sharded multi-GPU filter), `fill` draws replacement columns for a
- * rank-deficient panel (the caller's RNG, reference draw order). */
+ * row-sharded multi-GPU filter; `degs` is NULL or the sorted per-column
+ * degrees), `fill` draws replacement columns for a rank-deficient panel (the
+ * caller's RNG, reference draw order).
+ * adaptive != 0: per-vector degrees capped at deg, from the
+ * previous pass's Ritz values and residuals; the panel columns are reordered
+ * by ascending degree before each filter (oracle/chfsi_oracle.py restates
+ * the rule). */
 typedef int (*chfsi_filter_cb)(void* user, const void* panel, void* other, long long ld, int width,
-                               int deg, double a, double b, double scale_ref, void** result);
+                               int deg, const int* degs, double a, double b, double scale_ref,
+                               void** result);
 typedef int (*chfsi_fill_cb)(void* user, void* block, long long ld, int rows, const int* cols,
                              int ncols);
 
 typedef struct chfsi_loop {
   /* problem and device workspace (in) */
   int n, blk, nev, deg, max_repeats;
+  int adaptive, deg_min;     /* per-vector adaptive degree (deg = cap) */
   double tol;
   double rr_fast_tol;        /* > 0: near-diagonal RR eigensolver tried first (else zheevd only) */
   const void* H;
@@ -220,6 +237,7 @@ typedef struct chfsi_loop {
   void* coef;                /* nev x blk, ld nev */
   double* ritz_d;            /* device, blk */
   double* res_d;             /* device, blk */
+  int* perm_d;               /* device, blk ints (adaptive column order); may be NULL otherwise */
   chfsi_filter_cb filter;    /* NULL: chfsi_filter_z on this context */
   chfsi_fill_cb fill;        /* NULL: rank deficiency is an error */
   void* user;
@@ -233,8 +251,10 @@ typedef struct chfsi_loop {
   int* locked_per_loop;      /* max_repeats */
   double* ritz;              /* blk: the final pass's Ritz values */
   double* res;               /* blk: and residual norms */
+  int* degs;                 /* blk: the next pass's sorted per-column degrees (adaptive) */
   /* counters (SolveReport, chfsi.py:101-122) and device phase times */
   long long filtered_vectors, matvecs, residual_check_matvecs, filter_launches, rr_fast_eigs;
+  long long filter_degree_sum;  /* sum over passes and columns of the filter degree */
   double filter_flops;
   double t_filter, t_ortho, t_rr; /* seconds */
 } chfsi_loop;

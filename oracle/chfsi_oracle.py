@@ -98,6 +98,64 @@ def chebyshev_filter(h, y, deg, a, b, scale_ref):
     return cur
 
 
+# ------------------------------------------------- adaptive degree (G4) ---
+#
+# Config C5's "per-vector adaptive filter degree capped at 36" has no
+# reference implementation: this is the package's
+# own algorithm, restated here as its oracle (count parity against the
+# reference is unpinned for it). After each Rayleigh-Ritz pass, every
+# unlocked Ritz pair (lambda_i, r_i) gets the degree that damps its residual
+# to tol under the next window (a, b):
+#   t_i   = (lambda_i - c) / e,            c = (a+b)/2, e = (b-a)/2
+#   rho_i = |t_i| + sqrt(t_i^2 - 1)        (Chebyshev growth per degree)
+#   d_i   = ceil(log(r_i / tol) / log(rho_i)) + 2,  clamped to [d_min, d_max]
+# (r_i <= tol -> d_min; t_i >= -1 or a non-finite value -> d_max). The panel
+# columns are then reordered by ascending degree (stable) and each column is
+# filtered with its own degree (same scaled recurrence, stopped early).
+# Scalar math uses Python's `math` (the C library), exactly the operations
+# of the device loop (chfsi_loop.cu), so both compute identical degrees from
+# identical inputs.
+
+ADAPTIVE_MARGIN = 2  # measured at C1 (caps 24, 36): same loop counts as the fixed cap, 8-10 % fewer flops
+
+
+def adaptive_degree(lam, res, a, b, tol, d_min, d_max):
+    import math
+
+    if math.isnan(res) or math.isnan(lam):
+        return d_max
+    if not res > tol:
+        return d_min
+    c = (a + b) / 2
+    e = (b - a) / 2
+    t = (lam - c) / e
+    if not t < -1.0:
+        return d_max
+    rho = -t + math.sqrt(t * t - 1.0)
+    d = math.ceil(math.log(res / tol) / math.log(rho)) + ADAPTIVE_MARGIN
+    return int(min(max(d, d_min), d_max))
+
+
+def adaptive_order(degrees):
+    """Stable ascending order of the per-column degrees."""
+    return np.argsort(np.asarray(degrees), kind="stable")
+
+
+def chebyshev_filter_degrees(h, y, degrees, a, b, scale_ref):
+    """Per-column degrees: column j is the degree-``degrees[j]`` filter of
+    ``y[:, j]`` (the definition; the device runs one shared recurrence and
+    retires columns as their degree is reached)."""
+    y0 = np.asarray(y, dtype=np.complex128)
+    degrees = np.asarray(degrees, dtype=int)
+    if degrees.shape != (y0.shape[1],) or (degrees < 1).any():
+        raise ValueError("need one degree >= 1 per column")
+    out = np.empty_like(y0)
+    for d in np.unique(degrees):
+        cols = np.flatnonzero(degrees == d)
+        out[:, cols] = chebyshev_filter(h, y0[:, cols], int(d), a, b, scale_ref)
+    return out
+
+
 def chebyshev_response(lam, deg, a, b, scale_ref):
     """Scalar twin of the filter; restates chfsi.py:211-225."""
     x = np.asarray(lam, dtype=float)
@@ -202,12 +260,13 @@ class OracleReport:
     converged: bool = False
     operator_norm_estimate: float = 0.0
     filter_time: float = 0.0
+    filter_degree_sum: int = 0  # sum of per-column filter degrees (8 n^2 flops each)
     tail_vectors: np.ndarray | None = None
     lambda_blk_plus_1: float = float("nan")
 
 
 def chfsi_solve(h, nev, blk=None, deg=25, tol=1e-10, lanczos_steps=None, max_repeats=50,
-                guess=None, rng=None):
+                guess=None, rng=None, adaptive=False, d_min=2):
     """ChFSI with locking; restates chfsi.py:274-384.
 
     ``guess`` is ``(vectors n x blk, lambda1, lambda_blk_plus_1)`` or None.
@@ -215,7 +274,9 @@ def chfsi_solve(h, nev, blk=None, deg=25, tol=1e-10, lanczos_steps=None, max_rep
     ``report.tail_vectors`` is the full final block ``[locked | unlocked
     panel]`` (exactly ``blk`` columns at the break) and
     ``report.lambda_blk_plus_1`` the largest final Ritz value, which is what
-    the chained sequence driver hands to the next problem.
+    the chained sequence driver hands to the next problem. ``adaptive``:
+    per-vector degrees (G4, above) capped at ``deg``; the first pass uses
+    ``deg`` for every column.
     """
     t0 = time.perf_counter()
     rng = rng if isinstance(rng, np.random.Generator) else np.random.default_rng(rng)
@@ -242,14 +303,21 @@ def chfsi_solve(h, nev, blk=None, deg=25, tol=1e-10, lanczos_steps=None, max_rep
     vals, res_l = [], []
     locked = np.zeros((n, 0), dtype=np.complex128)
     ritz_vals = np.zeros(0)
+    degrees = None
     for _ in range(max_rep):
         rep.inner_loops += 1
         w = panel.shape[1]
         tf = time.perf_counter()
-        panel = chebyshev_filter(h, panel, deg, *win)
+        if degrees is None:
+            panel = chebyshev_filter(h, panel, deg, *win)
+            rep.matvecs += deg * w
+            rep.filter_degree_sum += deg * w
+        else:
+            panel = chebyshev_filter_degrees(h, panel, degrees, *win)
+            rep.matvecs += int(np.sum(degrees))
+            rep.filter_degree_sum += int(np.sum(degrees))
         rep.filter_time += time.perf_counter() - tf
         rep.filtered_vectors += w
-        rep.matvecs += deg * w
         panel = orthonormalize_panel(panel, locked, rng)
         hp = h @ panel
         rep.residual_check_matvecs += w
@@ -274,6 +342,12 @@ def chfsi_solve(h, nev, blk=None, deg=25, tol=1e-10, lanczos_steps=None, max_rep
             break
         panel = panel[:, nl:]
         win = safe_window(float(ritz_vals[nl]), float(ritz_vals[-1]), win[1])
+        if adaptive:
+            degrees = np.array([adaptive_degree(float(ritz_vals[i]), float(res[i]), win[0], win[1],
+                                                tol, d_min, deg) for i in range(nl, w)], dtype=int)
+            order = adaptive_order(degrees)
+            panel = panel[:, order]
+            degrees = degrees[order]
     else:
         rep.tail_vectors = np.hstack([locked, panel])
     rep.lambda_blk_plus_1 = float(ritz_vals[-1]) if ritz_vals.size else float("nan")
@@ -302,7 +376,7 @@ def back_transform(l, y):
 # --------------------------------------------------------- sequence driver ---
 
 def run_sequence(pencils, nev, nex, deg, tol=1e-10, seed=0, mode="chained",
-                 max_repeats=50):
+                 max_repeats=50, adaptive=False):
     """Solve a correlated sequence; restates harness.py:188-289 (parity mode).
 
     ``pencils`` yields ``(label, A, B)``. ``mode="harness"`` warm-starts from
@@ -322,7 +396,7 @@ def run_sequence(pencils, nev, nex, deg, tol=1e-10, seed=0, mode="chained",
         else:
             guess, rng = prev, np.random.default_rng((seed, label, 1))
         vals, vecs, rep = chfsi_solve(h, nev, blk, deg, tol, guess=guess, rng=rng,
-                                      max_repeats=max_repeats)
+                                      max_repeats=max_repeats, adaptive=adaptive)
         x = back_transform(l, vecs)
         wall = time.perf_counter() - t0
         if mode == "harness":
@@ -332,5 +406,5 @@ def run_sequence(pencils, nev, nex, deg, tol=1e-10, seed=0, mode="chained",
             prev = (rep.tail_vectors, float(vals[0]) if vals.size else float("nan"),
                     rep.lambda_blk_plus_1)
         out.append(dict(label=label, values=vals, vectors=vecs, x=x, report=rep, wall=wall,
-                        filter_flops=8.0 * h.shape[0] ** 2 * deg * rep.filtered_vectors))
+                        filter_flops=8.0 * h.shape[0] ** 2 * rep.filter_degree_sum))
     return out

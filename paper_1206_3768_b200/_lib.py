@@ -65,6 +65,8 @@ _SIGNATURES = {
     "chfsi_filter_coeffs": [_i, _d, _d, _d, _pd, _pd, _pd],
     "chfsi_filter_z": [_vp, _i, _i, _vp, _ll, _i, _vp, _ll, _vp, _vp, _ll, _i, _d, _d, _d,
                        ctypes.POINTER(_vp)],
+    "chfsi_filter_degrees_z": [_vp, _i, _i, _vp, _ll, _i, _vp, _ll, _vp, _vp, _ll, _pi, _d, _d, _d,
+                               ctypes.POINTER(_vp)],
     "chfsi_step_tiling": [_i, _i, _pi, _pi, _pi],
     "chfsi_debug_k1_trace": [ctypes.POINTER(ctypes.c_ulonglong), _i],
     "chfsi_lanczos_z": [_vp, _i, _i, _vp, _ll, _i, _vp, _vp, _pd, _pd, _pd, _pi],
@@ -85,7 +87,7 @@ _SIGNATURES = {
     "chfsi_back_transform_z": [_vp, _i, _i, _vp, _ll, _vp, _ll],
 }
 
-FILTER_CB = ctypes.CFUNCTYPE(_i, _vp, _vp, _vp, _ll, _i, _i, _d, _d, _d, ctypes.POINTER(_vp))
+FILTER_CB = ctypes.CFUNCTYPE(_i, _vp, _vp, _vp, _ll, _i, _i, _pi, _d, _d, _d, ctypes.POINTER(_vp))
 FILL_CB = ctypes.CFUNCTYPE(_i, _vp, _vp, _ll, _i, _pi, _i)
 
 
@@ -94,19 +96,20 @@ class LoopState(ctypes.Structure):
 
     _fields_ = [
         ("n", _i), ("blk", _i), ("nev", _i), ("deg", _i), ("max_repeats", _i),
+        ("adaptive", _i), ("deg_min", _i),
         ("tol", _d), ("rr_fast_tol", _d),
         ("H", _vp), ("ldh", _ll), ("conj_h", _i),
         ("bufs", _vp * 2), ("hp", _vp), ("hp_rot", _vp), ("locked", _vp), ("g", _vp),
-        ("coef", _vp), ("ritz_d", _vp), ("res_d", _vp),
+        ("coef", _vp), ("ritz_d", _vp), ("res_d", _vp), ("perm_d", _vp),
         ("filter", FILTER_CB), ("fill", FILL_CB), ("user", _vp),
         ("win_a", _d), ("win_b", _d), ("win_scale_ref", _d),
         ("inner_loops", _i), ("nlocked", _i), ("pb", _i), ("off", _i), ("width", _i),
         ("converged", _i),
         ("last_rot_pb", _i), ("last_width", _i), ("last_nlock", _i),
         ("locked_vals", _pd), ("locked_res", _pd), ("locked_per_loop", _pi),
-        ("ritz", _pd), ("res", _pd),
+        ("ritz", _pd), ("res", _pd), ("degs", _pi),
         ("filtered_vectors", _ll), ("matvecs", _ll), ("residual_check_matvecs", _ll),
-        ("filter_launches", _ll), ("rr_fast_eigs", _ll),
+        ("filter_launches", _ll), ("rr_fast_eigs", _ll), ("filter_degree_sum", _ll),
         ("filter_flops", _d),
         ("t_filter", _d), ("t_ortho", _d), ("t_rr", _d),
     ]

@@ -53,6 +53,10 @@ class ChfsiConfig:
 
     ``blk`` defaults to ``nev + 40``; ``nex`` (BASELINE.json's name for the
     extra vectors) is accepted as an alias: ``blk = nev + nex``.
+    ``adaptive_degree`` (additive, config C5 / SURVEY G4): per-vector filter
+    degrees capped at ``deg`` and floored at ``min_degree``, chosen after
+    every pass from each unlocked Ritz pair's residual (the rule is restated
+    in oracle/chfsi_oracle.py). Off by default: the reference's fixed degree.
     """
 
     nev: int
@@ -62,6 +66,8 @@ class ChfsiConfig:
     lanczos_steps: int | None = None
     max_repeats: int = 50
     nex: int | None = None
+    adaptive_degree: bool = False
+    min_degree: int = 2
 
     def __post_init__(self):
         if self.nex is not None:
@@ -77,6 +83,8 @@ class ChfsiConfig:
             raise ValueError(f"need 1 <= nev <= blk <= n, got nev={self.nev}, blk={blk}, n={n}")
         if self.deg < 1:
             raise ValueError("polynomial degree must be >= 1")
+        if self.adaptive_degree and not 1 <= self.min_degree <= self.deg:
+            raise ValueError("adaptive degree needs 1 <= min_degree <= deg")
         if self.tol <= 0:
             raise ValueError("tolerance must be positive")
         if self.lanczos_steps is not None:
@@ -142,6 +150,7 @@ class SolveReport:
     filter_flops: float = 0.0
     filter_launches: int = 0
     rr_fast_eigs: int = 0
+    filter_degree_sum: int = 0  # sum of per-column degrees (= deg * filtered_vectors unless adaptive)
     tail_vectors: object = None
     lambda_blk_plus_1: float = float("nan")
     host_phases: dict = field(default_factory=dict)  # wall seconds per host phase
@@ -239,16 +248,40 @@ def _filter_into(op, y, buf_a, buf_b, deg, window):
 def chebyshev_filter(h, y, deg, window):
     """Degree-``deg`` scaled Chebyshev filter of the block ``y``
     (chfsi.py:179-208) on the device; returns a new column-major device
-    block, ``y`` is untouched."""
-    if deg < 1:
-        raise ValueError("polynomial degree must be >= 1")
+    block, ``y`` is untouched. ``deg`` may also be a sequence of per-column
+    degrees (additive): column j is then filtered with degree
+    ``deg[j]``."""
     op = Operator.wrap(h)
     ym = to_fblock(y)
     if ym.shape[0] != op.n:
         raise ValueError(f"operator/block shapes do not conform: {(op.n, op.n)} vs {tuple(ym.shape)}")
     n, w = ym.shape
+    if np.ndim(deg) == 0:
+        if deg < 1:
+            raise ValueError("polynomial degree must be >= 1")
+        a, b = fblock(n, w), fblock(n, w)
+        return _filter_into(op, ym, a, b, int(deg), window)
+    degs = np.asarray(deg, dtype=np.int64)
+    if degs.shape != (w,) or (degs < 1).any():
+        raise ValueError("need one polynomial degree >= 1 per column")
+    order = np.argsort(degs, kind="stable")
+    ident = bool((order == np.arange(w)).all())
+    ys = ym if ident else ym.index_select(1, torch.from_numpy(order).to(ym.device))
+    ys = to_fblock(ys)
     a, b = fblock(n, w), fblock(n, w)
-    return _filter_into(op, ym, a, b, deg, window)
+    sd = np.ascontiguousarray(degs[order], dtype=np.int32)
+    res = ctypes.c_void_p()
+    check(lib().chfsi_filter_degrees_z(ctx(), n, w, dptr(op.tensor), op.ld, op.conj, dptr(ys),
+                                       ld_of(ys), dptr(a), dptr(b), ld_of(a),
+                                       sd.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                       float(window.a), float(window.b), float(window.scale_ref),
+                                       ctypes.byref(res)), "chebyshev_filter")
+    out = a if res.value == a.data_ptr() else b
+    if ident:
+        return out
+    inv = np.empty(w, dtype=np.int64)
+    inv[order] = np.arange(w)
+    return to_fblock(out.index_select(1, torch.from_numpy(inv).to(out.device)))
 
 
 def chebyshev_response(lam, deg, window):
@@ -353,9 +386,10 @@ class _LoopCallbacks:
             self.error = exc
             return -1
 
-    def _filter(self, user, panel, other, ld, width, deg, a, b, scale_ref, result):
+    def _filter(self, user, panel, other, ld, width, deg, degs, a, b, scale_ref, result):
         try:
-            out = self.sharded.apply(self._view(panel, width), deg,
+            d = [degs[j] for j in range(width)] if degs else deg
+            out = self.sharded.apply(self._view(panel, width), d,
                                      FilterWindow(a=a, b=b, scale_ref=scale_ref),
                                      out=self._view(other, width))
             result[0] = out.data_ptr()
@@ -388,7 +422,8 @@ def _workspace(dev, n, blk, nev):
             [fblock(n, blk, dev), fblock(n, blk, dev)], fblock(n, blk, dev), fblock(n, blk, dev),
             fblock(n, max(nev, 1), dev), fblock(blk, blk, dev), fblock(max(nev, 1), blk, dev),
             torch.empty(blk, dtype=torch.float64, device=dev),
-            torch.empty(blk, dtype=torch.float64, device=dev))
+            torch.empty(blk, dtype=torch.float64, device=dev),
+            torch.empty(blk, dtype=torch.int32, device=dev))
     return ws
 
 
@@ -434,7 +469,8 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
         chunks = shard if isinstance(shard, int) and not isinstance(shard, bool) else 2
         sharded = RowShardedFilter(op, n, group=group, chunks=chunks)
 
-    bufs, hp_buf, hp_rot, locked, g_buf, coef, ritz_d, res_d = _workspace(dev, n, blk, cfg.nev)
+    bufs, hp_buf, hp_rot, locked, g_buf, coef, ritz_d, res_d, perm_d = _workspace(dev, n, blk,
+                                                                                 cfg.nev)
 
     hw = {"setup": time.perf_counter() - t0}
     t_lz.start()
@@ -473,7 +509,8 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     st.bufs[0], st.bufs[1] = bufs[0].data_ptr(), bufs[1].data_ptr()
     st.hp, st.hp_rot, st.locked = hp_buf.data_ptr(), hp_rot.data_ptr(), locked.data_ptr()
     st.g, st.coef = g_buf.data_ptr(), coef.data_ptr()
-    st.ritz_d, st.res_d = ritz_d.data_ptr(), res_d.data_ptr()
+    st.ritz_d, st.res_d, st.perm_d = ritz_d.data_ptr(), res_d.data_ptr(), perm_d.data_ptr()
+    st.adaptive, st.deg_min = int(cfg.adaptive_degree), int(cfg.min_degree)
     st.win_a, st.win_b, st.win_scale_ref = window.a, window.b, window.scale_ref
     st.pb, st.off, st.width = 0, 0, blk
     host_f = np.zeros((4, blk))
@@ -483,6 +520,8 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     st.locked_res = host_f[1].ctypes.data_as(pd_)
     st.ritz = host_f[2].ctypes.data_as(pd_)
     st.res = host_f[3].ctypes.data_as(pd_)
+    host_degs = np.zeros(blk, dtype=np.int32)
+    st.degs = host_degs.ctypes.data_as(pi_)
     st.locked_per_loop = locked_per_loop.ctypes.data_as(pi_)
     callbacks = _LoopCallbacks(bufs, n, rng, sharded)
     st.fill = callbacks.fill_cb
@@ -502,6 +541,7 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     report.residual_check_matvecs = int(st.residual_check_matvecs)
     report.filter_launches = int(st.filter_launches)
     report.filter_flops = float(st.filter_flops)
+    report.filter_degree_sum = int(st.filter_degree_sum)
     report.rr_fast_eigs = int(st.rr_fast_eigs)
     report.converged = bool(st.converged)
     report.locked_per_loop = [int(x) for x in locked_per_loop[: st.inner_loops]]

@@ -205,6 +205,66 @@ int chfsi_cheb_step_rows_z(chfsi_ctx* ctx, int n, int rows, int w, const void* H
   return CHFSI_OK;
 }
 
+int chfsi_filter_degrees_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, int conj_h,
+                           const void* y0, long long ldy0, void* buf_a, void* buf_b, long long ldb,
+                           const int* degs, double a, double b, double scale_ref, void** result) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(n >= 0 && w >= 0, "negative size");
+  CK_ARG(result, "result is NULL");
+  CK_ARG(buf_a != buf_b && y0 != buf_a, "buffers must be distinct (y0 may equal buf_b)");
+  CK_ARG(w == 0 || degs, "degs is NULL");
+  for (int j = 0; j < w; ++j)
+    CK_ARG(degs[j] >= 1 && (j == 0 || degs[j] >= degs[j - 1]),
+           "per-column degrees must be >= 1 and non-decreasing");
+  if (w == 0) {
+    *result = buf_a;
+    return CHFSI_OK;
+  }
+  const int dmax = degs[w - 1];
+  std::vector<double> al(dmax), be(dmax);
+  double c = 0.0;
+  CK(chfsi_filter_coeffs(dmax, a, b, scale_ref, &c, al.data(), be.data()));
+  *result = (dmax % 2) ? buf_a : buf_b;
+  if (n == 0) return CHFSI_OK;
+  // One recurrence for all columns (the step coefficients do not depend on
+  // the final degree); step j only runs the columns whose degree exceeds j,
+  // a suffix [first, w) because degrees are sorted.
+  const double2* hh = static_cast<const double2*>(H);
+  const double2* prev = nullptr;
+  long long ldp = 0;
+  const double2* cur = static_cast<const double2*>(y0);
+  long long ldcur = ldy0;
+  int first = 0;
+  for (int j = 0; j < dmax; ++j) {
+    while (first < w && degs[first] <= j) ++first;
+    double2* dst = static_cast<double2*>((j % 2 == 0) ? buf_a : buf_b);
+    const int wa = w - first;
+    const chfsi::StepTiling tiling = ctx->tiling.bm ? ctx->tiling : chfsi::choose_step_tiling(n, wa);
+    CK_CUDA(chfsi::cheb_step_launch(hh, ldh, conj_h != 0, cur + first * ldcur, ldcur,
+                                    prev ? prev + first * ldp : nullptr, ldp, dst + first * ldb, ldb,
+                                    n, wa, al[j], c, be[j], tiling, ctx->step_ws, ctx->stream));
+    prev = cur;
+    ldp = ldcur;
+    cur = dst;
+    ldcur = ldb;
+  }
+  // a column of degree d ended in the buffer of step d-1 (buf_a when d is
+  // odd): move the groups whose parity differs from dmax's into *result
+  double2* res = static_cast<double2*>(*result);
+  for (int j0 = 0; j0 < w;) {
+    int j1 = j0;
+    while (j1 < w && (degs[j1] % 2) == (degs[j0] % 2)) ++j1;
+    if ((degs[j0] % 2) != (dmax % 2)) {
+      const double2* src = static_cast<const double2*>((degs[j0] % 2) ? buf_a : buf_b);
+      CK_CUDA(cudaMemcpy2DAsync(res + j0 * ldb, ldb * sizeof(double2), src + j0 * ldb,
+                                ldb * sizeof(double2), (size_t)n * sizeof(double2), j1 - j0,
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    j0 = j1;
+  }
+  return CHFSI_OK;
+}
+
 int chfsi_filter_coeffs(int deg, double a, double b, double scale_ref, double* c, double* alphas,
                         double* betas) {
   CK_ARG(deg >= 1, "polynomial degree must be >= 1");

@@ -13,6 +13,7 @@
 // traffic is the blk Ritz values and residuals the locking test needs (one
 // stream synchronisation per pass, plus the near-diagonal eigensolver's
 // regime checks). Device phase times are taken with events on the stream.
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -32,6 +33,22 @@ void safe_window(double scale_ref, double a, double b, double* out_a, double* ou
   if (!(scale_ref < a && a < b)) a = scale_ref + 0.5 * (b - scale_ref);
   *out_a = a;
   *out_b = b;
+}
+
+// Per-vector degree (oracle/chfsi_oracle.py adaptive_degree
+// restates it with the same C-library operations): damp the residual r of a
+// Ritz pair at lambda to tol under the window (a, b).
+constexpr int kAdaptiveMargin = 2;  // oracle ADAPTIVE_MARGIN
+int adaptive_degree(double lam, double r, double a, double b, double tol, int d_min, int d_max) {
+  if (std::isnan(r) || std::isnan(lam)) return d_max;
+  if (!(r > tol)) return d_min;
+  const double c = (a + b) / 2, e = (b - a) / 2;
+  const double t = (lam - c) / e;
+  if (!(t < -1.0)) return d_max;
+  const double rho = -t + std::sqrt(t * t - 1.0);
+  const double d = std::ceil(std::log(r / tol) / std::log(rho)) + kAdaptiveMargin;
+  if (!(d < (double)d_max)) return d_max;  // also catches inf / nan
+  return d < (double)d_min ? d_min : (int)d;
 }
 
 double2* col(void* base, long long ld, int j) { return static_cast<double2*>(base) + (long long)j * ld; }
@@ -101,7 +118,12 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
   cudaStream_t s = ctx->stream;
   cudaEvent_t* ev = ctx->loop_ev;
   const int n = L->n;
-  CK(chfsi::ensure_pinned(ctx, 2 * (size_t)L->blk * sizeof(double)));
+  CK_ARG(!L->adaptive || (L->degs && L->perm_d && 1 <= L->deg_min && L->deg_min <= L->deg),
+         "adaptive degree needs degs, perm_d and 1 <= deg_min <= deg");
+  // pinned staging: [ritz | res] readback, then the adaptive column order
+  CK(chfsi::ensure_pinned(ctx, 2 * (size_t)L->blk * sizeof(double) + (size_t)L->blk * sizeof(int)));
+  bool have_degs = false;
+  std::vector<int> dtmp, order;
 
   while (L->inner_loops < L->max_repeats) {
     L->inner_loops += 1;
@@ -112,19 +134,29 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
     // ---- filter (chfsi.py:331-334)
     CK_CUDA(cudaEventRecord(ev[0], s));
     void* result = nullptr;
+    const int* degs = have_degs ? L->degs : nullptr;  // adaptive: sorted per-column degrees
     if (L->filter) {
-      if (L->filter(L->user, panel, other, n, width, L->deg, L->win_a, L->win_b, L->win_scale_ref,
-                    &result) != 0 || !result)
+      if (L->filter(L->user, panel, other, n, width, L->deg, degs, L->win_a, L->win_b,
+                    L->win_scale_ref, &result) != 0 || !result)
         return fail(CHFSI_EINVAL, "filter callback failed");
+    } else if (degs) {
+      CK(chfsi_filter_degrees_z(ctx, n, width, L->H, L->ldh, L->conj_h, panel, n, other, panel, n,
+                                degs, L->win_a, L->win_b, L->win_scale_ref, &result));
     } else {
       CK(chfsi_filter_z(ctx, n, width, L->H, L->ldh, L->conj_h, panel, n, other, panel, n, L->deg,
                         L->win_a, L->win_b, L->win_scale_ref, &result));
     }
     CK_CUDA(cudaEventRecord(ev[1], s));
-    L->filter_launches += L->deg;
+    long long dsum = (long long)L->deg * width;
+    if (degs) {
+      dsum = 0;
+      for (int j = 0; j < width; ++j) dsum += degs[j];
+    }
+    L->filter_launches += degs ? degs[width - 1] : L->deg;
     L->filtered_vectors += width;
-    L->matvecs += (long long)L->deg * width;
-    L->filter_flops += 8.0 * (double)n * (double)n * (double)L->deg * (double)width;
+    L->matvecs += dsum;
+    L->filter_degree_sum += dsum;
+    L->filter_flops += 8.0 * (double)n * (double)n * (double)dsum;
     const bool q_in_other = result == other;
 
     // ---- orthonormalize (chfsi.py:335-336)
@@ -186,6 +218,35 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
     L->width = width - n_lock;
     L->win_scale_ref = ritz[n_lock];
     safe_window(ritz[n_lock], ritz[width - 1], L->win_b, &L->win_a, &L->win_b);
+
+    // ---- adaptive: per-vector degrees for the next panel, columns sorted
+    // by ascending degree (stable), gathered into the other buffer
+    if (L->adaptive) {
+      const int wn = L->width;
+      dtmp.resize(wn);
+      order.resize(wn);
+      for (int i = 0; i < wn; ++i) {
+        dtmp[i] = adaptive_degree(ritz[n_lock + i], res[n_lock + i], L->win_a, L->win_b, L->tol,
+                                  L->deg_min, L->deg);
+        order[i] = i;
+      }
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return dtmp[x] < dtmp[y]; });
+      bool ident = true;
+      for (int i = 0; i < wn; ++i) {
+        L->degs[i] = dtmp[order[i]];
+        ident = ident && order[i] == i;
+      }
+      if (!ident) {
+        int* hperm = reinterpret_cast<int*>(static_cast<double*>(ctx->pinned) + 2 * (size_t)L->blk);
+        for (int i = 0; i < wn; ++i) hperm[i] = order[i];
+        CK_CUDA(cudaMemcpyAsync(L->perm_d, hperm, (size_t)wn * sizeof(int), cudaMemcpyHostToDevice, s));
+        CK_CUDA(chfsi::nd_gather_cols_launch(col(L->bufs[L->pb], n, L->off), n, n, wn, L->perm_d,
+                                             static_cast<double2*>(L->bufs[1 - L->pb]), n, s));
+        L->pb = 1 - L->pb;
+        L->off = 0;
+      }
+      have_degs = true;
+    }
   }
   return CHFSI_OK;
 }

@@ -139,36 +139,53 @@ class RowShardedFilter:
 
     def apply(self, y, deg, window, out=None):
         """Filter the full block y (n x w, replicated on all ranks); returns
-        the full filtered block (replicated), column-major."""
+        the full filtered block (replicated), column-major. ``deg`` is one
+        degree, or non-decreasing per-column degrees (adaptive mode): the
+        columns then form groups of equal degree that leave the shared
+        recurrence as their degree is reached."""
         part = self.part
         n, w = y.shape
         if n != part.n:
             raise ValueError("operator/block shapes do not conform")
-        c, al, be = filter_coeffs(deg, float(window.a), float(window.b), float(window.scale_ref))
         dev = y.device
-        nchunks = 1 if part.world == 1 else min(self.chunks, w)  # nothing to overlap alone
-        edges = np.linspace(0, w, nchunks + 1).astype(int)
-        groups = [(int(edges[k]), int(edges[k + 1])) for k in range(len(edges) - 1)
-                  if edges[k + 1] > edges[k]]
+        if np.ndim(deg) == 0:
+            dmax = int(deg)
+            nchunks = 1 if part.world == 1 else min(self.chunks, w)  # nothing to overlap alone
+            edges = np.linspace(0, w, nchunks + 1).astype(int)
+            groups = [(int(edges[k]), int(edges[k + 1]), dmax) for k in range(len(edges) - 1)
+                      if edges[k + 1] > edges[k]]
+        else:
+            degs = [int(d) for d in deg]
+            if len(degs) != w or min(degs) < 1 or any(b < a for a, b in zip(degs, degs[1:])):
+                raise ValueError("per-column degrees must be >= 1 and non-decreasing")
+            dmax = degs[-1]
+            groups, j0 = [], 0
+            for j in range(1, w + 1):
+                if j == w or degs[j] != degs[j0]:
+                    groups.append((j0, j, degs[j0]))
+                    j0 = j
+        c, al, be = filter_coeffs(dmax, float(window.a), float(window.b), float(window.scale_ref))
         bufs = [[to_blocked(part, y[:, j0:j1], blocked_empty(part, j1 - j0, dev)),
-                 blocked_empty(part, j1 - j0, dev)] for j0, j1 in groups]
+                 blocked_empty(part, j1 - j0, dev)] for j0, j1, _ in groups]
         pending = [None] * len(groups)
-        cur = 0
-        for j in range(deg):
-            nxt = 1 - cur
-            for g, (j0, j1) in enumerate(groups):
+        cur = [0] * len(groups)
+        for j in range(dmax):
+            for g, (j0, j1, dg) in enumerate(groups):
+                if j >= dg:
+                    continue  # this group reached its degree
                 if pending[g] is not None:
                     pending[g].wait()  # step j of group g needs its step j-1 all-gather
                     pending[g] = None
+                nxt = 1 - cur[g]
                 yprev = bufs[g][nxt][part.rank] if j > 0 else None
-                self.step(bufs[g][cur], yprev, bufs[g][nxt][part.rank], j1 - j0, al[j], c, be[j])
+                self.step(bufs[g][cur[g]], yprev, bufs[g][nxt][part.rank], j1 - j0, al[j], c, be[j])
                 pending[g] = self.allgather(bufs[g][nxt], async_op=True)
-            cur = nxt
+                cur[g] = nxt
         for h in pending:
             if h is not None:
                 h.wait()
         if out is None:
             out = torch.empty((w, n), dtype=y.dtype, device=dev).t()
-        for g, (j0, j1) in enumerate(groups):
-            from_blocked(part, bufs[g][cur], out[:, j0:j1])
+        for g, (j0, j1, _) in enumerate(groups):
+            from_blocked(part, bufs[g][cur[g]], out[:, j0:j1])
         return out

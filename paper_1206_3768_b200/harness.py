@@ -201,4 +201,5 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
 
 def default_config(cfg):
     """ChfsiConfig for a BASELINE config (sequence.BaselineConfig)."""
-    return ChfsiConfig(nev=cfg.nev, nex=cfg.nex, deg=cfg.deg, tol=cfg.tol)
+    return ChfsiConfig(nev=cfg.nev, nex=cfg.nex, deg=cfg.deg, tol=cfg.tol,
+                       adaptive_degree=cfg.adaptive_degree)

@@ -61,13 +61,17 @@ def _worker(rank, world, port, n, w, deg, chunks, q):
         flt.step = _cpu_step(ht, flt.part)
         win = type("W", (), dict(a=-1.0, b=float(np.linalg.eigvalsh(h)[-1]) + 0.1, scale_ref=-2.5))
         out = flt.apply(yt, deg, win).numpy()
-        ref = orc.chebyshev_filter(h, y, deg, win.a, win.b, win.scale_ref)
+        if np.ndim(deg) == 0:
+            ref = orc.chebyshev_filter(h, y, deg, win.a, win.b, win.scale_ref)
+        else:  # per-column (adaptive) degrees, non-decreasing
+            ref = orc.chebyshev_filter_degrees(h, y, deg, win.a, win.b, win.scale_ref)
         q.put((rank, float(np.abs(out - ref).max() / np.abs(ref).max())))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,w,deg,chunks", [(64, 8, 5, 1), (101, 13, 7, 2), (150, 9, 4, 3)])
+@pytest.mark.parametrize("n,w,deg,chunks", [(64, 8, 5, 1), (101, 13, 7, 2), (150, 9, 4, 3),
+                                            (90, 7, [1, 2, 2, 3, 5, 5, 6], 2)])
 def test_row_sharded_filter_world2_matches_oracle(n, w, deg, chunks):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

@@ -159,6 +159,41 @@ def test_filter_input_untouched_and_column_major_operator(pkg):
         assert np.abs(out.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
+@pytest.mark.parametrize("n,w,degs,conj", [
+    (257, 9, [3, 1, 4, 1, 5, 9, 2, 6, 5], False),      # unsorted: the API sorts and restores
+    (512, 40, list(range(1, 41)), True),              # one column retires per step
+    (1000, 97, [7] * 50 + [12] * 47, False),          # two groups, parities differ
+    (300, 5, [4, 4, 4, 4, 4], False)])                # uniform == the fixed-degree filter
+def test_filter_per_column_degrees(pkg, n, w, degs, conj):
+    """Adaptive-degree filter: column j equals the degree-degs[j]
+    filter of y[:, j] (oracle: chebyshev_filter_degrees)."""
+    rng = np.random.default_rng(n + w)
+    h = random_hermitian(rng, n)
+    y = rng.standard_normal((n, w)) + 1j * rng.standard_normal((n, w))
+    ev = np.linalg.eigvalsh(h)
+    a, b, s = float(ev[n // 3]), float(ev[-1]) + 0.1, float(ev[0])
+    hd = torch.from_numpy(h).cuda()
+    if conj:
+        hd = hd.t().contiguous().t()
+    out = pkg.chebyshev_filter(hd, fb(y), degs, pkg.FilterWindow(a=a, b=b, scale_ref=s)).cpu().numpy()
+    ref = orc.chebyshev_filter_degrees(h, y, degs, a, b, s)
+    for j in range(w):  # per column: the degrees differ in scale by orders of magnitude
+        assert np.abs(out[:, j] - ref[:, j]).max() <= 1e-12 * np.abs(ref[:, j]).max(), j
+    if len(set(degs)) == 1:
+        fixed = pkg.chebyshev_filter(hd, fb(y), degs[0], pkg.FilterWindow(a=a, b=b, scale_ref=s))
+        assert np.abs(fixed.cpu().numpy() - out).max() <= 1e-13 * np.abs(out).max()
+
+
+def test_filter_per_column_degrees_rejects_bad_input(pkg):
+    h = torch.eye(16, dtype=torch.complex128, device="cuda")
+    y = fb(np.ones((16, 3), dtype=complex))
+    win = pkg.FilterWindow(a=0.5, b=2.0, scale_ref=-1.0)
+    with pytest.raises(ValueError):
+        pkg.chebyshev_filter(h, y, [1, 0, 2], win)
+    with pytest.raises(ValueError):
+        pkg.chebyshev_filter(h, y, [1, 2], win)
+
+
 @pytest.mark.parametrize("name", sorted(LANCZOS_CASES))
 def test_lanczos_matches_reference_golden(pkg, small_golden, name):
     from paper_1206_3768_b200.chfsi import _lanczos_estimates

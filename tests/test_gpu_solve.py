@@ -165,6 +165,32 @@ def test_c1_chained_sequence_matches_oracle(pkg):
         assert np.isfinite(x).all()
 
 
+@pytest.mark.parametrize("cap", [12, 36])
+def test_c1_adaptive_degree_sequence_matches_oracle(pkg, cap):
+    """Adaptive per-vector degree (config C5's mode) on the C1
+    sequence: the device loop vs the oracle restatement of the same rule
+    (no reference oracle exists for this mode, so counts are pinned to the
+    restatement: loops within +/-1, filter work within one pass's worth)."""
+    cfg_b = pkg.BASELINE_CONFIGS["C1"]
+    cfg = pkg.ChfsiConfig(nev=cfg_b.nev, nex=cfg_b.nex, deg=cap, tol=cfg_b.tol,
+                          adaptive_degree=True)
+    seq = list(pkg.iter_baseline_sequence(cfg_b.n, 4, seed=0))
+    ref = orc.run_sequence(seq, cfg_b.nev, cfg_b.nex, cap, cfg_b.tol, seed=0, mode="chained",
+                           adaptive=True)
+    got = pkg.solve_sequence(seq, cfg, seed=0, mode="chained", keep_standard=True)
+    blk = cfg_b.nev + cfg_b.nex
+    for r, g in zip(ref, got):
+        rr, gr = r["report"], g.report
+        assert gr.converged
+        assert gr.final_residuals.max() <= cfg_b.tol
+        assert abs(gr.inner_loops - rr.inner_loops) <= 1
+        assert abs(gr.filter_degree_sum - rr.filter_degree_sum) <= cap * blk
+        assert np.abs(g.values - r["values"]).max() <= 1e-9 * np.abs(r["values"]).max()
+        assert subspace_sines(r["vectors"], g.standard_vectors.cpu().numpy()).max() <= 1e-6
+        assert gr.filter_flops == 8.0 * cfg_b.n ** 2 * gr.filter_degree_sum
+        assert gr.matvecs == gr.filter_degree_sum + gr.lanczos_matvecs + gr.residual_check_matvecs
+
+
 @pytest.mark.slow
 def test_c2_harness_protocol_matches_reference(pkg, c2_golden):
     """BASELINE config 2 (n=2048, N=10): counts and eigenvalues of every

@@ -119,3 +119,52 @@ def test_c1_generator_bytes_and_harness_protocol(c1_golden):
             np.testing.assert_allclose(vals, c1_golden[pre + "values"], rtol=0, atol=1e-12)
             assert subspace_sines(c1_golden[pre + "vectors"], vecs).max() <= 1e-9
         prev = (dvec[:, : cfg.blk], float(dv[0]), float(dv[cfg.blk]))
+
+
+# ------------------------------------------------ adaptive degree (G4) ---
+# No reference oracle exists for the adaptive mode: these pin the
+# restatement's own invariants.
+
+def test_adaptive_degree_rule():
+    a, b, tol = 1.0, 9.0, 1e-10
+    # converged -> floor; at/above the window edge -> cap; NaN -> cap
+    assert orc.adaptive_degree(0.0, 1e-11, a, b, tol, 2, 36) == 2
+    assert orc.adaptive_degree(a, 1e-3, a, b, tol, 2, 36) == 36
+    assert orc.adaptive_degree(float("nan"), 1e-3, a, b, tol, 2, 36) == 36
+    # t = (lam - c)/e = -1.5 -> rho = 1.5 + sqrt(1.25); r/tol = 1e4
+    lam = 5.0 - 1.5 * 4.0
+    import math
+    d = math.ceil(math.log(1e4) / math.log(1.5 + math.sqrt(1.25))) + orc.ADAPTIVE_MARGIN
+    assert orc.adaptive_degree(lam, 1e-6, a, b, tol, 2, 36) == d
+    # monotone: a larger residual never asks for a lower degree
+    ds = [orc.adaptive_degree(lam, r, a, b, tol, 2, 36) for r in (1e-9, 1e-7, 1e-5, 1e-3)]
+    assert ds == sorted(ds)
+
+
+def test_per_column_filter_is_the_definition():
+    rng = np.random.default_rng(5)
+    n, w = 40, 6
+    g = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    h = (g + g.conj().T) / 2
+    y = rng.standard_normal((n, w)) + 1j * rng.standard_normal((n, w))
+    degs = [3, 1, 4, 1, 5, 2]
+    out = orc.chebyshev_filter_degrees(h, y, degs, -1.0, 12.0, -3.0)
+    for j, d in enumerate(degs):
+        ref = orc.chebyshev_filter(h, y[:, j:j + 1], d, -1.0, 12.0, -3.0)
+        # (BLAS may round a 1-column product differently from a 2-column one)
+        assert np.abs(out[:, j:j + 1] - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_adaptive_solve_converges_with_fewer_flops_than_the_cap():
+    """C1 shape: the adaptive mode reaches tol on every pair and spends
+    less filter work than running every column at the cap."""
+    from paper_1206_3768_b200.sequence import iter_baseline_sequence
+
+    seq = list(iter_baseline_sequence(512, 3, seed=0))
+    fixed = orc.run_sequence(seq, 32, 16, 24, adaptive=False)
+    adapt = orc.run_sequence(seq, 32, 16, 24, adaptive=True)
+    for f, a in zip(fixed, adapt):
+        assert a["report"].converged
+        assert a["report"].final_residuals.max() < 1e-10
+        assert np.abs(a["values"] - f["values"]).max() <= 1e-9 * np.abs(f["values"]).max()
+    assert sum(a["filter_flops"] for a in adapt) < sum(f["filter_flops"] for f in fixed)
