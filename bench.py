@@ -57,6 +57,9 @@ def parse_args():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--mode", choices=["chained", "harness"], default="chained")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gen", choices=["host", "device"], default="host",
+                    help="BASELINE generator: host numpy, or host draws + device algebra "
+                         "(same distribution and draw order; the CPU sample gets the same bytes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=2, help="problems in the CPU sample")
     ap.add_argument("--no-clocks", action="store_true", help="diagnostics: no clock sampler")
@@ -152,6 +155,26 @@ def host_sequence(cfg_b, limit=None):
     return out
 
 
+class _HostView:
+    """Lazy host (numpy) view of a device-generated sequence: the CPU sample
+    and the e2e path copy only the problems they use."""
+
+    def __init__(self, dseq):
+        self.dseq = dseq
+
+    def __len__(self):
+        return len(self.dseq)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        lab, a, b = self.dseq[i]
+        return lab, a.cpu().numpy(), b.cpu().numpy()
+
+    def __iter__(self):
+        return (self[i] for i in range(len(self)))
+
+
 # --------------------------------------------------------------- CPU arm ---
 
 def cpu_sample(seq, cfg_b, mode="chained"):
@@ -172,7 +195,17 @@ def run_reference(args):
     from paper_1206_3768_b200.sequence import BASELINE_CONFIGS
 
     cfg_b = BASELINE_CONFIGS[args.config]
-    seq = host_sequence(cfg_b, limit=args.cpu_sample)
+    if args.gen == "device":  # the same bytes the GPU arm solves
+        from paper_1206_3768_b200.sequence import iter_baseline_sequence
+
+        it = iter_baseline_sequence(cfg_b.n, cfg_b.length, seed=0, device="cuda:0")
+        seq = []
+        for lab, a, b in it:
+            seq.append((lab, a.cpu().numpy(), b.cpu().numpy()))
+            if len(seq) >= args.cpu_sample:
+                break
+    else:
+        seq = host_sequence(cfg_b, limit=args.cpu_sample)
     for _ in range(args.warmup):
         cpu_sample(seq[:1], cfg_b)
     times, flops = [], 0.0
@@ -225,7 +258,14 @@ def run_ours(args):
 
     cfg_b = pkg.BASELINE_CONFIGS[args.config]
     cfg = default_config(cfg_b)
-    seq = host_sequence(cfg_b)
+    if args.gen == "device":
+        from paper_1206_3768_b200.sequence import iter_baseline_sequence
+
+        dseq = list(iter_baseline_sequence(cfg_b.n, cfg_b.length, seed=0, device=dev))
+        seq = _HostView(dseq)
+    else:
+        dseq = None
+        seq = host_sequence(cfg_b)
     n = cfg_b.n
 
     def barrier():
@@ -241,8 +281,11 @@ def run_ours(args):
         return float(t.item())
 
     # resident inputs (HBM) for `value`
-    dev_pencils = [pkg.EigenPencil(a=torch.from_numpy(a).to(dev), b=torch.from_numpy(b).to(dev),
-                                   label=lab) for lab, a, b in seq]
+    if dseq is not None:
+        dev_pencils = [pkg.EigenPencil(a=a, b=b, label=lab) for lab, a, b in dseq]
+    else:
+        dev_pencils = [pkg.EigenPencil(a=torch.from_numpy(a).to(dev), b=torch.from_numpy(b).to(dev),
+                                       label=lab) for lab, a, b in seq]
 
     shard = True if args.shard else None
 

@@ -20,6 +20,14 @@ so the CPU oracle and the device path see the SAME bytes:
 
 Problems are yielded lazily (``iter_baseline_sequence``) so that n=20000
 sequences never hold more than one (A, B) pair plus the running sums.
+
+``device=...`` keeps the host to what fixes the bytes'
+distribution — the numpy Generator draws, in the same order — and does the
+O(n^3) part on the GPU through libchfsi (ZGEMM for C C^H and U diag(d) U^H,
+the positive-diagonal QR for the Haar U) plus the O(n^2) symmetrize /
+rescale steps, yielding device tensors. Results equal the host generator's
+to rounding (tests/test_gpu_io.py), and C5's generation drops from tens of
+minutes of host LAPACK to the time of its random draws.
 """
 
 from __future__ import annotations
@@ -88,14 +96,18 @@ def hermitian_unit_frobenius(rng, n):
     return e
 
 
-def iter_baseline_sequence(n, length, seed=0):
+def iter_baseline_sequence(n, length, seed=0, device=None):
     """Yield ``(label, A_l, B_l)`` for l = 1..length (complex128, C-ordered).
 
     The yielded arrays are fresh copies; the generator keeps its own running
-    ``A``/``B``.
+    ``A``/``B``. With ``device`` (e.g. ``"cuda:0"``) they are row-major CUDA
+    tensors computed on the GPU from the same host draws.
     """
     if n < 2 or length < 1:
         raise ValueError("need n >= 2 and length >= 1")
+    if device is not None:
+        yield from _device_sequence(n, length, seed, device)
+        return
     rng = np.random.default_rng(seed)
     c = complex_gaussian(rng, n, n)
     b = c @ c.conj().T
@@ -122,6 +134,63 @@ def iter_baseline_sequence(n, length, seed=0):
         b += (eps / 10.0) * f
         del e, f
         yield ell + 1, a.copy(), b.copy()
+
+
+def _device_sequence(n, length, seed, device):
+    import torch
+
+    from ._device import C128, fblock
+    from ._lib import check, ctx, dptr, lib
+    from .linalg import qr_orthonormalize_inplace
+
+    dev = torch.device(device)
+
+    def upload_gaussian():
+        z = complex_gaussian(rng, n, n)
+        return torch.from_numpy(z).pin_memory().to(dev, non_blocking=True)  # row-major
+
+    def gemm_nc(x, y, alpha):  # alpha * x y^H for column-major n x n blocks
+        out = fblock(n, n, dev)
+        check(lib().chfsi_gemm_z(ctx(), b"N", b"C", n, n, n, alpha, 0.0, dptr(x), n, dptr(y), n,
+                                 0.0, 0.0, dptr(out), n), "generator gemm")
+        return out
+
+    def symmetrize(m):  # column-major in place
+        check(lib().chfsi_symmetrize_z(ctx(), n, dptr(m), n), "generator symmetrize")
+        return m
+
+    def herm_unit_frobenius():
+        g = upload_gaussian()
+        e = (g + g.conj().t()) * 0.5
+        del g
+        return e * (float(np.sqrt(n)) / torch.linalg.vector_norm(e).item())
+
+    def colmajor(t):  # column-major copy of a (logical) n x n tensor
+        return t.t().contiguous().t()
+
+    rng = np.random.default_rng(seed)
+    with torch.cuda.device(dev):
+        c = colmajor(upload_gaussian())
+        b = gemm_nc(c, c, 1.0 / (4.0 * n))        # C C^H / (4n)
+        del c
+        b.diagonal().add_(1.0)
+        symmetrize(b)
+        u = colmajor(upload_gaussian())
+        qr_orthonormalize_inplace(u)              # Q diag(conj(r_ii/|r_ii|)): positive-real R
+        d = torch.from_numpy(-1.0 + 11.0 * (np.arange(n, dtype=np.float64) / n) ** 1.5).to(dev)
+        a = symmetrize(gemm_nc(u * d.to(C128)[None, :], u, 1.0))  # U diag(d) U^H
+        del u
+        a = a.contiguous()                        # row-major, like the host generator
+        b = b.contiguous()
+        yield 1, a.clone(), b.clone()
+        for ell in range(1, length):
+            eps = 1e-2 * 0.5**ell
+            e = herm_unit_frobenius()
+            f = herm_unit_frobenius()
+            a.add_(e, alpha=eps)
+            b.add_(f, alpha=eps / 10.0)
+            del e, f
+            yield ell + 1, a.clone(), b.clone()
 
 
 def generate_baseline_sequence(n, length, seed=0):
