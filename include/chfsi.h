@@ -62,6 +62,9 @@ CHFSI_API int chfsi_ctx_set_stream(chfsi_ctx* ctx, void* cuda_stream);
  * SM), plus 32x32 | 32x64, grid = number of persistent CTAs (0 = all resident CTAs;
  * fewer CTAs exercise other stream-K splits). bm = 0 restores automatic. */
 CHFSI_API int chfsi_ctx_set_tiling(chfsi_ctx* ctx, int bm, int bn, int grid);
+/* With a forced tiling: groups = 2 selects the one-CTA-per-SM K1 whose two
+ * 8-warp groups take alternate k-slabs of the same tile (64x16, 64x32). */
+CHFSI_API int chfsi_ctx_set_step_groups(chfsi_ctx* ctx, int groups);
 
 /* ---------------------------------------------------------------- K1 ---
  * One fused Chebyshev step (chfsi.py:203 / chfsi.py:206):

@@ -168,12 +168,18 @@ __device__ __forceinline__ void epilogue_store(const StepParams& p, int row, int
   p.ynext[(long long)col * p.ldn + row] = make_double2(tr, ti);
 }
 
-template <int BM, int BN, int WM, int WN, int STAGES, int MINB, bool CONJ>
-__global__ void __launch_bounds__(WM* WN * 32, MINB)
+// GROUPS = 2: one CTA per SM holds two 8-warp groups on the SAME tile that
+// take alternate k-slabs (each group its own TMA producer and half of the
+// stage ring) and add their partial tiles in fixed order at every segment
+// end — 16 warps per SM without the priority imbalance of two co-resident
+// CTAs (the older CTA's warps win the schedulers; measured ~40 % earlier).
+template <int BM, int BN, int WM, int WN, int STAGES, int MINB, bool CONJ, int GROUPS>
+__global__ void __launch_bounds__(GROUPS* WM* WN * 32, MINB)
     cheb_step_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const StepParams p) {
-  constexpr int NWARPS = WM * WN;
-  constexpr int THREADS = NWARPS * 32;
+  constexpr int NWARPS = WM * WN;          // warps per group (one tile's worth)
+  constexpr int THREADS = NWARPS * 32;     // threads per group
+  static_assert(GROUPS == 1 || (GROUPS == 2 && STAGES % 2 == 0), "two groups need an even ring");
   constexpr int TM = BM / WM, TN = BN / WN;
   constexpr int MI = TM / 8, NI = TN / 8;
   constexpr int ACC = MI * NI * 4;
@@ -191,9 +197,17 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
   const unsigned smem0 = smem_u32(smem);
   const unsigned full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lane = threadIdx.x & 31;
+  const int group = GROUPS == 1 ? 0 : (int)threadIdx.x / THREADS;
+  const int tid = (int)threadIdx.x - group * THREADS;  // thread index within the group
+  const int warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp / WN, wn = warp % WN;
+  // group-local barrier (named barrier 2 for group 0 when two groups run)
+  auto gsync = [&]() {
+    if (GROUPS == 1) __syncthreads();
+    else asm volatile("bar.sync 2, %0;\n" ::"n"(THREADS) : "memory");
+  };
   const int G = gridDim.x;
   const int cta = (p.dbg & 16) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x;  // 16: reversed (diagnostic)
   const int kiters = p.kiters;
@@ -278,23 +292,26 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
     }
   };
 
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, NWARPS);
+      mbar_init(empty0 + 8 * s, NWARPS);  // one arrival per warp of the consuming group
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
-  Cursor lc;  // producer cursor (thread 0)
+  // producer cursor (the group's thread 0): the group's iterations are
+  // j = group, group + GROUPS, ... and stage j % STAGES is always its own
+  Cursor lc;
   start(lc);
+  for (int k = 0; k < group; ++k) advance(lc);
   if (tid == 0) {
-    for (int s = 0; s < STAGES && lc.j < total; ++s) {
+    for (int s = group; s < STAGES && lc.j < total; s += GROUPS) {
       issue(lc, s);
-      advance(lc);
+      for (int k = 0; k < GROUPS; ++k) advance(lc);
     }
   }
 
@@ -326,79 +343,110 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
   const int off_even = ((g & 1) << 6) | lo, off_odd = (((g & 1) ^ 1) << 6) | lo;
   const unsigned char* a_base = smem + (wm * TM + sg) * HALF;
   const unsigned char* b_base = smem + 2 * A_BYTES + (wn * TN + sg) * HALF;
+  // two groups: hand-over buffer for group 1's partial tile
+  double* cbuf = reinterpret_cast<double*>(bars + 2 * STAGES);
 
   Cursor cc;
   start(cc);
-  int stage = 0;
-  unsigned phase = 0;
   for (int j = 0; j < total; ++j) {
-    mbar_wait(full0 + 8 * stage, phase);
-    // mma.sync.aligned needs the whole warp converged: lane 0 of warp 0 may
-    // still be issuing TMA (prologue) or spinning on an empty barrier
-    __syncwarp();
-    const unsigned char* sa = a_base + stage * STAGE_BYTES;
-    const unsigned char* sbm = b_base + stage * STAGE_BYTES;
+    const int stage = j % STAGES;
+    const unsigned phase = (unsigned)(j / STAGES) & 1u;
+    if (GROUPS == 1 || (j % GROUPS) == group) {
+      mbar_wait(full0 + 8 * stage, phase);
+      // mma.sync.aligned needs the whole warp converged: lane 0 of warp 0 may
+      // still be issuing TMA (prologue) or spinning on an empty barrier
+      __syncwarp();
+      const unsigned char* sa = a_base + stage * STAGE_BYTES;
+      const unsigned char* sbm = b_base + stage * STAGE_BYTES;
 #pragma unroll
-    for (int k4 = 0; k4 < BK / 4; ++k4) {
-      const int off = (k4 & 1) ? off_odd : off_even;
-      const unsigned char* ah = sa + (k4 >> 1) * A_BYTES + off;
-      const unsigned char* bh = sbm + (k4 >> 1) * B_BYTES + off;
-      double2 a[MI], b[NI];
+      for (int k4 = 0; k4 < BK / 4; ++k4) {
+        const int off = (k4 & 1) ? off_odd : off_even;
+        const unsigned char* ah = sa + (k4 >> 1) * A_BYTES + off;
+        const unsigned char* bh = sbm + (k4 >> 1) * B_BYTES + off;
+        double2 a[MI], b[NI];
 #pragma unroll
-      for (int i = 0; i < MI; ++i) a[i] = lds128(ah + i * 8 * HALF);
+        for (int i = 0; i < MI; ++i) a[i] = lds128(ah + i * 8 * HALF);
 #pragma unroll
-      for (int jj = 0; jj < NI; ++jj) b[jj] = lds128(bh + jj * 8 * HALF);
-      // Re/Im of (a or conj(a)) * b: four real DMMAs per complex 8x8x4 block
+        for (int jj = 0; jj < NI; ++jj) b[jj] = lds128(bh + jj * 8 * HALF);
+        // Re/Im of (a or conj(a)) * b: four real DMMAs per complex 8x8x4 block
 #pragma unroll
-      for (int i = 0; i < MI; ++i)
+        for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int jj = 0; jj < NI; ++jj) {
-          double(&cr)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][0]);
-          double(&ci)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][2]);
-          dmma884(cr, a[i].x, b[jj].x);
-          dmma884(ci, a[i].x, b[jj].y);
-        }
+          for (int jj = 0; jj < NI; ++jj) {
+            double(&cr)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][0]);
+            double(&ci)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][2]);
+            dmma884(cr, a[i].x, b[jj].x);
+            dmma884(ci, a[i].x, b[jj].y);
+          }
 #pragma unroll
-      for (int i = 0; i < MI; ++i) {
-        const double ai = a[i].y, nai = -a[i].y;
+        for (int i = 0; i < MI; ++i) {
+          const double ai = a[i].y, nai = -a[i].y;
 #pragma unroll
-        for (int jj = 0; jj < NI; ++jj) {
-          double(&cr)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][0]);
-          double(&ci)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][2]);
-          dmma884(cr, CONJ ? ai : nai, b[jj].y);
-          dmma884(ci, CONJ ? nai : ai, b[jj].x);
+          for (int jj = 0; jj < NI; ++jj) {
+            double(&cr)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][0]);
+            double(&ci)[2] = *reinterpret_cast<double(*)[2]>(&acc[i][jj][2]);
+            dmma884(cr, CONJ ? ai : nai, b[jj].y);
+            dmma884(ci, CONJ ? nai : ai, b[jj].x);
+          }
         }
       }
-    }
-    // Release the stage; the elected thread refills it once every warp has.
-    // The fragments were read through the generic proxy (LDS) and the refill
-    // is an async-proxy (TMA) write of the same bytes: the proxy fence makes
-    // the reads complete before the release (without it ptxas schedules the
-    // arrive ahead of the last LDS and a slow warp can read refilled data).
-    // (Measured alternative: the last-arriving warp refills via a shared
-    // counter — no empty-barrier wait, but ~3 % slower at 2 CTAs/SM.)
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty0 + 8 * stage);
-    if (p.dbg & 1) __syncthreads();
-    if (tid == 0 && lc.j < total) {
-      mbar_wait(empty0 + 8 * stage, phase);
-      issue(lc, stage);
-      advance(lc);
-    }
-    // warp 0 must reconverge before its next mma.sync.aligned (lane 0 may
-    // have spun on the empty barrier while lanes 1-31 ran ahead)
-    __syncwarp();
-    if (++stage == STAGES) {
-      stage = 0;
-      phase ^= 1u;
+      // Release the stage; the group's elected thread refills it once every
+      // warp of the group has. The fragments were read through the generic
+      // proxy (LDS) and the refill is an async-proxy (TMA) write of the same
+      // bytes: the proxy fence makes the reads complete before the release
+      // (without it ptxas schedules the arrive ahead of the last LDS and a
+      // slow warp can read refilled data). (Measured alternative: the
+      // last-arriving warp refills via a shared counter — no empty-barrier
+      // wait, but ~3 % slower at 2 CTAs/SM.)
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * stage);
+      if (tid == 0 && lc.j < total) {
+        mbar_wait(empty0 + 8 * stage, phase);
+        issue(lc, stage);
+        for (int k = 0; k < GROUPS; ++k) advance(lc);
+      }
+      // warp 0 must reconverge before its next mma.sync.aligned (lane 0 may
+      // have spun on the empty barrier while lanes 1-31 ran ahead)
+      __syncwarp();
     }
 
     // ---- end of a tile segment?
     const bool tile_end = cc.kk == kiters - 1;
     const bool pub_end = pub > 0 && j == pub - 1;
     if (tile_end || pub_end) {
-      if (p.dbg & 4) __syncthreads();
+      if (GROUPS == 2) {
+        // group 1 hands its partial tile to group 0 (fixed order: group 0's
+        // own slabs first, then group 1's)
+        double* cb = cbuf + tid;
+        if (group == 1) {
+#pragma unroll
+          for (int i = 0; i < MI; ++i)
+#pragma unroll
+            for (int jj = 0; jj < NI; ++jj)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                cb[((i * NI + jj) * 4 + e) * THREADS] = acc[i][jj][e];
+                acc[i][jj][e] = 0.0;
+              }
+        }
+        asm volatile("bar.sync 1, %0;\n" ::"n"(2 * THREADS) : "memory");
+        if (group == 0) {
+#pragma unroll
+          for (int i = 0; i < MI; ++i)
+#pragma unroll
+            for (int jj = 0; jj < NI; ++jj)
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                acc[i][jj][e] = dadd(acc[i][jj][e], cb[((i * NI + jj) * 4 + e) * THREADS]);
+        }
+        // group 1 may refill the buffer only after group 0 has read it
+        asm volatile("bar.sync 3, %0;\n" ::"n"(2 * THREADS) : "memory");
+        if (group == 1) {
+          advance(cc);
+          continue;  // group 0 finishes the segment
+        }
+      }
       if (pub_end) {
         // non-owner: publish the partial head of this CTA's last tile
         double* dst = p.partials + (size_t)cta * ACC * THREADS + tid;
@@ -409,7 +457,7 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
 #pragma unroll
             for (int e = 0; e < 4; ++e) __stcg(dst + ((i * NI + jj) * 4 + e) * THREADS, acc[i][jj][e]);
         __threadfence();
-        __syncthreads();
+        gsync();
         if (tid == 0) st_release(p.flags + cta, p.epoch);
       } else if (j < pub + dp_iters) {
         epilogue(cc);
@@ -427,7 +475,7 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
               while (ld_acquire(p.flags + q) != p.epoch) __nanosleep(64);
             if (tr) p.trace[cta * 5 + 2] = gtimer();
           }
-          __syncthreads();
+          gsync();
           // fixed fold order: own partial, then peers first..cta-1
           for (int q = first; q < cta; ++q) {
             const double* src = p.partials + (size_t)q * ACC * THREADS + tid;
@@ -508,19 +556,22 @@ bool encode_map_blocked(CUtensorMap* map, const void* base, long long len, long 
 
 struct Variant {
   const void* fn;
-  int bm, bn, threads, smem;
+  int bm, bn, groups, threads, smem;
   int resident;  // CTAs per SM actually achievable
 };
 
-template <int BM, int BN, int WM, int WN, int STAGES, int MINB, bool CONJ>
+template <int BM, int BN, int WM, int WN, int STAGES, int MINB, bool CONJ, int GROUPS>
 Variant make_variant() {
   Variant v{};
-  auto fn = cheb_step_kernel<BM, BN, WM, WN, STAGES, MINB, CONJ>;
+  auto fn = cheb_step_kernel<BM, BN, WM, WN, STAGES, MINB, CONJ, GROUPS>;
   v.fn = reinterpret_cast<const void*>(fn);
   v.bm = BM;
   v.bn = BN;
-  v.threads = WM * WN * 32;
-  v.smem = STAGES * 2 * (BM + BN) * HALF + 2 * STAGES * 8 + 1024;
+  v.groups = GROUPS;
+  v.threads = GROUPS * WM * WN * 32;
+  constexpr int ACC = (BM / WM / 8) * (BN / WN / 8) * 4;
+  v.smem = STAGES * 2 * (BM + BN) * HALF + 2 * STAGES * 8 + 1024 +
+           (GROUPS == 2 ? ACC * WM * WN * 32 * 8 : 0);  // + group hand-over buffer
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem);
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, v.threads, v.smem);
@@ -528,22 +579,25 @@ Variant make_variant() {
   return v;
 }
 
-// (bm, bn) -> kernel configuration. Function-local statics: built once, on
-// first use (the caller has set the device).
-const Variant* variant(int bm, int bn, bool conj) {
-#define CHFSI_V(BM_, BN_, WM_, WN_, ST_, MB_)                                     \
-  if (bm == BM_ && bn == BN_) {                                                   \
-    static const Variant a = make_variant<BM_, BN_, WM_, WN_, ST_, MB_, false>(); \
-    static const Variant b = make_variant<BM_, BN_, WM_, WN_, ST_, MB_, true>();  \
-    return conj ? &b : &a;                                                        \
+// (bm, bn, groups) -> kernel configuration. Function-local statics: built
+// once, on first use (the caller has set the device).
+const Variant* variant(int bm, int bn, int groups, bool conj) {
+#define CHFSI_V(BM_, BN_, WM_, WN_, ST_, MB_, GR_)                                        \
+  if (bm == BM_ && bn == BN_ && groups == GR_) {                                          \
+    static const Variant a = make_variant<BM_, BN_, WM_, WN_, ST_, MB_, false, GR_>();    \
+    static const Variant b = make_variant<BM_, BN_, WM_, WN_, ST_, MB_, true, GR_>();     \
+    return conj ? &b : &a;                                                                \
   }
-  CHFSI_V(64, 16, 8, 1, 4, 2)
-  CHFSI_V(64, 32, 4, 2, 4, 2)
-  CHFSI_V(64, 64, 4, 2, 3, 2)
-  CHFSI_V(32, 32, 2, 2, 4, 3)
-  CHFSI_V(32, 64, 2, 2, 3, 3)
-  CHFSI_V(128, 32, 8, 2, 5, 1)
-  CHFSI_V(128, 16, 8, 1, 6, 1)
+  CHFSI_V(64, 16, 8, 1, 4, 2, 1)
+  CHFSI_V(64, 32, 4, 2, 4, 2, 1)
+  CHFSI_V(64, 64, 4, 2, 3, 2, 1)
+  CHFSI_V(32, 32, 2, 2, 4, 3, 1)
+  CHFSI_V(32, 64, 2, 2, 3, 3, 1)
+  CHFSI_V(128, 32, 8, 2, 5, 1, 1)
+  CHFSI_V(128, 16, 8, 1, 6, 1, 1)
+  // two 8-warp groups per CTA, one CTA per SM (alternate k-slabs)
+  CHFSI_V(64, 16, 8, 1, 10, 1, 2)
+  CHFSI_V(64, 32, 4, 2, 8, 1, 2)
 #undef CHFSI_V
   return nullptr;
 }
@@ -551,19 +605,20 @@ const Variant* variant(int bm, int bn, bool conj) {
 }  // namespace
 
 StepTiling choose_step_tiling(int n, int w) {
-  // Measured on B200 (profiles/r01_k1_tiling.log, TFLOP/s per (n, w)):
+  // Measured on B200 (profiles/r01_k1_tiling.log, r01_k1_dual.log, TFLOP/s):
   //  * padding dominates at small w: 64x16 (8 warps x 8x16) runs at ~0.9x the
   //    speed of 64x32 per padded column, so it wins when it pads >10 % less;
-  //  * n <= 4096: 64x32 otherwise (two CTAs per SM);
-  //  * large n: the 16-warp 128x32 CTA (one per SM, B tile reused by twice the
-  //    rows) reaches 33-35 TF/s (94 % of the DMMA peak at C4); 64x64 is
-  //    slightly ahead at n ~ 5000 when it pads no more than 64x32.
+  //  * n <= 3000: 64x32 with two CTAs per SM (29.3 at C2's 2048x160);
+  //  * larger n: the two-group 64x32 CTA (one per SM, alternate k-slabs;
+  //    no co-resident-CTA imbalance) gains 3-5 % (4096x160: 32.2 vs 30.7);
+  //    the 16-warp 128x32 CTA is level with it once n >= 8000 or w >= 400
+  //    (34.9 TFLOP/s = 94 % of the DMMA peak at C4).
   if (w <= 16) return StepTiling{64, 16, 0};
-  const int pad16 = ((w + 15) / 16) * 16, pad32 = ((w + 31) / 32) * 32, pad64 = ((w + 63) / 64) * 64;
+  const int pad16 = ((w + 15) / 16) * 16, pad32 = ((w + 31) / 32) * 32;
   if (pad16 * 10 < pad32 * 9) return StepTiling{64, 16, 0};
-  if (n <= 4096) return StepTiling{64, 32, 0};
+  if (n <= 3000) return StepTiling{64, 32, 0};
   if (n >= 8000 || w >= 400) return StepTiling{128, 32, 0};
-  return pad64 <= pad32 ? StepTiling{64, 64, 0} : StepTiling{64, 32, 0};
+  return StepTiling{64, 32, 0, 2};
 }
 
 int step_trace_copy(unsigned long long* host, int max_ctas) {
@@ -578,7 +633,7 @@ int step_trace_copy(unsigned long long* host, int max_ctas) {
 size_t step_workspace_doubles(int max_grid) { return (size_t)max_grid * kSlotDoubles; }
 
 int step_grid_size(int bn, bool conj) {
-  const Variant* v = variant(64, bn, conj);
+  const Variant* v = variant(64, bn, 1, conj);
   return v ? v->resident * kNumSMs : 0;
 }
 
@@ -599,7 +654,7 @@ cudaError_t cheb_step_rows_launch(const double2* h, long long ldh, bool conj_h, 
   const int m = shard.rows;
   if (n <= 0 || w <= 0 || m <= 0) return cudaSuccess;
   if (tiling.bm == 0) tiling = choose_step_tiling(n, w);
-  const Variant* vp = variant(tiling.bm, tiling.bn, conj_h);
+  const Variant* vp = variant(tiling.bm, tiling.bn, tiling.groups ? tiling.groups : 1, conj_h);
   if (vp == nullptr) return cudaErrorInvalidValue;
   const Variant& v = *vp;
   int grid = v.resident * kNumSMs;

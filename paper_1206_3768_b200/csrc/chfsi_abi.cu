@@ -157,6 +157,16 @@ int chfsi_ctx_set_tiling(chfsi_ctx* ctx, int bm, int bn, int split) {
   return CHFSI_OK;
 }
 
+int chfsi_ctx_set_step_groups(chfsi_ctx* ctx, int groups) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(groups == 1 || groups == 2, "groups must be 1 or 2");
+  CK_ARG(ctx->tiling.bm != 0, "set a tiling first (chfsi_ctx_set_tiling)");
+  CK_ARG(groups == 1 || (ctx->tiling.bm == 64 && (ctx->tiling.bn == 16 || ctx->tiling.bn == 32)),
+         "two-group K1 exists for 64x16 and 64x32");
+  ctx->tiling.groups = groups;
+  return CHFSI_OK;
+}
+
 int chfsi_ctx_set_stream(chfsi_ctx* ctx, void* stream) {
   CK_ARG(ctx, "ctx is NULL");
   ctx->stream = static_cast<cudaStream_t>(stream);

@@ -15,6 +15,7 @@ struct StepTiling {
   int bm;     // 0 = choose automatically; 32, 64 or 128 rows per CTA tile
   int bn;     // 16, 32 or 64 columns per CTA tile
   int split;  // grid override for tests/tuning (0 = all resident CTAs)
+  int groups = 1;  // 1: one 8/16-warp tile group per CTA; 2: two 8-warp groups splitting k
 };
 
 // Stream-K scratch owned by the context: partial tiles + ready flags.

@@ -47,9 +47,11 @@ def _lib():
     return _lib
 
 
-def set_tiling(bm, bn, split):
+def set_tiling(bm, bn, split, groups=1):
     L = _lib()
     L.check(L.lib().chfsi_ctx_set_tiling(L.ctx(), bm, bn, split))
+    if bm and groups != 1:
+        L.check(L.lib().chfsi_ctx_set_step_groups(L.ctx(), groups))
 
 
 def cheb_step(h_dev, conj, ycur, yprev, ynext, alpha, c, beta):
@@ -73,7 +75,8 @@ def fb(x):
 # (bm, bn, grid): grid 0 = every resident CTA; small grids force other
 # data-parallel / stream-K splits and multi-peer fix-ups
 TILINGS = [(64, 64, 0), (64, 32, 0), (64, 16, 0), (64, 64, 1), (64, 32, 7), (64, 16, 13),
-           (64, 64, 150), (64, 32, 296), (128, 32, 0), (128, 32, 5), (128, 16, 0), (128, 16, 77)]
+           (64, 64, 150), (64, 32, 296), (128, 32, 0), (128, 32, 5), (128, 16, 0), (128, 16, 77),
+           (64, 32, 0, 2), (64, 32, 9, 2), (64, 16, 0, 2), (64, 16, 31, 2)]
 
 
 @pytest.mark.parametrize("tiling", TILINGS)
@@ -114,10 +117,11 @@ def test_cheb_step_plain_product_and_determinism(pkg):
     assert torch.equal(o1, o2)  # bitwise run-to-run
 
 
-@pytest.mark.parametrize("n,w,grid,bm", [(2048, 160, 0, 64), (2048, 131, 0, 64), (2048, 97, 0, 64),
-                                         (1500, 40, 37, 64), (700, 33, 0, 64), (4096, 160, 0, 64),
-                                         (2048, 160, 0, 128), (3000, 70, 0, 128)])
-def test_cheb_step_bitwise_repeatable(pkg, n, w, grid, bm):
+@pytest.mark.parametrize("n,w,grid,bm,groups", [
+    (2048, 160, 0, 64, 1), (2048, 131, 0, 64, 1), (2048, 97, 0, 64, 1), (1500, 40, 37, 64, 1),
+    (700, 33, 0, 64, 1), (4096, 160, 0, 64, 1), (2048, 160, 0, 128, 1), (3000, 70, 0, 128, 1),
+    (2048, 160, 0, 64, 2), (1500, 40, 37, 64, 2), (3000, 131, 0, 64, 2)])
+def test_cheb_step_bitwise_repeatable(pkg, n, w, grid, bm, groups):
     """Stream-K fix-ups, TMA/mbarrier pipeline and warp convergence: 40
     back-to-back filters must agree bit for bit. (This caught two real
     races: divergent lanes entering mma.sync.aligned, and the missing
@@ -126,7 +130,7 @@ def test_cheb_step_bitwise_repeatable(pkg, n, w, grid, bm):
     h = torch.from_numpy(random_hermitian(rng, n)).cuda()
     y = fb(rng.standard_normal((n, w)) + 1j * rng.standard_normal((n, w)))
     win = pkg.FilterWindow(a=-1.0, b=1.5, scale_ref=-1.6)
-    set_tiling(bm, 32, grid)
+    set_tiling(bm, 32, grid, groups)
     try:
         outs = [pkg.chebyshev_filter(h, y, 4, win) for _ in range(40)]
     finally:

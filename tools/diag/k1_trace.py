@@ -23,6 +23,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=4096)
 ap.add_argument("--w", type=int, default=160)
 ap.add_argument("--bn", type=int, default=0)
+ap.add_argument("--groups", type=int, default=1)
 a = ap.parse_args()
 assert int(os.environ.get("CHFSI_K1_DEBUG", "0")) & 8, "run with CHFSI_K1_DEBUG=8"
 g = torch.randn(a.n, a.n, dtype=torch.complex128, device="cuda")
@@ -32,6 +33,8 @@ y.copy_(torch.randn(a.n, a.w, dtype=torch.complex128, device="cuda"))
 x = fblock(a.n, a.w)
 if a.bn:
     _lib.check(_lib.lib().chfsi_ctx_set_tiling(_lib.ctx(), 64, a.bn, 0))
+    if a.groups != 1:
+        _lib.check(_lib.lib().chfsi_ctx_set_step_groups(_lib.ctx(), a.groups))
 win = pkg.FilterWindow(a=-5.0, b=60.0, scale_ref=-70.0)
 for _ in range(3):
     _filter_into(op, y, x, y, 1, win)

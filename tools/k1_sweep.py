@@ -70,8 +70,11 @@ for n, w in shapes:
         if v == "auto":
             _lib.check(_lib.lib().chfsi_ctx_set_tiling(_lib.ctx(), 0, 0, 0))
         else:
-            bm, bn = (int(t) for t in v.split("x"))
+            dual = v.endswith("d")  # "64x32d": two 8-warp groups per CTA
+            bm, bn = (int(t) for t in v.rstrip("d").split("x"))
             _lib.check(_lib.lib().chfsi_ctx_set_tiling(_lib.ctx(), bm, bn, 0))
+            if dual:
+                _lib.check(_lib.lib().chfsi_ctx_set_step_groups(_lib.ctx(), 2))
         ms = timed(lambda: _filter_into(op, y, x, y, deg, win), reps) / deg
         fl = 8.0 * n * n * w
         print(json.dumps({"n": n, "w": w, "variant": v, "k1_us": round(ms * 1e3, 2),
