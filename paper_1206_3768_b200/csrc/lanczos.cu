@@ -20,7 +20,7 @@ namespace chfsi {
 
 namespace {
 
-constexpr int LZ_THREADS = 256;
+constexpr int LZ_THREADS = 512;
 constexpr int LZ_WARPS = LZ_THREADS / 32;
 
 struct LanczosParams {
@@ -73,6 +73,7 @@ __device__ double grid_total(const double* part, int G, double* sh) {
 template <bool CONJ>
 __global__ void __launch_bounds__(LZ_THREADS) lanczos_coop_kernel(const LanczosParams p) {
   __shared__ double sh[LZ_WARPS + 1];
+  __shared__ double2 red[LZ_THREADS];  // (row, j-group) partials of r -= V coef
   cg::grid_group grid = cg::this_grid();
   const int G = gridDim.x, b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -104,22 +105,23 @@ __global__ void __launch_bounds__(LZ_THREADS) lanczos_coop_kernel(const LanczosP
       const double2* hr = p.h + (long long)row * p.ldh;
       double sr = 0.0, si = 0.0;
       int c = lane;
-      for (; c + 96 < n; c += 128) {
-        const double2 a0 = hr[c], a1 = hr[c + 32], a2 = hr[c + 64], a3 = hr[c + 96];
-        const double2 b0 = q[c], b1 = q[c + 32], b2 = q[c + 64], b3 = q[c + 96];
-        const double sg = CONJ ? -1.0 : 1.0;
-        sr = fma(a0.x, b0.x, fma(-sg * a0.y, b0.y, sr));
-        si = fma(a0.x, b0.y, fma(sg * a0.y, b0.x, si));
-        sr = fma(a1.x, b1.x, fma(-sg * a1.y, b1.y, sr));
-        si = fma(a1.x, b1.y, fma(sg * a1.y, b1.x, si));
-        sr = fma(a2.x, b2.x, fma(-sg * a2.y, b2.y, sr));
-        si = fma(a2.x, b2.y, fma(sg * a2.y, b2.x, si));
-        sr = fma(a3.x, b3.x, fma(-sg * a3.y, b3.y, sr));
-        si = fma(a3.x, b3.y, fma(sg * a3.y, b3.x, si));
+      const double sg = CONJ ? -1.0 : 1.0;
+      // 8 independent 16-byte loads of H per lane in flight (HBM-bound GEMV:
+      // the bytes in flight per SM set the bandwidth)
+      for (; c + 224 < n; c += 256) {
+        double2 a[8], bq[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = __ldcs(hr + c + 32 * u);  // streamed once per step
+#pragma unroll
+        for (int u = 0; u < 8; ++u) bq[u] = q[c + 32 * u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          sr = fma(a[u].x, bq[u].x, fma(-sg * a[u].y, bq[u].y, sr));
+          si = fma(a[u].x, bq[u].y, fma(sg * a[u].y, bq[u].x, si));
+        }
       }
       for (; c < n; c += 32) {
         const double2 a = hr[c], bb = q[c];
-        const double sg = CONJ ? -1.0 : 1.0;
         sr = fma(a.x, bb.x, fma(-sg * a.y, bb.y, sr));
         si = fma(a.x, bb.y, fma(sg * a.y, bb.x, si));
       }
@@ -150,18 +152,17 @@ __global__ void __launch_bounds__(LZ_THREADS) lanczos_coop_kernel(const LanczosP
       p.r[i] = make_double2(rr, ri);
     }
     __syncthreads();
-    // ---- reorthogonalisation partials: cpart[b][j] = V[own rows, j]^H r
-    for (int j = warp; j <= it; j += LZ_WARPS) {
+    // ---- reorthogonalisation partials: cpart[b][j] = V[own rows, j]^H r,
+    // one thread per column j (each reads its column's contiguous row range)
+    for (int j = tid; j <= it; j += LZ_THREADS) {
       const double2* vj = p.V + (long long)j * n;
       double cr = 0.0, ci = 0.0;
-      for (int i = r0 + lane; i < r1; i += 32) {
+      for (int i = r0; i < r1; ++i) {
         const double2 a = vj[i], rv = p.r[i];
         cr = fma(a.x, rv.x, fma(a.y, rv.y, cr));
         ci = fma(a.x, rv.y, fma(-a.y, rv.x, ci));
       }
-      cr = warp_sum(cr);
-      ci = warp_sum(ci);
-      if (lane == 0) p.cpart[(long long)b * p.k + j] = make_double2(cr, ci);
+      p.cpart[(long long)b * p.k + j] = make_double2(cr, ci);
     }
     grid.sync();  // (2) partials complete
 
@@ -179,19 +180,53 @@ __global__ void __launch_bounds__(LZ_THREADS) lanczos_coop_kernel(const LanczosP
     }
     grid.sync();  // (3) coefficients complete
 
-    // ---- r -= V coef (fixed j order), beta partial
+    // ---- r -= V coef, beta partial. Threads split as (row, j-group): RP
+    // rows x JG groups, each group summing a strided subset of the columns;
+    // the JG partial sums are combined in group order (deterministic).
     double bp = 0.0;
-    for (int i = r0 + tid; i < r1; i += LZ_THREADS) {
+    const int rows = r1 - r0;
+    if (rows <= LZ_THREADS) {
+      int rp = 1;
+      while (rp < rows) rp <<= 1;
+      const int jg = LZ_THREADS / rp;
+      const int ri = tid % rp, gi = tid / rp;
       double sr = 0.0, si = 0.0;
-      for (int j = 0; j <= it; ++j) {
-        const double2 a = p.V[(long long)j * n + i], c = __ldcg(p.coef + j);
-        sr = fma(a.x, c.x, fma(-a.y, c.y, sr));
-        si = fma(a.x, c.y, fma(a.y, c.x, si));
+      if (ri < rows) {
+        const int i = r0 + ri;
+        for (int j = gi; j <= it; j += jg) {
+          const double2 a = p.V[(long long)j * n + i], c = __ldcg(p.coef + j);
+          sr = fma(a.x, c.x, fma(-a.y, c.y, sr));
+          si = fma(a.x, c.y, fma(a.y, c.x, si));
+        }
       }
-      const double2 rv = p.r[i];
-      const double2 nr = make_double2(rv.x - sr, rv.y - si);
-      p.r[i] = nr;
-      bp = fma(nr.x, nr.x, fma(nr.y, nr.y, bp));
+      red[tid] = make_double2(sr, si);
+      __syncthreads();
+      if (tid < rows) {
+        double tr = 0.0, ti = 0.0;
+        for (int gg = 0; gg < jg; ++gg) {
+          const double2 v = red[gg * rp + tid];
+          tr += v.x;
+          ti += v.y;
+        }
+        const double2 rv = p.r[r0 + tid];
+        const double2 nr = make_double2(rv.x - tr, rv.y - ti);
+        p.r[r0 + tid] = nr;
+        bp = fma(nr.x, nr.x, fma(nr.y, nr.y, bp));
+      }
+      __syncthreads();
+    } else {  // very tall blocks: one thread per row, fixed j order
+      for (int i = r0 + tid; i < r1; i += LZ_THREADS) {
+        double sr = 0.0, si = 0.0;
+        for (int j = 0; j <= it; ++j) {
+          const double2 a = p.V[(long long)j * n + i], c = __ldcg(p.coef + j);
+          sr = fma(a.x, c.x, fma(-a.y, c.y, sr));
+          si = fma(a.x, c.y, fma(a.y, c.x, si));
+        }
+        const double2 rv = p.r[i];
+        const double2 nr = make_double2(rv.x - sr, rv.y - si);
+        p.r[i] = nr;
+        bp = fma(nr.x, nr.x, fma(nr.y, nr.y, bp));
+      }
     }
     bp = block_sum_all(bp, sh);
     if (tid == 0) p.part[b] = bp;
