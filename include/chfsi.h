@@ -153,11 +153,13 @@ CHFSI_API int chfsi_cgs_project_z(chfsi_ctx* ctx, int n, int nlocked, int w, con
 CHFSI_API int chfsi_qr_orthonormalize_z(chfsi_ctx* ctx, int m, int n, void* Y, long long ldy, int* dead,
                               int* ndead);
 
-/* QR algorithm selection (tests/tuning): 0 = shifted Cholesky-QR3 (three
- * GEMM + potrf + TRSM passes) with automatic fallback to Householder when a
- * pivot fails or any |R_ii| < 1e-11 ||Y||_F, so the reference's rank test is
- * always decided by Householder; 1 = Householder only. Both return the same
- * (unique) Q with positive-real R diagonal. */
+/* QR algorithm selection (tests/tuning): 0 (default) = Cholesky-QR2 (two
+ * GEMM + potrf + TRSM passes), accepted when the second pass's R is the
+ * identity to 1e-6, else shifted Cholesky-QR3 (three passes, Fukaya's shift),
+ * else Householder — Householder also whenever a pivot fails or any
+ * |R_ii| < 1e-11 ||Y||_F, so the reference's rank test is always decided by
+ * Householder; 1 = Householder only; 2 = shifted Cholesky-QR3, then
+ * Householder. All return the same (unique) Q with positive-real R diagonal. */
 CHFSI_API int chfsi_ctx_set_qr_mode(chfsi_ctx* ctx, int mode);
 
 /* Dense Hermitian eigensolver (linalg.py:181-206): ascending values to the

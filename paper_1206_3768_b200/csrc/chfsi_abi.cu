@@ -489,17 +489,12 @@ int qr_householder(chfsi_ctx* ctx, int m, int n, double2* y, const double2* back
   return CHFSI_OK;
 }
 
-// Shifted Cholesky-QR3 (Fukaya et al.): three passes of Gram (ZGEMM),
-// Cholesky (potrf) and triangular solve, the first with a shift that keeps
-// the Gram matrix definite up to cond(Y) ~ 1/u. Q is the unique QR factor
-// with positive-real R diagonal, i.e. the one linalg.py:152-178 returns.
-// Returns 1 ("use Householder") when the decision of the reference's rank
-// test could be affected by Cholesky rounding: a pivot failed, or some
-// |R_ii| < 1e-11 ||Y||_F (100x above the 1e-13 threshold).
-int qr_cholqr3(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdiag_acc,
-               const double* fro, bool* fallback) {
+int qr_cholqr(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdiag_acc,
+              double* rlast, const double* fro, int passes, bool shifted, bool* fallback,
+              double* last_dev) {
   cudaStream_t s = ctx->stream;
   *fallback = false;
+  *last_dev = 0.0;
   int lwork = 0;
   CK_SOLVER(cusolverDnZpotrf_bufferSize(ctx->solver, CUBLAS_FILL_MODE_UPPER, n,
                                         reinterpret_cast<cuDoubleComplex*>(g), n, &lwork));
@@ -507,38 +502,47 @@ int qr_cholqr3(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdi
   const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
   // unit roundoff 2^-53; Fukaya's shift 11 (mn + n(n+1)) u ||Y||_2^2 with ||Y||_F >= ||Y||_2
   const double shift_coef = 11.0 * ((double)m * n + (double)n * (n + 1)) * 1.1102230246251565e-16;
-  for (int pass = 0; pass < 3; ++pass) {
+  for (int pass = 0; pass < passes; ++pass) {
     CK_BLAS(cublasZgemm(ctx->blas, CUBLAS_OP_C, CUBLAS_OP_N, n, n, m, &one,
                         reinterpret_cast<const cuDoubleComplex*>(y), m,
                         reinterpret_cast<const cuDoubleComplex*>(y), m, &zero,
                         reinterpret_cast<cuDoubleComplex*>(g), n));
-    if (pass == 0) CK_CUDA(chfsi::add_diag_shift_launch(g, n, n, fro, shift_coef, s));
+    if (shifted && pass == 0) CK_CUDA(chfsi::add_diag_shift_launch(g, n, n, fro, shift_coef, s));
     CK_SOLVER(cusolverDnZpotrf(ctx->solver, CUBLAS_FILL_MODE_UPPER, n,
                                reinterpret_cast<cuDoubleComplex*>(g), n,
                                static_cast<cuDoubleComplex*>(ctx->ws), lwork, ctx->dinfo + pass));
     CK_CUDA(chfsi::diag_accumulate_launch(g, n, n, rdiag_acc, pass == 0, s));
+    if (pass == passes - 1) CK_CUDA(chfsi::diag_accumulate_launch(g, n, n, rlast, true, s));
     CK_BLAS(cublasZtrsm(ctx->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
                         CUBLAS_DIAG_NON_UNIT, m, n, &one, reinterpret_cast<const cuDoubleComplex*>(g),
                         n, reinterpret_cast<cuDoubleComplex*>(y), m));
   }
-  CK(chfsi::ensure_pinned(ctx, (size_t)(n + 1) * sizeof(double) + 4 * sizeof(int)));
+  CK(chfsi::ensure_pinned(ctx, (size_t)(2 * n + 1) * sizeof(double) + 4 * sizeof(int)));
   double* hd = static_cast<double*>(ctx->pinned);
-  int* info = reinterpret_cast<int*>(hd + n + 1);
+  double* hl = hd + n + 1;
+  int* info = reinterpret_cast<int*>(hl + n);
   CK_CUDA(cudaMemcpyAsync(hd, rdiag_acc, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s));
   CK_CUDA(cudaMemcpyAsync(hd + n, fro, sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK_CUDA(cudaMemcpyAsync(info, ctx->dinfo, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK_CUDA(cudaMemcpyAsync(hl, rlast, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK_CUDA(cudaMemcpyAsync(info, ctx->dinfo, passes * sizeof(int), cudaMemcpyDeviceToHost, s));
   CK_CUDA(cudaStreamSynchronize(s));
   const double hfro = hd[n];
-  if (info[0] || info[1] || info[2] || !std::isfinite(hfro)) {
+  bool bad = !std::isfinite(hfro);
+  for (int pass = 0; pass < passes; ++pass) bad = bad || info[pass] != 0;
+  if (bad) {
     *fallback = true;
     return CHFSI_OK;
   }
   const double safe = 1e-11 * hfro;
-  for (int j = 0; j < n; ++j)
+  double dev = 0.0;
+  for (int j = 0; j < n; ++j) {
     if (!(hd[j] >= safe)) {  // also catches NaN
       *fallback = true;
       return CHFSI_OK;
     }
+    dev = std::max(dev, std::fabs(hl[j] - 1.0));
+  }
+  *last_dev = std::isfinite(dev) ? dev : INFINITY;
   return CHFSI_OK;
 }
 
@@ -556,10 +560,11 @@ int chfsi_qr_orthonormalize_z(chfsi_ctx* ctx, int m, int n, void* Y, long long l
   CK_ARG(ldy == m, "QR needs a packed block (ldy == m)");
   cudaStream_t s = ctx->stream;
   double2* y = static_cast<double2*>(Y);
-  // scratch: backup copy of Y (m*n), tau (n), rdiag (n), Gram (n*n), diag accumulator (n)
+  // scratch: backup copy of Y (m*n), tau (n), rdiag (n), Gram (n*n), diag accumulator (n),
+  // last pass's diagonal (n)
   const size_t blk = (size_t)m * n * sizeof(double2);
   CK(ensure_scratch(ctx, blk + 2 * (size_t)n * sizeof(double2) + (size_t)n * n * sizeof(double2) +
-                             (size_t)n * sizeof(double)));
+                             2 * (size_t)n * sizeof(double)));
   double2* backup = static_cast<double2*>(ctx->scratch);
   double2* tau = backup + (size_t)m * n;
   double2* rdiag = tau + n;
@@ -568,9 +573,21 @@ int chfsi_qr_orthonormalize_z(chfsi_ctx* ctx, int m, int n, void* Y, long long l
   double* fro = ctx->scalars + 1;
   CK_CUDA(cudaMemcpyAsync(backup, y, blk, cudaMemcpyDeviceToDevice, s));
   CK_CUDA(chfsi::norm2_launch(y, (long long)m * n, ctx->partial, fro, nullptr, s));
-  if (ctx->qr_mode != 1) {  // 0: Cholesky-QR3 first, 1: Householder only
+  if (ctx->qr_mode != 1) {  // 0: Cholesky-QR first, 1: Householder only
     bool fallback = false;
-    CK(qr_cholqr3(ctx, m, n, y, g, racc, fro, &fallback));
+    double dev = 0.0;
+    // Cholesky-QR2 (no shift) accepts when the second pass's R is the
+    // identity to 1e-6, i.e. the first pass already left Q within 1e-6 of
+    // orthonormal: the second pass then makes it orthonormal to rounding.
+    // The filtered panels are well conditioned (R diagonal ranges <= 50 over
+    // the C2 sequence), so this is the common case; otherwise the shifted
+    // Cholesky-QR3 runs from the backup, and Householder after that.
+    if (ctx->qr_mode == 0) {
+      CK(qr_cholqr(ctx, m, n, y, g, racc, racc + n, fro, 2, false, &fallback, &dev));
+      if (!fallback && dev <= 1e-6) return CHFSI_OK;
+      CK_CUDA(cudaMemcpyAsync(y, backup, blk, cudaMemcpyDeviceToDevice, s));
+    }
+    CK(qr_cholqr(ctx, m, n, y, g, racc, racc + n, fro, 3, true, &fallback, &dev));
     if (!fallback) return CHFSI_OK;
     CK_CUDA(cudaMemcpyAsync(y, backup, blk, cudaMemcpyDeviceToDevice, s));
   }
@@ -586,7 +603,9 @@ int chfsi_ctx_set_lanczos_mode(chfsi_ctx* ctx, int mode) {
 
 int chfsi_ctx_set_qr_mode(chfsi_ctx* ctx, int mode) {
   CK_ARG(ctx, "ctx is NULL");
-  CK_ARG(mode == 0 || mode == 1, "qr mode must be 0 (Cholesky-QR3 + fallback) or 1 (Householder)");
+  CK_ARG(mode >= 0 && mode <= 2,
+         "qr mode must be 0 (Cholesky-QR2, then shifted Cholesky-QR3, then Householder), "
+         "1 (Householder) or 2 (shifted Cholesky-QR3, then Householder)");
   ctx->qr_mode = mode;
   return CHFSI_OK;
 }

@@ -262,9 +262,11 @@ def set_qr_mode(mode):
     L.check(L.lib().chfsi_ctx_set_qr_mode(L.ctx(), mode))
 
 
+@pytest.mark.parametrize("mode", [0, 2])
 @pytest.mark.parametrize("kind", ["random", "graded", "near_dependent", "tall"])
-def test_cholqr3_matches_householder(pkg, kind):
-    """Shifted Cholesky-QR3 (default) vs Householder: the same unique Q
+def test_cholqr3_matches_householder(pkg, kind, mode):
+    """Cholesky-QR2 with its shifted-QR3 escalation (mode 0, default) and
+    shifted Cholesky-QR3 (mode 2) vs Householder: the same unique Q
     (positive-real R diagonal) to rounding x cond, orthonormal to 1e-13."""
     rng = np.random.default_rng(31)
     m, n = (4000, 24) if kind == "tall" else (300, 40)
@@ -279,7 +281,7 @@ def test_cholqr3_matches_householder(pkg, kind):
     try:
         set_qr_mode(1)
         qh = pkg.qr_orthonormalize(y).cpu().numpy()
-        set_qr_mode(0)
+        set_qr_mode(mode)
         qc = pkg.qr_orthonormalize(y).cpu().numpy()
     finally:
         set_qr_mode(0)
