@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -622,14 +623,18 @@ namespace {
 // stops as soon as max|G_ij| <= tol * max(1, max|G_ii|), and the number of
 // NS iterations follows r (the unitarity defect of W X is ~|S|^2 and squares
 // per NS iteration). *done = false (A untouched) when G is not in that regime
-// (r > 0.1), does not converge within kMaxSteps, or W is not unitary to
+// (r > 0.5, CHFSI_RR_BAIL), does not converge within kMaxSteps, or W is not unitary to
 // rounding (defect at the last NS input > 1e-8): the caller uses zheevd.
 int heev_near_diag(chfsi_ctx* ctx, int n, double2* a, long long lda, double* w, double tol,
                    bool* done) {
   *done = false;
   cudaStream_t s = ctx->stream;
   const size_t mat = (size_t)n * n * sizeof(double2);
-  constexpr int kMaxSteps = 4;
+  constexpr int kMaxSteps = 6;
+  static const double bail = [] {  // regime bound on max|G_ij| / |d_j - d_i| (tuning)
+    const char* e = getenv("CHFSI_RR_BAIL");
+    return e ? atof(e) : 0.5;  // measured: 0.1 -> 0.5 turns 5 of the cold C2 start's 10 zheevd calls into fast ones
+  }();
   constexpr int kSlots = 4 * (kMaxSteps + 1) + kMaxSteps;  // build stats + NS defects
   const size_t need = 5 * mat + kSlots * sizeof(double) + (size_t)n * sizeof(int) + 1024;
   if (need > ctx->eig_ws_bytes) {
@@ -669,12 +674,14 @@ int heev_near_diag(chfsi_ctx* ctx, int n, double2* a, long long lda, double* w, 
       CK_CUDA(cudaMemcpyAsync(hs + 4, defect + it - 1, sizeof(double), cudaMemcpyDeviceToHost, s));
     CK_CUDA(cudaStreamSynchronize(s));
     const double rmax = hs[0], emax = hs[1], dmax = hs[2];
+    static const bool dbg = getenv("CHFSI_RR_DEBUG") != nullptr;  // diagnostics: regime per step
+    if (dbg) fprintf(stderr, "nd n=%d it=%d rmax=%.3e emax=%.3e dmax=%.3e\n", n, it, rmax, emax, dmax);
     if (it > 0) last_defect = hs[4];
     if (it > 0 && emax <= tol * std::max(1.0, dmax)) {
       if (!(last_defect <= 1e-8)) return CHFSI_OK;  // W not unitary to rounding: zheevd
       break;
     }
-    if (it == kMaxSteps || !(rmax <= 0.1)) return CHFSI_OK;  // not near-diagonal / not converging
+    if (it == kMaxSteps || !(rmax <= bail)) return CHFSI_OK;  // not near-diagonal / not converging
     if (it == 0) {
       std::swap(W, X);  // W = X
     } else {
@@ -683,7 +690,7 @@ int heev_near_diag(chfsi_ctx* ctx, int n, double2* a, long long lda, double* w, 
     }
     // unitarity defect of W X ~ |S|^2 <~ (sqrt(n) r)^2, squared by each NS step
     const double sr = std::sqrt((double)n) * rmax;
-    const int ns = sr <= 5e-5 ? 1 : (sr <= 7e-3 ? 2 : 3);
+    const int ns = sr <= 5e-5 ? 1 : (sr <= 7e-3 ? 2 : (sr <= 0.08 ? 3 : (sr <= 0.3 ? 4 : 5)));
     for (int k = 0; k < ns; ++k) {  // W <- W (3I - W^H W) / 2
       CK(gemm(CUBLAS_OP_C, W, W, Y));
       CK_CUDA(chfsi::nd_ns_matrix_launch(Y, n, n, k == ns - 1 ? defect + it : nullptr, s));
