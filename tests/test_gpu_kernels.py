@@ -367,6 +367,24 @@ def test_reduction_matches_reference_golden(pkg, small_golden, name):
     np.testing.assert_allclose(x, xref, rtol=0, atol=1e-11 * max(1.0, np.abs(xref).max()))
 
 
+@pytest.mark.parametrize("n,nev", [(700, 40), (1500, 97), (2048, 128)])
+def test_back_transform_blocked_matches_triangular_solve(pkg, n, nev):
+    """x = L^-H y through the block back-substitution (n > 512: ZTRSM on
+    256-row diagonal blocks + ZGEMM updates) vs scipy's triangular solve."""
+    import scipy.linalg
+
+    rng = np.random.default_rng(n)
+    c = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    b = np.eye(n) + c @ c.conj().T / (4 * n)
+    l = np.linalg.cholesky(b)
+    y = rng.standard_normal((n, nev)) + 1j * rng.standard_normal((n, nev))
+    sol = pkg.EigenSolution(values=np.zeros(nev), vectors=y)
+    x = pkg.back_transform(torch.from_numpy(np.asfortranarray(l)).cuda().t().contiguous().t(),
+                           sol).vectors.cpu().numpy()
+    ref = scipy.linalg.solve_triangular(l, y, lower=True, trans="C")
+    assert np.abs(x - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
 def test_reduction_rejects_indefinite_overlap(pkg):
     rng = np.random.default_rng(8)
     a = random_hermitian(rng, 6)
