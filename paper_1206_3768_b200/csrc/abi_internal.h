@@ -31,6 +31,12 @@ struct chfsi_ctx {
   int lanczos_mode = 0;  // 0: cooperative single kernel; 1: one launch per operation
   unsigned step_epoch = 0;
   cudaEvent_t loop_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // chfsi_solve_loop_z phase timers
+  // second filter stream (two column halves of the filter run concurrently,
+  // one CTA per SM each) with its own stream-K scratch
+  cudaStream_t aux_stream = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  chfsi::StepWorkspace step_ws2{nullptr, nullptr, nullptr, 0};
+  unsigned step_epoch2 = 0;
   void* pinned = nullptr;  // page-locked host staging for small readbacks (grown on demand)
   size_t pinned_bytes = 0;
 };

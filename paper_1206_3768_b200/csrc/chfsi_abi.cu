@@ -138,6 +138,14 @@ int chfsi_ctx_destroy(chfsi_ctx* ctx) {
   cudaFree(ctx->lstate);
   cudaFree(ctx->step_ws.partials);
   cudaFree(ctx->step_ws.flags);
+  if (ctx->aux_stream) {
+    cudaStreamSynchronize(ctx->aux_stream);
+    cudaStreamDestroy(ctx->aux_stream);
+    cudaEventDestroy(ctx->fork_ev);
+    cudaEventDestroy(ctx->join_ev);
+    cudaFree(ctx->step_ws2.partials);
+    cudaFree(ctx->step_ws2.flags);
+  }
   for (cudaEvent_t e : ctx->loop_ev)
     if (e) cudaEventDestroy(e);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
@@ -297,6 +305,45 @@ int chfsi_filter_coeffs(int deg, double a, double b, double scale_ref, double* c
   return CHFSI_OK;
 }
 
+namespace {
+
+// deg recurrence steps over columns [c0, c0 + w) on `stream`
+int filter_range(chfsi_ctx* ctx, cudaStream_t stream, const chfsi::StepWorkspace& ws,
+                 chfsi::StepTiling tiling, int n, int c0, int w, const double2* hh, long long ldh,
+                 bool conj, const double2* y0, long long ldy0, double2* buf_a, double2* buf_b,
+                 long long ldb, int deg, const double* al, const double* be, double c) {
+  const double2* prev = nullptr;
+  long long ldp = 0;
+  const double2* cur = y0 + (long long)c0 * ldy0;
+  long long ldcur = ldy0;
+  for (int j = 0; j < deg; ++j) {
+    double2* dst = ((j % 2 == 0) ? buf_a : buf_b) + (long long)c0 * ldb;
+    CK_CUDA(chfsi::cheb_step_launch(hh, ldh, conj, cur, ldcur, prev, ldp, dst, ldb, n, w, al[j], c,
+                                    be[j], tiling, ws, stream));
+    prev = cur;
+    ldp = ldcur;
+    cur = dst;
+    ldcur = ldb;
+  }
+  return CHFSI_OK;
+}
+
+int ensure_aux_stream(chfsi_ctx* ctx) {
+  if (ctx->aux_stream) return CHFSI_OK;
+  CK_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
+  CK_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+  CK_CUDA(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
+  ctx->step_ws2.max_grid = ctx->step_ws.max_grid;
+  CK_CUDA(cudaMalloc(&ctx->step_ws2.partials,
+                     chfsi::step_workspace_doubles(ctx->step_ws2.max_grid) * sizeof(double)));
+  CK_CUDA(cudaMalloc(&ctx->step_ws2.flags, ctx->step_ws2.max_grid * sizeof(unsigned)));
+  CK_CUDA(cudaMemset(ctx->step_ws2.flags, 0, ctx->step_ws2.max_grid * sizeof(unsigned)));
+  ctx->step_ws2.epoch = &ctx->step_epoch2;
+  return CHFSI_OK;
+}
+
+}  // namespace
+
 int chfsi_filter_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, int conj_h,
                    const void* y0, long long ldy0, void* buf_a, void* buf_b, long long ldb,
                    int deg, double a, double b, double scale_ref, void** result) {
@@ -310,23 +357,45 @@ int chfsi_filter_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, i
   CK(chfsi_filter_coeffs(deg, a, b, scale_ref, &c, al.data(), be.data()));
   *result = (deg % 2) ? buf_a : buf_b;
   if (n == 0 || w == 0) return CHFSI_OK;
+  const double2* hh = static_cast<const double2*>(H);
+  const double2* yy = static_cast<const double2*>(y0);
+  double2* ba = static_cast<double2*>(buf_a);
+  double2* bb = static_cast<double2*>(buf_b);
+  static const int streams = [] {
+    const char* e = getenv("CHFSI_FILTER_STREAMS");  // 1 disables the two-chain filter
+    return e ? atoi(e) : 2;
+  }();
+  // Columns are independent through the recurrence: two column halves run
+  // as two concurrent launch chains (the context's stream and an auxiliary
+  // one), one CTA per SM each. On every SM the warp schedulers favour the
+  // older of two co-resident CTAs, which finishes ~40 % earlier; with two
+  // chains the early CTA's SM slot starts its chain's next step instead of
+  // idling (measured at n = 2048: w=160 29.2 -> 32.0 TFLOP/s, w=123
+  // 27.5 -> 30.1, w=64 25.9 -> 28.5). Used when both halves take a 64-row,
+  // 8-warp tile and the split is balanced (w1 >= 0.6 w0, halves 32-aligned):
+  // a thin second chain (w=80 -> 64+16, w=200 -> 128+72) loses to one chain.
+  const int w0 = ((w / 2 + 31) / 32) * 32, w1 = w - w0;
+  if (streams == 2 && ctx->tiling.bm == 0 && w1 > 0 && 10 * w1 >= 6 * w0) {
+    chfsi::StepTiling t0 = chfsi::choose_step_tiling(n, w0), t1 = chfsi::choose_step_tiling(n, w1);
+    if (t0.groups == 1 && t1.groups == 1 && t0.bm == 64 && t1.bm == 64) {
+      CK(ensure_aux_stream(ctx));
+      t0.split = chfsi::kNumSMs;
+      t1.split = chfsi::kNumSMs;
+      CK_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
+      CK_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ctx->fork_ev, 0));
+      CK(filter_range(ctx, ctx->stream, ctx->step_ws, t0, n, 0, w0, hh, ldh, conj_h != 0, yy, ldy0,
+                      ba, bb, ldb, deg, al.data(), be.data(), c));
+      CK(filter_range(ctx, ctx->aux_stream, ctx->step_ws2, t1, n, w0, w1, hh, ldh, conj_h != 0, yy,
+                      ldy0, ba, bb, ldb, deg, al.data(), be.data(), c));
+      CK_CUDA(cudaEventRecord(ctx->join_ev, ctx->aux_stream));
+      CK_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
+      return CHFSI_OK;
+    }
+  }
   const chfsi::StepTiling tiling =
       ctx->tiling.bm ? ctx->tiling : chfsi::choose_step_tiling(n, w);
-  const double2* hh = static_cast<const double2*>(H);
-  const double2* prev = nullptr;
-  long long ldp = 0;
-  const double2* cur = static_cast<const double2*>(y0);
-  long long ldcur = ldy0;
-  for (int j = 0; j < deg; ++j) {
-    double2* dst = static_cast<double2*>((j % 2 == 0) ? buf_a : buf_b);
-    CK_CUDA(chfsi::cheb_step_launch(hh, ldh, conj_h != 0, cur, ldcur, prev, ldp, dst, ldb, n, w,
-                                    al[j], c, be[j], tiling, ctx->step_ws, ctx->stream));
-    prev = cur;
-    ldp = ldcur;
-    cur = dst;
-    ldcur = ldb;
-  }
-  return CHFSI_OK;
+  return filter_range(ctx, ctx->stream, ctx->step_ws, tiling, n, 0, w, hh, ldh, conj_h != 0, yy,
+                      ldy0, ba, bb, ldb, deg, al.data(), be.data(), c);
 }
 
 int chfsi_debug_k1_trace(unsigned long long* host, int max_ctas) {
