@@ -371,13 +371,20 @@ int chfsi_filter_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, i
   // older of two co-resident CTAs, which finishes ~40 % earlier; with two
   // chains the early CTA's SM slot starts its chain's next step instead of
   // idling (measured at n = 2048: w=160 29.2 -> 32.0 TFLOP/s, w=123
-  // 27.5 -> 30.1, w=64 25.9 -> 28.5). Used when both halves take a 64-row,
-  // 8-warp tile and the split is balanced (w1 >= 0.6 w0, halves 32-aligned):
-  // a thin second chain (w=80 -> 64+16, w=200 -> 128+72) loses to one chain.
+  // 27.5 -> 30.1, w=64 25.9 -> 28.5; n = 4096..8192 +2-5 % over the
+  // one-CTA-per-SM tiles). Used for n < 10000 when the split is balanced
+  // (w1 >= 0.6 w0, halves 32-aligned): a thin second chain (w=80 -> 64+16,
+  // w=200 -> 128+72) loses to one chain.
   const int w0 = ((w / 2 + 31) / 32) * 32, w1 = w - w0;
   if (streams == 2 && ctx->tiling.bm == 0 && w1 > 0 && 10 * w1 >= 6 * w0) {
-    chfsi::StepTiling t0 = chfsi::choose_step_tiling(n, w0), t1 = chfsi::choose_step_tiling(n, w1);
-    if (t0.groups == 1 && t1.groups == 1 && t0.bm == 64 && t1.bm == 64) {
+    // each chain: the 8-warp 64-row tile (64x16 when it pads >10 % less)
+    auto chain_tiling = [](int wc) {
+      const int p16 = ((wc + 15) / 16) * 16, p32 = ((wc + 31) / 32) * 32;
+      return p16 * 10 < p32 * 9 ? chfsi::StepTiling{64, 16, 0} : chfsi::StepTiling{64, 32, 0};
+    };
+    chfsi::StepTiling t0 = chain_tiling(w0), t1 = chain_tiling(w1);
+    // (n >= 10000: the single 16-warp 128x32 chain is ahead, 34.9 vs 34.2 at C4)
+    if (n < 10000) {
       CK(ensure_aux_stream(ctx));
       t0.split = chfsi::kNumSMs;
       t1.split = chfsi::kNumSMs;
