@@ -65,6 +65,11 @@ CHFSI_API int chfsi_ctx_set_tiling(chfsi_ctx* ctx, int bm, int bn, int grid);
 /* With a forced tiling: groups = 2 selects the one-CTA-per-SM K1 whose two
  * 8-warp groups take alternate k-slabs of the same tile (64x16, 64x32). */
 CHFSI_API int chfsi_ctx_set_step_groups(chfsi_ctx* ctx, int groups);
+/* Filter launch chains (default 2): with 2, chfsi_filter_z runs balanced
+ * column halves as two concurrent launch chains (the context's stream and an
+ * internal one, joined before returning) when the automatic tiling allows;
+ * 1 = one chain (tests/tuning). */
+CHFSI_API int chfsi_ctx_set_filter_chains(chfsi_ctx* ctx, int chains);
 
 /* ---------------------------------------------------------------- K1 ---
  * One fused Chebyshev step (chfsi.py:203 / chfsi.py:206):

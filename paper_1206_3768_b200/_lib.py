@@ -60,6 +60,7 @@ _SIGNATURES = {
     "chfsi_ctx_set_stream": [_vp, _vp],
     "chfsi_ctx_set_tiling": [_vp, _i, _i, _i],
     "chfsi_ctx_set_step_groups": [_vp, _i],
+    "chfsi_ctx_set_filter_chains": [_vp, _i],
     "chfsi_cheb_step_z": [_vp, _i, _i, _vp, _ll, _i, _vp, _ll, _vp, _ll, _vp, _ll, _d, _d, _d],
     "chfsi_cheb_step_rows_z": [_vp, _i, _i, _i, _vp, _ll, _i, _vp, _ll, _i, _i, _vp, _ll, _vp, _ll,
                                _vp, _ll, _d, _d, _d],

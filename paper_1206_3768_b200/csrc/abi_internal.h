@@ -37,6 +37,7 @@ struct chfsi_ctx {
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   chfsi::StepWorkspace step_ws2{nullptr, nullptr, nullptr, 0};
   unsigned step_epoch2 = 0;
+  int filter_chains = 2;  // 1: one launch chain per filter (chfsi_ctx_set_filter_chains)
   void* pinned = nullptr;  // page-locked host staging for small readbacks (grown on demand)
   size_t pinned_bytes = 0;
 };

@@ -166,6 +166,13 @@ int chfsi_ctx_set_tiling(chfsi_ctx* ctx, int bm, int bn, int split) {
   return CHFSI_OK;
 }
 
+int chfsi_ctx_set_filter_chains(chfsi_ctx* ctx, int chains) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(chains == 1 || chains == 2, "chains must be 1 or 2");
+  ctx->filter_chains = chains;
+  return CHFSI_OK;
+}
+
 int chfsi_ctx_set_step_groups(chfsi_ctx* ctx, int groups) {
   CK_ARG(ctx, "ctx is NULL");
   CK_ARG(groups == 1 || groups == 2, "groups must be 1 or 2");
@@ -361,10 +368,11 @@ int chfsi_filter_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, i
   const double2* yy = static_cast<const double2*>(y0);
   double2* ba = static_cast<double2*>(buf_a);
   double2* bb = static_cast<double2*>(buf_b);
-  static const int streams = [] {
+  static const int env_chains = [] {
     const char* e = getenv("CHFSI_FILTER_STREAMS");  // 1 disables the two-chain filter
     return e ? atoi(e) : 2;
   }();
+  const int streams = std::min(env_chains, ctx->filter_chains);
   // Columns are independent through the recurrence: two column halves run
   // as two concurrent launch chains (the context's stream and an auxiliary
   // one), one CTA per SM each. On every SM the warp schedulers favour the

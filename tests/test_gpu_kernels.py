@@ -139,6 +139,32 @@ def test_cheb_step_bitwise_repeatable(pkg, n, w, grid, bm, groups):
         assert torch.equal(o, outs[0])
 
 
+@pytest.mark.parametrize("n,w", [(2048, 160), (2048, 64), (3000, 123), (5000, 250)])
+def test_two_chain_filter_matches_one_chain_and_oracle(pkg, n, w):
+    """The default filter runs balanced column halves as two concurrent
+    launch chains: same result as one chain (to rounding) and as the oracle,
+    bitwise reproducible run to run."""
+    L = _lib()
+    rng = np.random.default_rng(n + w)
+    h = random_hermitian(rng, n)
+    y = rng.standard_normal((n, w)) + 1j * rng.standard_normal((n, w))
+    hd, yd = torch.from_numpy(h).cuda(), fb(y)
+    ev = np.linalg.eigvalsh(h)
+    win = pkg.FilterWindow(a=float(ev[n // 4]), b=float(ev[-1]) + 0.1, scale_ref=float(ev[0]))
+    two = [pkg.chebyshev_filter(hd, yd, 6, win) for _ in range(5)]
+    try:
+        L.check(L.lib().chfsi_ctx_set_filter_chains(L.ctx(), 1))
+        one = pkg.chebyshev_filter(hd, yd, 6, win)
+    finally:
+        L.check(L.lib().chfsi_ctx_set_filter_chains(L.ctx(), 2))
+    for t in two[1:]:
+        assert torch.equal(t, two[0])
+    scale = one.abs().max().item()
+    assert (two[0] - one).abs().max().item() <= 1e-13 * scale
+    ref = orc.chebyshev_filter(h, y, 6, win.a, win.b, win.scale_ref)
+    assert np.abs(two[0].cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
 @pytest.mark.parametrize("name", sorted(FILTER_CASES))
 def test_filter_matches_reference_golden(pkg, small_golden, name):
     h, y, (a, b, s), deg = build_filter_case(FILTER_CASES[name])
