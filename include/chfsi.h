@@ -205,6 +205,14 @@ CHFSI_API int chfsi_trsm_z(chfsi_ctx* ctx, char side, char trans, int m, int n, 
  * (lower, column-major) and A holds H = L^-1 A L^-H, re-symmetrised. */
 CHFSI_API int chfsi_to_standard_z(chfsi_ctx* ctx, int n, void* A, long long lda, void* B, long long ldb,
                         int rowmajor_in, int* info);
+/* Stream-ordered variants for pipelined sequences (no host synchronisation):
+ * the potrf pivot status / (defect, max|A|) are copied to caller-owned
+ * PAGE-LOCKED host memory and are valid once the stream has passed this
+ * point; the caller raises the reference's exceptions then. */
+CHFSI_API int chfsi_to_standard_async_z(chfsi_ctx* ctx, int n, void* A, long long lda, void* B,
+                                        long long ldb, int rowmajor_in, int* info_host);
+CHFSI_API int chfsi_herm_defect_async_z(chfsi_ctx* ctx, int n, const void* A, long long lda,
+                                        double* out_host);
 /* back_transform (reduction.py:122-134): Y <- L^-H Y in place. */
 CHFSI_API int chfsi_back_transform_z(chfsi_ctx* ctx, int n, int nev, const void* L, long long ldl, void* Y,
                            long long ldy);

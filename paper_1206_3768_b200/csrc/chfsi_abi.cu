@@ -905,6 +905,47 @@ int chfsi_trsm_z(chfsi_ctx* ctx, char side, char trans, int m, int n, const void
   return CHFSI_OK;
 }
 
+int chfsi_to_standard_async_z(chfsi_ctx* ctx, int n, void* A, long long lda, void* B,
+                              long long ldb, int rowmajor_in, int* info_host) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(info_host, "info_host is NULL");
+  if (n == 0) {
+    *info_host = 0;
+    return CHFSI_OK;
+  }
+  cudaStream_t s = ctx->stream;
+  if (rowmajor_in) {
+    CK(chfsi_conj_z(ctx, n, n, A, lda));
+    CK(chfsi_conj_z(ctx, n, n, B, ldb));
+  }
+  cuDoubleComplex* b = static_cast<cuDoubleComplex*>(B);
+  int lwork = 0;
+  CK_SOLVER(cusolverDnZpotrf_bufferSize(ctx->solver, CUBLAS_FILL_MODE_LOWER, n, b, (int)ldb, &lwork));
+  CK(ensure_ws(ctx, (size_t)lwork * sizeof(cuDoubleComplex)));
+  CK_SOLVER(cusolverDnZpotrf(ctx->solver, CUBLAS_FILL_MODE_LOWER, n, b, (int)ldb,
+                             static_cast<cuDoubleComplex*>(ctx->ws), lwork, ctx->dinfo));
+  CK_CUDA(cudaMemcpyAsync(info_host, ctx->dinfo, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK_CUDA(chfsi::zero_upper_launch(static_cast<double2*>(B), ldb, n, s));
+  CK(chfsi_trsm_z(ctx, 'L', 'N', n, n, B, ldb, A, lda));
+  CK(chfsi_trsm_z(ctx, 'R', 'C', n, n, B, ldb, A, lda));
+  CK(chfsi_symmetrize_z(ctx, n, A, lda));
+  return CHFSI_OK;
+}
+
+int chfsi_herm_defect_async_z(chfsi_ctx* ctx, int n, const void* A, long long lda,
+                              double* out_host) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(out_host, "NULL output");
+  if (n == 0) {
+    out_host[0] = out_host[1] = 0.0;
+    return CHFSI_OK;
+  }
+  double* out = ctx->scalars + 4;
+  CK_CUDA(chfsi::herm_defect_launch(static_cast<const double2*>(A), lda, n, out, ctx->stream));
+  CK_CUDA(cudaMemcpyAsync(out_host, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  return CHFSI_OK;
+}
+
 int chfsi_to_standard_z(chfsi_ctx* ctx, int n, void* A, long long lda, void* B, long long ldb,
                         int rowmajor_in, int* info) {
   CK_ARG(ctx, "ctx is NULL");

@@ -25,7 +25,7 @@ import torch
 
 from .chfsi import ChfsiConfig, ChfsiGuess, chfsi_solve
 from .linalg import hermitian_eig
-from .reduction import EigenPencil, EigenSolution, back_transform, to_standard
+from .reduction import EigenPencil, EigenSolution, back_transform, stage_standard, to_standard
 
 __all__ = [
     "OracleMismatchError",
@@ -98,14 +98,20 @@ def side_stream(device=None):
 
 
 def _stage(item, side):
-    """Upload/validate and reduce one pencil on the side stream; returns
-    (pencil, StandardProblem, ready event)."""
+    """Upload, validate and reduce one pencil on the side stream without any
+    host synchronisation (the validation results land in page-locked memory
+    and are checked when the problem is about to be solved, raising the
+    reference's exceptions then); returns (pencil, StandardProblem, ready
+    event, pending checks)."""
     with torch.cuda.stream(side):
-        pencil = _as_pencil(item)
-        sp = to_standard(pencil)
+        if isinstance(item, EigenPencil):  # validated at construction
+            pencil, sp, checks = stage_standard(item.a, item.b, item.label, check_hermitian=False)
+        else:
+            label, a, b = item
+            pencil, sp, checks = stage_standard(a, b, label)
         ev = torch.cuda.Event()
         ev.record(side)
-    return pencil, sp, ev
+    return pencil, sp, ev, checks
 
 
 def _reserve_outputs(pencil, cfg, pencils):
@@ -158,7 +164,9 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
         _reserve_outputs(staged[0], cfg, pencils)
     while staged is not None:
         t0 = time.perf_counter()
-        pencil, sp, ev = staged
+        pencil, sp, ev, checks = staged
+        ev.synchronize()  # long done for l >= 2: staged while l-1 was solved
+        checks.raise_if_invalid()
         main.wait_event(ev)
         if side is not main:
             for t in (sp.h, sp.cholesky_factor, pencil.a, pencil.b):

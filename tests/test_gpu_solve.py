@@ -277,3 +277,23 @@ def test_c3_harness_protocol_matches_reference(pkg):
             assert subspace_sines(dvec[:, : cfg_b.nev].cpu().numpy(), v).max() <= 1e-6
         prev = pkg.ChfsiGuess(vectors=dvec[:, : cfg_b.blk], lambda1=float(dv[0]),
                               lambda_blk_plus_1=float(dv[cfg_b.blk]))
+
+
+def test_sequence_driver_raises_reference_errors_for_staged_problems(pkg):
+    """solve_sequence stages problem l+1 without host syncs; invalid inputs
+    still raise the reference's exceptions (before that problem is solved)."""
+    cfg_b = pkg.BASELINE_CONFIGS["C1"]
+    cfg = pkg.ChfsiConfig(nev=cfg_b.nev, nex=cfg_b.nex, deg=cfg_b.deg)
+    seq = list(pkg.iter_baseline_sequence(cfg_b.n, 2, seed=0))
+    lab, a, b = seq[1]
+    bad_a = a.copy()
+    bad_a[0, 1] += 1e-3  # not Hermitian
+    with pytest.raises(pkg.NotHermitianError):
+        pkg.solve_sequence([seq[0], (lab, bad_a, b)], cfg)
+    bad_b = b.copy()
+    bad_b[np.diag_indices(b.shape[0])] -= 10.0  # indefinite
+    with pytest.raises(pkg.NotPositiveDefiniteError):
+        pkg.solve_sequence([seq[0], (lab, a, bad_b)], cfg)
+    # and a clean sequence afterwards still solves
+    res = pkg.solve_sequence(seq, cfg)
+    assert all(r.report.converged for r in res)
