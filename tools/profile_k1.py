@@ -23,15 +23,16 @@ ap.add_argument("--w", type=int, default=160)
 ap.add_argument("--deg", type=int, default=16)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--variant", default="auto")
+ap.add_argument("--split", type=int, default=0, help="grid override (148: one chain of the two-chain filter)")
 a = ap.parse_args()
 torch.manual_seed(0)
 g = torch.randn(a.n, a.n, dtype=torch.complex128, device="cuda")
 h = (g + g.conj().T) / 2
 del g
 op = Operator(h)
-if a.variant != "auto":
-    bm, bn = (int(t) for t in a.variant.split("x"))
-    _lib.check(_lib.lib().chfsi_ctx_set_tiling(_lib.ctx(), bm, bn, 0))
+if a.variant != "auto" or a.split:
+    bm, bn = (64, 32) if a.variant == "auto" else (int(t) for t in a.variant.split("x"))
+    _lib.check(_lib.lib().chfsi_ctx_set_tiling(_lib.ctx(), bm, bn, a.split))
 y = fblock(a.n, a.w)
 y.copy_(torch.randn(a.n, a.w, dtype=torch.complex128, device="cuda"))
 x = fblock(a.n, a.w)
