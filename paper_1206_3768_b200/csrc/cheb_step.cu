@@ -70,7 +70,7 @@ struct StepParams {
   double* partials;    // [grid][ACC][THREADS]
   unsigned* flags;     // [grid]
   unsigned epoch;
-  int dbg;             // diagnostics (CHFSI_K1_DEBUG): 1 = block barrier before each refill
+  int dbg;             // diagnostics (CHFSI_K1_DEBUG): 2 = whole tiles only, 8 = trace, 16 = reversed
   unsigned long long* trace;  // dbg & 8: per CTA [start, owner wait begin, wait end, end, smid]
 };
 
