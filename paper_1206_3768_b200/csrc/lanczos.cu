@@ -4,7 +4,7 @@
 // Per step: u = H q (HBM-bound GEMV, each block its own row range),
 // alpha = Re(q^H u), r = u - alpha q - beta q_prev, full reorthogonalisation
 // r -= V (V^H r), beta = ||r||, q_next = r / beta, with the breakdown test
-// beta < 1e-14 of chfsi.py:152. Five grid-wide barriers per step replace the
+// beta < 1e-14 of chfsi.py:152. Four grid-wide barriers per step replace the
 // nine kernel launches of the multi-kernel version (launch latency dominated
 // it below n ~ 5000). Every reduction uses a fixed partition and a fixed
 // combining order (block partials summed in block order), so alphas/betas are
@@ -99,6 +99,12 @@ __global__ void __launch_bounds__(LZ_THREADS) lanczos_coop_kernel(const LanczosP
   double beta_prev = 0.0;
   for (int it = 0; it < p.k; ++it) {
     const double2* q = p.V + (long long)it * n;
+    // The GEMV input: q itself at it = 0; afterwards the complete r of the
+    // previous step scaled by 1/beta (q = r / beta is written by each block
+    // for its own rows only, so reading r saves the grid barrier that would
+    // otherwise publish q before the GEMV).
+    const double2* gq = it ? p.r : q;
+    const double gscale = it ? 1.0 / beta_prev : 1.0;
     // ---- u = H q on this block's rows (warp per row), alpha partial
     double ap = 0.0;
     for (int row = r0 + warp; row < r1; row += LZ_WARPS) {
@@ -113,7 +119,7 @@ __global__ void __launch_bounds__(LZ_THREADS) lanczos_coop_kernel(const LanczosP
 #pragma unroll
         for (int u = 0; u < 8; ++u) a[u] = __ldcs(hr + c + 32 * u);  // streamed once per step
 #pragma unroll
-        for (int u = 0; u < 8; ++u) bq[u] = q[c + 32 * u];
+        for (int u = 0; u < 8; ++u) bq[u] = gq[c + 32 * u];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           sr = fma(a[u].x, bq[u].x, fma(-sg * a[u].y, bq[u].y, sr));
@@ -121,12 +127,12 @@ __global__ void __launch_bounds__(LZ_THREADS) lanczos_coop_kernel(const LanczosP
         }
       }
       for (; c < n; c += 32) {
-        const double2 a = hr[c], bb = q[c];
+        const double2 a = hr[c], bb = gq[c];
         sr = fma(a.x, bb.x, fma(-sg * a.y, bb.y, sr));
         si = fma(a.x, bb.y, fma(sg * a.y, bb.x, si));
       }
-      sr = warp_sum(sr);
-      si = warp_sum(si);
+      sr = warp_sum(sr) * gscale;
+      si = warp_sum(si) * gscale;
       if (lane == 0) {
         p.u[row] = make_double2(sr, si);
         const double2 qv = q[row];
@@ -247,7 +253,8 @@ __global__ void __launch_bounds__(LZ_THREADS) lanczos_coop_kernel(const LanczosP
       qn[i] = make_double2(__ddiv_rn(x.x, beta), __ddiv_rn(x.y, beta));
     }
     beta_prev = beta;
-    grid.sync();  // (5) q_next complete before the next GEMV
+    // no barrier: the next GEMV reads r (complete since barrier (4)), and r
+    // is rewritten only after the next barrier (1)
   }
 }
 
