@@ -50,14 +50,20 @@ def _run(cmd, verbose):
 def build(force=False, verbose=False, ptxas_verbose=False):
     os.makedirs(BUILD, exist_ok=True)
     headers = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "chfsi.h")]
-    objs = []
+    objs, jobs = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _newer(o, [s] + headers + [__file__]):
             extra = ["-Xptxas", "-v"] if ptxas_verbose else []
-            _run([NVCC, *ARCH, *CFLAGS, *extra, "-DCHFSI_BUILDING", "-c", s, "-o", o], verbose or ptxas_verbose)
+            jobs.append([NVCC, *ARCH, *CFLAGS, *extra, "-DCHFSI_BUILDING", "-c", s, "-o", o])
+    if jobs:  # translation units compile in parallel (nvcc is single-threaded)
+        import concurrent.futures
+
+        with concurrent.futures.ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as ex:
+            for f in [ex.submit(_run, cmd, verbose or ptxas_verbose) for cmd in jobs]:
+                f.result()
     if force or _newer(LIB, objs):
         _run([NVCC, *ARCH, "-shared", *objs, "-o", LIB, *LDFLAGS], verbose)
     return LIB
