@@ -256,6 +256,8 @@ typedef struct chfsi_loop {
   double* ritz_d;            /* device, blk */
   double* res_d;             /* device, blk */
   int* perm_d;               /* device, blk ints (adaptive column order); may be NULL otherwise */
+  void* tail;                /* NULL, or n x blk (ld n): filled at exit with [locked | unlocked
+                                remainder of the final panel], the chained warm start */
   chfsi_filter_cb filter;    /* NULL: chfsi_filter_z on this context */
   chfsi_fill_cb fill;        /* NULL: rank deficiency is an error */
   void* user;

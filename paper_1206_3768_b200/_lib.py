@@ -104,7 +104,7 @@ class LoopState(ctypes.Structure):
         ("tol", _d), ("rr_fast_tol", _d),
         ("H", _vp), ("ldh", _ll), ("conj_h", _i),
         ("bufs", _vp * 2), ("hp", _vp), ("hp_rot", _vp), ("locked", _vp), ("g", _vp),
-        ("coef", _vp), ("ritz_d", _vp), ("res_d", _vp), ("perm_d", _vp),
+        ("coef", _vp), ("ritz_d", _vp), ("res_d", _vp), ("perm_d", _vp), ("tail", _vp),
         ("filter", FILTER_CB), ("fill", FILL_CB), ("user", _vp),
         ("win_a", _d), ("win_b", _d), ("win_scale_ref", _d),
         ("inner_loops", _i), ("nlocked", _i), ("pb", _i), ("off", _i), ("width", _i),

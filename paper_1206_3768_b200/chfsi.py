@@ -542,6 +542,8 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     st.g, st.coef = g_buf.data_ptr(), coef.data_ptr()
     st.ritz_d, st.res_d, st.perm_d = ritz_d.data_ptr(), res_d.data_ptr(), perm_d.data_ptr()
     st.adaptive, st.deg_min = int(cfg.adaptive_degree), int(cfg.min_degree)
+    tail = fblock(n, blk, dev)
+    st.tail = tail.data_ptr()
     st.win_a, st.win_b, st.win_scale_ref = window.a, window.b, window.scale_ref
     st.pb, st.off, st.width = 0, 0, blk
     host_f = np.zeros((4, blk))
@@ -579,13 +581,9 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     locked_vals = host_f[0, :nlocked].tolist()
     locked_res = host_f[1, :nlocked].tolist()
 
-    # chained-mode tail: [locked | unlocked remainder of the final panel]
+    # chained-mode tail [locked | unlocked remainder of the final panel],
+    # assembled by the native loop (always exactly blk columns)
     if st.inner_loops:
-        rot_p = bufs[st.last_rot_pb][:, : st.last_width]
-        n_lock = st.last_nlock
-        tail = fblock(n, nlocked + st.last_width - n_lock)
-        tail[:, :nlocked].copy_(locked[:, :nlocked])
-        tail[:, nlocked:].copy_(rot_p[:, n_lock:])
         report.tail_vectors = tail
         report.lambda_blk_plus_1 = float(host_f[2, st.last_width - 1])
 

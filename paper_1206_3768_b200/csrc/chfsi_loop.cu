@@ -248,5 +248,15 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
       have_degs = true;
     }
   }
+  // chained-mode tail: [locked | unlocked remainder of the final panel]
+  if (L->tail && L->inner_loops > 0) {
+    const size_t col_bytes = (size_t)n * sizeof(double2);
+    if (L->nlocked)
+      CK_CUDA(cudaMemcpyAsync(L->tail, L->locked, col_bytes * L->nlocked, cudaMemcpyDeviceToDevice, s));
+    const int rest = L->last_width - L->last_nlock;
+    if (rest > 0)
+      CK_CUDA(cudaMemcpyAsync(col(L->tail, n, L->nlocked), col(L->bufs[L->last_rot_pb], n, L->last_nlock),
+                              col_bytes * rest, cudaMemcpyDeviceToDevice, s));
+  }
   return CHFSI_OK;
 }

@@ -182,7 +182,7 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
         rng = np.random.default_rng((seed, pencil.label, start))
         sol, rep = chfsi_solve(sp.h, cfg, guess=guess, rng=rng, label=pencil.label, shard=shard)
         t2 = time.perf_counter()
-        gsol = back_transform(sp.cholesky_factor, sol)
+        gsol = back_transform(sp.cholesky_factor, sol, inplace=not keep_standard)
         main.synchronize()
         t3 = time.perf_counter()
         res = ProblemResult(label=pencil.label, values=sol.values, solution=gsol,
