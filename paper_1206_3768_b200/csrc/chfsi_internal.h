@@ -84,7 +84,7 @@ struct LanczosState {
   double beta_last;
 };
 // whole k-step Lanczos in one cooperative kernel (lanczos.cu)
-int lanczos_coop_grid();
+int lanczos_coop_grid(int n);
 size_t lanczos_coop_workspace_bytes(int n, int k);
 cudaError_t lanczos_coop_launch(const double2* h, long long ldh, bool conj_h, int n, int k,
                                 const double2* q0, double2* V, void* ws, double* alphas,
