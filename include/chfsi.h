@@ -94,6 +94,18 @@ CHFSI_API int chfsi_cheb_step_rows_z(chfsi_ctx* ctx, int n, int rows, int w, con
                                      int kblk, int nblk, const void* ycur_rows, long long ldcr,
                                      const void* yprev, long long ldp, void* ynext, long long ldn,
                                      double alpha, double c, double beta);
+/* Fused all-gather variant (multi-GPU over NVLink): additionally stores every
+ * output element at the same position of npeer (<= 7) peer buffers,
+ * peer_ynext[k] being the peer's equivalent of `ynext` mapped into this
+ * process (CUDA IPC / symmetric memory). The all-gather then happens tile by
+ * tile from K1's epilogue; the caller orders steps with a cross-rank
+ * barrier. */
+CHFSI_API int chfsi_cheb_step_rows_peers_z(chfsi_ctx* ctx, int n, int rows, int w, const void* H_rows,
+                                           long long ldh, int conj_h, const void* ycur, long long ldc,
+                                           int kblk, int nblk, const void* ycur_rows, long long ldcr,
+                                           const void* yprev, long long ldp, void* ynext, long long ldn,
+                                           double alpha, double c, double beta,
+                                           const void* const* peer_ynext, int npeer);
 
 /* Host-only: the filter's shift c and per-step (alpha_j, beta_j) exactly as
  * chebyshev_filter computes them (chfsi.py:198-207). alphas/betas hold deg. */

@@ -64,6 +64,8 @@ _SIGNATURES = {
     "chfsi_cheb_step_z": [_vp, _i, _i, _vp, _ll, _i, _vp, _ll, _vp, _ll, _vp, _ll, _d, _d, _d],
     "chfsi_cheb_step_rows_z": [_vp, _i, _i, _i, _vp, _ll, _i, _vp, _ll, _i, _i, _vp, _ll, _vp, _ll,
                                _vp, _ll, _d, _d, _d],
+    "chfsi_cheb_step_rows_peers_z": [_vp, _i, _i, _i, _vp, _ll, _i, _vp, _ll, _i, _i, _vp, _ll, _vp,
+                                     _ll, _vp, _ll, _d, _d, _d, ctypes.POINTER(_vp), _i],
     "chfsi_filter_coeffs": [_i, _d, _d, _d, _pd, _pd, _pd],
     "chfsi_filter_z": [_vp, _i, _i, _vp, _ll, _i, _vp, _ll, _vp, _vp, _ll, _i, _d, _d, _d,
                        ctypes.POINTER(_vp)],

@@ -478,7 +478,7 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
 
         group = shard if not isinstance(shard, (bool, int)) else None
         chunks = shard if isinstance(shard, int) and not isinstance(shard, bool) else 2
-        sharded = RowShardedFilter(op, n, group=group, chunks=chunks)
+        sharded = RowShardedFilter(op, n, group=group, chunks=chunks, max_cols=blk)
 
     bufs, hp_buf, hp_rot, locked, g_buf, coef, ritz_d, res_d, perm_d = _workspace(dev, n, blk,
                                                                                  cfg.nev)

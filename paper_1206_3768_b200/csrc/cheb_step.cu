@@ -48,6 +48,7 @@ constexpr int BK = 16;             // complex elements per K slab (two 128-byte 
 constexpr int HALF = 128;          // bytes per row per half-slab (one TMA box row)
 constexpr int kMaxThreads = 512;
 constexpr int kSlotDoubles = 8192; // partial-tile slot per CTA: ACC * THREADS <= this
+constexpr int kMaxPeers = 7;       // fused all-gather: up to 8 ranks
 
 struct StepParams {
   const double2* ycur;  // rows of Ycur matching the output rows (epilogue c*Ycur term)
@@ -72,6 +73,11 @@ struct StepParams {
   unsigned epoch;
   int dbg;             // diagnostics (CHFSI_K1_DEBUG): 2 = whole tiles only, 8 = trace, 16 = reversed
   unsigned long long* trace;  // dbg & 8: per CTA [start, owner wait begin, wait end, end, smid]
+  // fused all-gather (multi-GPU row shards): every Ynext element is also
+  // stored at ynext + peer_shift[k] — the same location of the rank-blocked
+  // buffer on peer k, mapped into this process (NVLink P2P stores)
+  long long peer_shift[kMaxPeers];
+  int npeer;
 };
 
 // ------------------------------------------------------------ PTX helpers ---
@@ -165,7 +171,10 @@ __device__ __forceinline__ void epilogue_store(const StepParams& p, int row, int
     tr = dsub(tr, dmul(p.beta, yp.x));
     ti = dsub(ti, dmul(p.beta, yp.y));
   }
-  p.ynext[(long long)col * p.ldn + row] = make_double2(tr, ti);
+  const long long idx = (long long)col * p.ldn + row;
+  const double2 v = make_double2(tr, ti);
+  p.ynext[idx] = v;
+  for (int k = 0; k < p.npeer; ++k) p.ynext[idx + p.peer_shift[k]] = v;  // P2P store to peer k
 }
 
 // GROUPS = 2: one CTA per SM holds two 8-warp groups on the SAME tile that
@@ -643,14 +652,15 @@ cudaError_t cheb_step_launch(const double2* h, long long ldh, bool conj_h, const
                              StepTiling tiling, const StepWorkspace& ws, cudaStream_t stream) {
   const RowShard whole{n, 0, 0, nullptr, 0};
   return cheb_step_rows_launch(h, ldh, conj_h, ycur, ldc, yprev, ldp, ynext, ldn, n, w, alpha, c,
-                               beta, whole, tiling, ws, stream);
+                               beta, whole, tiling, ws, stream, nullptr, 0);
 }
 
 cudaError_t cheb_step_rows_launch(const double2* h, long long ldh, bool conj_h, const double2* ycur,
                                   long long ldc, const double2* yprev, long long ldp, double2* ynext,
                                   long long ldn, int n, int w, double alpha, double c, double beta,
                                   const RowShard& shard, StepTiling tiling, const StepWorkspace& ws,
-                                  cudaStream_t stream) {
+                                  cudaStream_t stream, const long long* peer_shift, int npeer) {
+  if (npeer < 0 || npeer > kMaxPeers) return cudaErrorInvalidValue;
   const int m = shard.rows;
   if (n <= 0 || w <= 0 || m <= 0) return cudaSuccess;
   if (tiling.bm == 0) tiling = choose_step_tiling(n, w);
@@ -681,6 +691,8 @@ cudaError_t cheb_step_rows_launch(const double2* h, long long ldh, bool conj_h, 
   p.ldp = yprev ? ldp : ldn;
   p.ynext = ynext;
   p.ldn = ldn;
+  p.npeer = npeer;
+  for (int k = 0; k < npeer; ++k) p.peer_shift[k] = peer_shift[k];
   p.n = n;
   p.w = w;
   p.tiles_n = (w + v.bn - 1) / v.bn;

@@ -231,6 +231,36 @@ int chfsi_cheb_step_rows_z(chfsi_ctx* ctx, int n, int rows, int w, const void* H
   return CHFSI_OK;
 }
 
+int chfsi_cheb_step_rows_peers_z(chfsi_ctx* ctx, int n, int rows, int w, const void* H_rows,
+                                 long long ldh, int conj_h, const void* ycur, long long ldc, int kblk,
+                                 int nblk, const void* ycur_rows, long long ldcr, const void* yprev,
+                                 long long ldp, void* ynext, long long ldn, double alpha, double c,
+                                 double beta, const void* const* peer_ynext, int npeer) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(n >= 0 && rows >= 0 && w >= 0, "negative size");
+  if (n == 0 || w == 0 || rows == 0) return CHFSI_OK;
+  CK_ARG(H_rows && ycur && ynext && ycur_rows, "NULL operand");
+  CK_ARG(npeer >= 0 && npeer <= 7 && (npeer == 0 || peer_ynext), "0 <= npeer <= 7 peer outputs");
+  long long shift[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int k = 0; k < npeer; ++k) {
+    const long long d = reinterpret_cast<const char*>(peer_ynext[k]) -
+                        reinterpret_cast<const char*>(ynext);
+    CK_ARG(peer_ynext[k] && d % (long long)sizeof(double2) == 0, "peer outputs must be 16-byte aligned");
+    shift[k] = d / (long long)sizeof(double2);
+  }
+  CK_ARG(ldh >= n && ldn >= rows && ldcr >= rows && (!yprev || ldp >= rows), "leading dimension");
+  CK_ARG(kblk == 0 ? ldc >= n : (kblk % 16 == 0 && (long long)kblk * nblk >= n),
+         "blocked layout needs kblk % 16 == 0 and kblk * nblk >= n");
+  const chfsi::RowShard shard{rows, kblk, nblk, static_cast<const double2*>(ycur_rows), ldcr};
+  CK_CUDA(chfsi::cheb_step_rows_launch(static_cast<const double2*>(H_rows), ldh, conj_h != 0,
+                                       static_cast<const double2*>(ycur), ldc,
+                                       static_cast<const double2*>(yprev), ldp,
+                                       static_cast<double2*>(ynext), ldn, n, w, alpha, c, beta, shard,
+                                       ctx->tiling.bm ? ctx->tiling : chfsi::choose_step_tiling(rows, w),
+                                       ctx->step_ws, ctx->stream, shift, npeer));
+  return CHFSI_OK;
+}
+
 int chfsi_filter_degrees_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, int conj_h,
                            const void* y0, long long ldy0, void* buf_a, void* buf_b, long long ldb,
                            const int* degs, double a, double b, double scale_ref, void** result) {

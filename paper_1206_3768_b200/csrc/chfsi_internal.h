@@ -52,11 +52,15 @@ struct RowShard {
   const double2* ycur_rows;
   long long ldcr;
 };
+// peer_shift / npeer: fused all-gather — every output element is also stored
+// at ynext + peer_shift[k] (elements), k < npeer <= 7 (peers' buffers mapped
+// into this process; NVLink P2P stores from the epilogue).
 cudaError_t cheb_step_rows_launch(const double2* h, long long ldh, bool conj_h, const double2* ycur,
                                   long long ldc, const double2* yprev, long long ldp, double2* ynext,
                                   long long ldn, int n, int w, double alpha, double c, double beta,
                                   const RowShard& shard, StepTiling tiling, const StepWorkspace& ws,
-                                  cudaStream_t stream);
+                                  cudaStream_t stream, const long long* peer_shift = nullptr,
+                                  int npeer = 0);
 
 // ---- auxiliary kernels (aux_kernels.cu) ----
 // u = op(H) q for a row-major H (conj_h: conj(H)).

@@ -78,18 +78,85 @@ def from_blocked(part, buf, out):
     return out
 
 
-def gpu_row_step(op, part, ycur_blk, yprev_slab, ynext_slab, w, alpha, c, beta):
+def gpu_row_step(op, part, ycur_blk, yprev_slab, ynext_slab, w, alpha, c, beta, peers=None):
     """K1 over this rank's rows (libchfsi); slabs are [w][kblk] views of
-    the rank's block (column-major, ld kblk)."""
+    the rank's block (column-major, ld kblk). ``peers``: device addresses of
+    the same slab in the other ranks' buffers (mapped into this process) —
+    the fused all-gather, K1's epilogue storing every tile to them too."""
     if part.rows == 0:
         return
+    import ctypes
+
     h_rows = op.tensor.data_ptr() + part.r0 * op.ld * 16
     ycur_rows = ycur_blk[part.rank]
-    check(lib().chfsi_cheb_step_rows_z(
-        ctx(), part.n, part.rows, w, ctypes_ptr(h_rows), op.ld, op.conj, dptr(ycur_blk), 0,
-        part.kblk, part.world, dptr(ycur_rows), part.kblk,
-        None if yprev_slab is None else dptr(yprev_slab), part.kblk, dptr(ynext_slab),
-        part.kblk, alpha, c, beta), "sharded chebyshev step")
+    args = (ctx(), part.n, part.rows, w, ctypes_ptr(h_rows), op.ld, op.conj, dptr(ycur_blk), 0,
+            part.kblk, part.world, dptr(ycur_rows), part.kblk,
+            None if yprev_slab is None else dptr(yprev_slab), part.kblk, dptr(ynext_slab),
+            part.kblk, alpha, c, beta)
+    if peers:
+        arr = (ctypes.c_void_p * len(peers))(*peers)
+        check(lib().chfsi_cheb_step_rows_peers_z(*args, arr, len(peers)),
+              "sharded chebyshev step (fused all-gather)")
+    else:
+        check(lib().chfsi_cheb_step_rows_z(*args), "sharded chebyshev step")
+
+
+class SymmetricBlocks:
+    """Fused-all-gather storage: one symmetric-memory allocation per rank
+    (torch.distributed._symmetric_memory, CUDA IPC over NVLink) holding the
+    ping-pong rank-blocked buffers of every column group, identical layout on
+    all ranks, so a slab's peer address is the peer's base + the same offset.
+    `barrier()` is the cross-rank device barrier that orders filter steps."""
+
+    def __init__(self, part, cols, group, device):
+        import torch.distributed._symmetric_memory as symm
+
+        self.part = part
+        self.elems = 2 * part.world * cols * part.kblk  # two ping-pong slots
+        self.buf = symm.empty(self.elems, dtype=torch.complex128, device=device)
+        self.handle = symm.rendezvous(self.buf, group if group is not None else dist.group.WORLD)
+        self.base = self.buf.data_ptr()
+        self.peer_bases = [int(self.handle.buffer_ptrs[q]) for q in range(part.world)]
+        self.cols = cols
+
+    def views(self, groups):
+        """[(slot0, slot1)] blocked views [world][wg][kblk] per column group."""
+        out, off = [], 0
+        span = self.part.world * self.part.kblk
+        for j0, j1, _ in groups:
+            wg = j1 - j0
+            pair = []
+            for s in range(2):
+                start = s * self.part.world * self.cols * self.part.kblk + off
+                pair.append(self.buf[start:start + wg * span].view(self.part.world, wg,
+                                                                   self.part.kblk))
+            out.append(pair)
+            off += wg * span
+        return out
+
+    def peers_of(self, slab):
+        """Device addresses of `slab` (a view into this rank's buffer) on the other ranks."""
+        off = slab.data_ptr() - self.base
+        return [self.peer_bases[q] + off for q in range(self.part.world) if q != self.part.rank]
+
+    def barrier(self):
+        self.handle.barrier(channel=0)
+
+
+_SYMM_CACHE = {}
+
+
+def fused_available(group=None):
+    """NCCL world > 1 with torch symmetric memory (CUDA IPC peers)."""
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return False
+    if dist.get_backend(group) != "nccl":
+        return False
+    try:
+        import torch.distributed._symmetric_memory  # noqa: F401
+    except ImportError:
+        return False
+    return True
 
 
 def ctypes_ptr(addr):
@@ -125,13 +192,27 @@ class RowShardedFilter:
     libchfsi and NCCL.
     """
 
-    def __init__(self, op, n, group=None, step=None, allgather=None, chunks=1):
+    def __init__(self, op, n, group=None, step=None, allgather=None, chunks=1, fused=None,
+                 max_cols=None):
         self.group = group
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.part = RowPartition(n, world, rank)
         self.op = op
         self.chunks = max(1, int(chunks))
+        # fused all-gather: K1's epilogue stores each tile into every peer's
+        # buffer (NVLink P2P, symmetric memory); default on for NCCL worlds > 1
+        if fused is None:
+            fused = step is None and allgather is None and fused_available(group)
+        self.symm = None
+        if fused:
+            if max_cols is None:
+                raise ValueError("the fused all-gather needs max_cols (the widest panel)")
+            dev = op.tensor.device if op is not None else torch.device("cuda")
+            key = (id(group), str(dev), n, world, int(max_cols))
+            self.symm = _SYMM_CACHE.get(key)
+            if self.symm is None:  # collective allocation + IPC rendezvous: once per shape
+                self.symm = _SYMM_CACHE[key] = SymmetricBlocks(self.part, int(max_cols), group, dev)
         self.step = step or (lambda yc, yp, yn, w, a, c, b: gpu_row_step(op, self.part, yc, yp, yn,
                                                                         w, a, c, b))
         self.allgather = allgather or (lambda buf, async_op=False: nccl_allgather(
@@ -165,6 +246,8 @@ class RowShardedFilter:
                     groups.append((j0, j, degs[j0]))
                     j0 = j
         c, al, be = filter_coeffs(dmax, float(window.a), float(window.b), float(window.scale_ref))
+        if self.symm is not None:
+            return self._apply_fused(y, groups, dmax, c, al, be, out)
         bufs = [[to_blocked(part, y[:, j0:j1], blocked_empty(part, j1 - j0, dev)),
                  blocked_empty(part, j1 - j0, dev)] for j0, j1, _ in groups]
         pending = [None] * len(groups)
@@ -188,4 +271,36 @@ class RowShardedFilter:
             out = torch.empty((w, n), dtype=y.dtype, device=dev).t()
         for g, (j0, j1, _) in enumerate(groups):
             from_blocked(part, bufs[g][cur[g]], out[:, j0:j1])
+        return out
+
+    def _apply_fused(self, y, groups, dmax, c, al, be, out):
+        """Every step: K1 over this rank's rows of each column group, its
+        epilogue storing the tiles into all ranks' next buffers; then one
+        cross-rank barrier (all slabs landed before anyone reads them)."""
+        part, symm = self.part, self.symm
+        n, w = y.shape
+        if w > symm.cols:
+            raise ValueError(f"panel wider ({w}) than the symmetric buffers ({symm.cols})")
+        pairs = symm.views(groups)
+        for (j0, j1, _), pair in zip(groups, pairs):
+            pair[0].zero_()  # K padding rows must read as 0; peers write real rows only
+            pair[1].zero_()
+            to_blocked(part, y[:, j0:j1], pair[0])
+        symm.barrier()  # every rank's start block is in place before step 0 reads it
+        cur = [0] * len(groups)
+        for j in range(dmax):
+            for g, (j0, j1, dg) in enumerate(groups):
+                if j >= dg:
+                    continue
+                nxt = 1 - cur[g]
+                yprev = pairs[g][nxt][part.rank] if j > 0 else None
+                ynext = pairs[g][nxt][part.rank]
+                gpu_row_step(self.op, part, pairs[g][cur[g]], yprev, ynext, j1 - j0, al[j], c,
+                             be[j], peers=symm.peers_of(ynext))
+                cur[g] = nxt
+            symm.barrier()
+        if out is None:
+            out = torch.empty((w, n), dtype=y.dtype, device=y.device).t()
+        for g, (j0, j1, _) in enumerate(groups):
+            from_blocked(part, pairs[g][cur[g]], out[:, j0:j1])
         return out
