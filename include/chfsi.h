@@ -196,6 +196,10 @@ CHFSI_API int chfsi_heev_rr_z(chfsi_ctx* ctx, int n, void* A, long long lda, dou
  * P and lambda may be NULL (plain column norms). */
 CHFSI_API int chfsi_colnorm_residual_z(chfsi_ctx* ctx, int n, int w, const void* HP, long long ldhp,
                              const void* P, long long ldp, const double* lambda, double* res);
+/* The squares ||HP[:,j] - lambda[j] P[:,j]||^2 (row-sharded partial sums). */
+CHFSI_API int chfsi_colnorm_residual_sq_z(chfsi_ctx* ctx, int n, int w, const void* HP, long long ldhp,
+                                          const void* P, long long ldp, const double* lambda,
+                                          double* res);
 
 /* ------------------------------------------------------------------ K5 ---
  * A <- (A + A^H)/2 in place (reduction.py:112, chfsi.py:346). */
@@ -249,6 +253,18 @@ typedef int (*chfsi_filter_cb)(void* user, const void* panel, void* other, long 
                                void** result);
 typedef int (*chfsi_fill_cb)(void* user, void* block, long long ld, int rows, const int* cols,
                              int ncols);
+/* Row-sharded (multi-GPU) loop: in-place sum over the ranks of `count`
+ * doubles at the device pointer `buf`, complete on return (stream-ordered
+ * after the context's stream); identical result on every rank. */
+typedef int (*chfsi_allreduce_cb)(void* user, void* buf, long long count);
+/* out_local = rows row0..row0+n_local of H * P, from this rank's rows of P
+ * (ld n_local); complete or stream-ordered on return. */
+typedef int (*chfsi_hp_cb)(void* user, const void* panel_local, void* out_local, long long ld,
+                           int width);
+/* *full (n x width, ld n, owned by the caller of the loop) = all ranks' rows
+ * of the local block (ld ld_local). */
+typedef int (*chfsi_gather_cb)(void* user, const void* local, long long ld_local, int width,
+                               void** full);
 
 typedef struct chfsi_loop {
   /* problem and device workspace (in) */
@@ -270,6 +286,16 @@ typedef struct chfsi_loop {
   int* perm_d;               /* device, blk ints (adaptive column order); may be NULL otherwise */
   void* tail;                /* NULL, or n x blk (ld n): filled at exit with [locked | unlocked
                                 remainder of the final panel], the chained warm start */
+  /* Row-sharded mode (multi-GPU): every n x w block above holds
+   * only rows row0 .. row0+n_local-1 of this rank (ld n_local, so `n` stays
+   * the global dimension); n x w products run on local rows and their w x w
+   * / w-sized results are summed with `allreduce`; H*P comes from `hp` and
+   * the filter from `filter`; the rare full-matrix fallbacks (Householder,
+   * rank repair) use `gather`. allreduce == NULL: single GPU (n_local = n). */
+  int row0, n_local;
+  chfsi_allreduce_cb allreduce;
+  chfsi_hp_cb hp_fn;
+  chfsi_gather_cb gather;
   chfsi_filter_cb filter;    /* NULL: chfsi_filter_z on this context */
   chfsi_fill_cb fill;        /* NULL: rank deficiency is an error */
   void* user;

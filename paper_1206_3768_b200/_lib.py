@@ -82,6 +82,7 @@ _SIGNATURES = {
     "chfsi_heevd_z": [_vp, _i, _vp, _ll, _vp],
     "chfsi_heev_rr_z": [_vp, _i, _vp, _ll, _vp, _d, _pi],
     "chfsi_colnorm_residual_z": [_vp, _i, _i, _vp, _ll, _vp, _ll, _vp, _vp],
+    "chfsi_colnorm_residual_sq_z": [_vp, _i, _i, _vp, _ll, _vp, _ll, _vp, _vp],
     "chfsi_symmetrize_z": [_vp, _i, _vp, _ll],
     "chfsi_herm_defect_z": [_vp, _i, _vp, _ll, _pd, _pd],
     "chfsi_conj_z": [_vp, _i, _i, _vp, _ll],
@@ -95,6 +96,9 @@ _SIGNATURES = {
 
 FILTER_CB = ctypes.CFUNCTYPE(_i, _vp, _vp, _vp, _ll, _i, _i, _pi, _d, _d, _d, ctypes.POINTER(_vp))
 FILL_CB = ctypes.CFUNCTYPE(_i, _vp, _vp, _ll, _i, _pi, _i)
+ALLREDUCE_CB = ctypes.CFUNCTYPE(_i, _vp, _vp, _ll)
+HP_CB = ctypes.CFUNCTYPE(_i, _vp, _vp, _vp, _ll, _i)
+GATHER_CB = ctypes.CFUNCTYPE(_i, _vp, _vp, _ll, _i, ctypes.POINTER(_vp))
 
 
 class LoopState(ctypes.Structure):
@@ -107,6 +111,8 @@ class LoopState(ctypes.Structure):
         ("H", _vp), ("ldh", _ll), ("conj_h", _i),
         ("bufs", _vp * 2), ("hp", _vp), ("hp_rot", _vp), ("locked", _vp), ("g", _vp),
         ("coef", _vp), ("ritz_d", _vp), ("res_d", _vp), ("perm_d", _vp), ("tail", _vp),
+        ("row0", _i), ("n_local", _i), ("allreduce", ALLREDUCE_CB), ("hp_fn", HP_CB),
+        ("gather", GATHER_CB),
         ("filter", FILTER_CB), ("fill", FILL_CB), ("user", _vp),
         ("win_a", _d), ("win_b", _d), ("win_scale_ref", _d),
         ("inner_loops", _i), ("nlocked", _i), ("pb", _i), ("off", _i), ("width", _i),

@@ -30,7 +30,7 @@ import scipy.linalg
 import torch
 
 from ._device import C128, Operator, fblock, ld_of, to_fblock
-from ._lib import FILL_CB, FILTER_CB, LoopState, check, ctx, dptr, lib
+from ._lib import ALLREDUCE_CB, FILL_CB, FILTER_CB, GATHER_CB, HP_CB, LoopState, check, ctx, dptr, lib
 from .linalg import qr_orthonormalize_inplace
 from .reduction import EigenSolution
 
@@ -368,46 +368,92 @@ def rayleigh_ritz(h, y):
 
 class _LoopCallbacks:
     """Host callbacks of the native loop: rank-repair draws from the
-    caller's Generator (reference order, chfsi.py:255-259) and, for the
-    row-sharded multi-GPU filter, the filter itself. Exceptions raised in a
-    callback are re-raised after the loop returns."""
+    caller's Generator (reference order, chfsi.py:255-259) and, in the
+    row-sharded multi-GPU loop, the sharded filter, H*P, the all-reduce of
+    partial Grams / norms and the gather for the full-matrix fallbacks.
+    Exceptions raised in a callback are re-raised after the loop returns."""
 
-    def __init__(self, bufs, n, rng, sharded):
-        self.bufs, self.n, self.rng, self.sharded = bufs, n, rng, sharded
+    def __init__(self, bufs, rows, rng, comm=None, op=None, blk=0, reduce_bufs=(), hp_buf=None):
+        self.bufs, self.rows, self.rng = bufs, rows, rng
+        self.hp_buf = hp_buf
+        self.comm, self.op, self.blk = comm, op, blk
+        self.reduce_bufs = list(reduce_bufs)  # device tensors the loop all-reduces
+        self.full = None                      # scratch of the gather fallback
         self.error = None
         self.fill_cb = FILL_CB(self._fill)
         self.filter_cb = FILTER_CB(self._filter)
+        self.allreduce_cb = ALLREDUCE_CB(self._allreduce)
+        self.hp_cb = HP_CB(self._hp)
+        self.gather_cb = GATHER_CB(self._gather)
 
     def _view(self, ptr, width):
         for b in self.bufs:
-            off = (ptr - b.data_ptr()) // (16 * self.n)
-            if 0 <= off < b.shape[1] and b.data_ptr() + off * 16 * self.n == ptr:
+            off = (ptr - b.data_ptr()) // (16 * self.rows)
+            if 0 <= off < b.shape[1] and b.data_ptr() + off * 16 * self.rows == ptr:
                 return b[:, off:off + width]
         raise ValueError("pointer outside the panel buffers")
 
-    def _fill(self, user, block, ld, rows, cols, ncols):
+    def _guard(self, fn, *args):
         try:
-            idx = [cols[j] for j in range(ncols)]
-            work = self._view(block, max(idx) + 1)
-            fresh = random_block(self.rng, self.n, ncols)
-            for j, c in enumerate(idx):
-                work[:, c].copy_(fresh[:, j])
+            fn(*args)
             return 0
         except BaseException as exc:  # noqa: BLE001 - re-raised by reraise()
             self.error = exc
             return -1
 
+    def _fill(self, user, block, ld, rows, cols, ncols):
+        def run():
+            idx = [cols[j] for j in range(ncols)]
+            work = self._view(block, max(idx) + 1)
+            n = self.comm.part.n if self.comm is not None else self.rows
+            fresh = random_block(self.rng, n, ncols)  # every rank draws the full columns
+            if self.comm is not None:
+                fresh = fresh[self.comm.part.r0:self.comm.part.r0 + self.rows]
+            for j, c in enumerate(idx):
+                work[:, c].copy_(fresh[:, j])
+
+        return self._guard(run)
+
     def _filter(self, user, panel, other, ld, width, deg, degs, a, b, scale_ref, result):
-        try:
+        def run():
             d = [degs[j] for j in range(width)] if degs else deg
-            out = self.sharded.apply(self._view(panel, width), d,
-                                     FilterWindow(a=a, b=b, scale_ref=scale_ref),
-                                     out=self._view(other, width))
+            win = FilterWindow(a=a, b=b, scale_ref=scale_ref)
+            out = self.comm.filter_local(self.op, self.blk, self._view(panel, width), d, win,
+                                         self._view(other, width))
             result[0] = out.data_ptr()
-            return 0
-        except BaseException as exc:  # noqa: BLE001
-            self.error = exc
-            return -1
+
+        return self._guard(run)
+
+    def _allreduce(self, user, buf, count):
+        def run():
+            for t in self.reduce_bufs:
+                base = t.t() if (t.dim() == 2 and t.stride(0) == 1) else t  # F-block storage
+                flat = (torch.view_as_real(base) if base.is_complex() else base).view(-1)
+                off = (buf - base.data_ptr()) // 8
+                if 0 <= off and off + count <= flat.numel() and base.data_ptr() + 8 * off == buf:
+                    self.comm.allreduce_(flat[off:off + count])
+                    return
+            raise ValueError("allreduce pointer outside the reduction buffers")
+
+        return self._guard(run)
+
+    def _hp(self, user, panel, out, ld, width):
+        def run():
+            assert out == self.hp_buf.data_ptr()
+            self.comm.hp_local(self.op, self._view(panel, width), self.hp_buf[:, :width])
+
+        return self._guard(run)
+
+    def _gather(self, user, local, ld, width, full_out):
+        def run():
+            n = self.comm.part.n
+            if self.full is None or self.full.shape[1] < width:
+                self.full = fblock(n, max(width, self.blk), self.bufs[0].device)
+            full = self.full[:, :width]
+            self.comm.gather_rows(self._view(local, width), full)
+            full_out[0] = full.data_ptr()
+
+        return self._guard(run)
 
     def reraise(self):
         if self.error is not None:
@@ -454,12 +500,15 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     (chfsi.py:274-384). ``h`` may be a numpy array (uploaded once) or a CUDA
     tensor in either row- or column-major layout (used in place).
 
-    ``shard`` (multi-GPU): ``True`` or a torch.distributed process
-    group row-shards the filter across the group's ranks (one GPU each; every
-    rank calls chfsi_solve with the same arguments); ``shard=k`` (int) also
-    sets the number of overlapped column groups. Everything else is computed
-    redundantly and bit-identically on every rank, so no other exchange is
-    needed and every rank returns the same solution.
+    ``shard`` (multi-GPU): ``True``, a torch.distributed process
+    group or a `distributed.RowComm` runs the row-sharded loop: every rank
+    (one GPU each, all calling chfsi_solve with the same arguments) keeps its
+    rows of every n x w block, the filter and H*P run as row-sharded K1
+    steps (fused all-gather over NVLink with NCCL), and the w x w Grams and
+    residual norms are all-reduced; Lanczos and the w x w eigenproblems are
+    replicated from identical inputs. ``shard=k`` (int) also sets the number
+    of column groups of the unfused filter. Every rank returns the same full
+    solution; ``report.tail_vectors`` holds this rank's rows.
 
     Returns ``(EigenSolution(form="standard"), SolveReport)``; the solution
     vectors stay on the device.
@@ -472,15 +521,21 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     report = SolveReport()
     dev = op.tensor.device
     t_lz = _PhaseTimer()
-    sharded = None
+    comm = None
     if shard is not None and shard is not False:
-        from .distributed import RowShardedFilter
+        from .distributed import RowComm
 
-        group = shard if not isinstance(shard, (bool, int)) else None
-        chunks = shard if isinstance(shard, int) and not isinstance(shard, bool) else 2
-        sharded = RowShardedFilter(op, n, group=group, chunks=chunks, max_cols=blk)
+        if hasattr(shard, "part") and hasattr(shard, "allreduce_"):
+            comm = shard  # a RowComm (or a stand-in with the same interface)
+        else:
+            group = shard if not isinstance(shard, (bool, int)) else None
+            chunks = shard if isinstance(shard, int) and not isinstance(shard, bool) else 2
+            comm = RowComm(n, group=group, chunks=chunks)
+    r0, rows = (comm.part.r0, comm.part.rows) if comm is not None else (0, n)
+    if rows < 1:
+        raise ValueError("every rank needs at least one row of the problem")
 
-    bufs, hp_buf, hp_rot, locked, g_buf, coef, ritz_d, res_d, perm_d = _workspace(dev, n, blk,
+    bufs, hp_buf, hp_rot, locked, g_buf, coef, ritz_d, res_d, perm_d = _workspace(dev, rows, blk,
                                                                                  cfg.nev)
 
     hw = {"setup": time.perf_counter() - t0}
@@ -488,12 +543,13 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     if guess is not None:
         gv = guess.vectors
         shape = tuple(gv.shape)
-        if shape != (n, blk):
+        if shape not in ((n, blk), (rows, blk)):
             raise ValueError(f"guess block must be {n}x{blk}, got {shape}")
         ritz, beta_last, steps = _lanczos_estimates(op, min(10, n), rng)
         b_up = float(ritz[-1] + beta_last)
         window = _safe_window(guess.lambda1, guess.lambda_blk_plus_1, b_up)
-        bufs[0].copy_(to_fblock(gv))
+        gv = to_fblock(gv)
+        bufs[0].copy_(gv if gv.shape[0] == rows else gv[r0:r0 + rows])
     else:
         # The start block is the next draw after the Lanczos vector
         # (chfsi.py:137 then chfsi.py:323): draw q0, then let a host thread
@@ -522,8 +578,9 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
         else:
             a = float(ritz[-1] - 0.10 * (ritz[-1] - ritz[0]))
         window = _safe_window(float(ritz[0]), a, b_up)
-        bufs[0].copy_(to_fblock(torch.from_numpy(box["z"]).pin_memory()))
-        qr_orthonormalize_inplace(bufs[0])
+        start = to_fblock(torch.from_numpy(box["z"]).pin_memory())
+        qr_orthonormalize_inplace(start)  # full block on every rank (replicated)
+        bufs[0].copy_(start if rows == n else start[r0:r0 + rows])
     t_lz.stop()
     report.lanczos_matvecs = steps
     report.matvecs += steps
@@ -542,7 +599,7 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     st.g, st.coef = g_buf.data_ptr(), coef.data_ptr()
     st.ritz_d, st.res_d, st.perm_d = ritz_d.data_ptr(), res_d.data_ptr(), perm_d.data_ptr()
     st.adaptive, st.deg_min = int(cfg.adaptive_degree), int(cfg.min_degree)
-    tail = fblock(n, blk, dev)
+    tail = fblock(rows, blk, dev)
     st.tail = tail.data_ptr()
     st.win_a, st.win_b, st.win_scale_ref = window.a, window.b, window.scale_ref
     st.pb, st.off, st.width = 0, 0, blk
@@ -556,10 +613,15 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     host_degs = np.zeros(blk, dtype=np.int32)
     st.degs = host_degs.ctypes.data_as(pi_)
     st.locked_per_loop = locked_per_loop.ctypes.data_as(pi_)
-    callbacks = _LoopCallbacks(bufs, n, rng, sharded)
+    callbacks = _LoopCallbacks(bufs, rows, rng, comm, op, blk, reduce_bufs=(coef, g_buf, res_d),
+                               hp_buf=hp_buf)
     st.fill = callbacks.fill_cb
-    if sharded is not None:
+    if comm is not None:  # row-sharded loop: local rows + collectives
+        st.row0, st.n_local = r0, rows
         st.filter = callbacks.filter_cb
+        st.allreduce = callbacks.allreduce_cb
+        st.hp_fn = callbacks.hp_cb
+        st.gather = callbacks.gather_cb
     hw["lanczos_start"] = time.perf_counter() - t0 - hw["setup"]
     t_loop = time.perf_counter()
     status = lib().chfsi_solve_loop_z(ctx(), ctypes.byref(st))
@@ -592,6 +654,9 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     if nlocked and not np.array_equal(order, np.arange(nlocked)):
         idx = torch.from_numpy(order).to(dev)
         vecs = vecs.index_select(1, idx)
+    if comm is not None:  # every rank returns the full vectors
+        full = fblock(n, nlocked, dev)
+        vecs = comm.gather_rows(to_fblock(vecs, copy=True), full)
     sol = EigenSolution(values=np.asarray(locked_vals)[order], vectors=to_fblock(vecs, copy=True),
                         form="standard", label=label)
     report.final_residuals = np.asarray(locked_res)[order]

@@ -209,7 +209,7 @@ __global__ void lanczos_advance_kernel(const double2* __restrict__ r, const doub
 __global__ void colnorm_residual_kernel(const double2* __restrict__ hp, long long ldhp,
                                         const double2* __restrict__ p, long long ldp,
                                         const double* __restrict__ lambda, int n,
-                                        double* __restrict__ res) {
+                                        double* __restrict__ res, int squared) {
   __shared__ double sh[32];
   const int j = blockIdx.x;
   const double lam = lambda ? lambda[j] : 0.0;
@@ -226,7 +226,7 @@ __global__ void colnorm_residual_kernel(const double2* __restrict__ hp, long lon
     acc = fma(x.x, x.x, fma(x.y, x.y, acc));
   }
   acc = block_sum(acc, sh);
-  if (threadIdx.x == 0) res[j] = sqrt(acc);
+  if (threadIdx.x == 0) res[j] = squared ? acc : sqrt(acc);
 }
 
 // -------------------------------------------------- Hermitian helpers (K5) ---
@@ -455,10 +455,10 @@ cudaError_t lanczos_advance_launch(const double2* r, const double* beta, double2
 
 cudaError_t colnorm_residual_launch(const double2* hp, long long ldhp, const double2* p,
                                     long long ldp, const double* lambda, int n, int w,
-                                    double* res, cudaStream_t s) {
+                                    double* res, cudaStream_t s, bool squared) {
   if (w <= 0) return cudaSuccess;
   note_launch();
-  colnorm_residual_kernel<<<w, 256, 0, s>>>(hp, ldhp, p, ldp, lambda, n, res);
+  colnorm_residual_kernel<<<w, 256, 0, s>>>(hp, ldhp, p, ldp, lambda, n, res, squared ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -864,6 +864,16 @@ int chfsi_heevd_z(chfsi_ctx* ctx, int n, void* A, long long lda, double* w) {
   return CHFSI_OK;
 }
 
+int chfsi_colnorm_residual_sq_z(chfsi_ctx* ctx, int n, int w, const void* HP, long long ldhp,
+                                const void* P, long long ldp, const double* lambda, double* res) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(HP && res, "NULL argument");
+  CK_CUDA(chfsi::colnorm_residual_launch(static_cast<const double2*>(HP), ldhp,
+                                         static_cast<const double2*>(P), ldp, lambda, n, w, res,
+                                         ctx->stream, true));
+  return CHFSI_OK;
+}
+
 int chfsi_colnorm_residual_z(chfsi_ctx* ctx, int n, int w, const void* HP, long long ldhp,
                              const void* P, long long ldp, const double* lambda, double* res) {
   CK_ARG(ctx, "ctx is NULL");

@@ -101,9 +101,10 @@ cudaError_t lanczos_advance_launch(const double2* r, const double* beta, double2
                                    cudaStream_t s);
 
 // res[j] = || HP[:,j] - lambda[j] P[:,j] ||_2  (col-major, one block per column)
+// (squared: sums of squares, for row-sharded partial norms)
 cudaError_t colnorm_residual_launch(const double2* hp, long long ldhp, const double2* p,
                                     long long ldp, const double* lambda, int n, int w,
-                                    double* res, cudaStream_t s);
+                                    double* res, cudaStream_t s, bool squared = false);
 // res[j] = || X[:,j] ||_2
 cudaError_t colnorm_launch(const double2* x, long long ldx, int n, int w, double* res,
                            cudaStream_t s);

@@ -101,6 +101,113 @@ int rayleigh_ritz(chfsi_ctx* ctx, chfsi_loop* L, const void* q, void* rot_p, int
   return CHFSI_OK;
 }
 
+// ------------------------------------------------ row-sharded (multi-GPU) ---
+// Every n x w block holds this rank's n_local rows (ld n_local). Products
+// that contract over rows leave partial w x w / w-sized results, summed over
+// the ranks by the allreduce callback (NCCL returns identical bytes on all
+// ranks, so the replicated factorizations and decisions stay consistent).
+
+int allreduce(chfsi_loop* L, void* buf, long long count) {
+  if (L->allreduce(L->user, buf, count) != 0) return fail(CHFSI_ENCCL, "allreduce callback failed");
+  return CHFSI_OK;
+}
+
+// diag(A)[0..w) of a device w x w block (ld lda) -> host (real parts), synchronous
+int read_diag_re(chfsi_ctx* ctx, const void* A, long long lda, int w, double* out) {
+  CK(chfsi::ensure_pinned(ctx, (size_t)w * sizeof(double2)));
+  double2* h = static_cast<double2*>(ctx->pinned);
+  CK_CUDA(cudaMemcpy2DAsync(h, sizeof(double2), A, (size_t)(lda + 1) * sizeof(double2),
+                            sizeof(double2), w, cudaMemcpyDeviceToHost, ctx->stream));
+  CK_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < w; ++i) out[i] = h[i].x;
+  return CHFSI_OK;
+}
+
+// Two CGS passes + Cholesky-QR2 on local rows with all-reduced Grams; the
+// rank test and any failure fall back to the full-matrix QR (gather, then
+// chfsi_qr_orthonormalize_z replicated on every rank, local rows kept).
+int orthonormalize_dist(chfsi_ctx* ctx, chfsi_loop* L, void* work, int width) {
+  const int n = L->n, nl = L->n_local, nk = L->nlocked;
+  constexpr int retries = 3;
+  std::vector<int> dead(width);
+  std::vector<double> d0(width), r1(width), r2(width);
+  for (int attempt = 0;; ++attempt) {
+    for (int pass = 0; nk && pass < 2; ++pass) {  // coef = L^H W summed; W -= L coef
+      CK(chfsi_gemm_z(ctx, 'C', 'N', nk, width, nl, 1.0, 0.0, L->locked, nl, work, nl, 0.0, 0.0,
+                      L->coef, nk));
+      CK(allreduce(L, L->coef, 2LL * nk * width));
+      CK(chfsi_gemm_z(ctx, 'N', 'N', nl, width, nk, -1.0, 0.0, L->locked, nl, L->coef, nk, 1.0, 0.0,
+                      work, nl));
+    }
+    // backup for the fallback: hp_rot is free until Rayleigh-Ritz
+    CK_CUDA(cudaMemcpyAsync(L->hp_rot, work, (size_t)nl * width * sizeof(double2),
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+    bool ok = true;
+    double fro2 = 0.0;
+    for (int pass = 0; ok && pass < 2; ++pass) {
+      CK(chfsi_gemm_z(ctx, 'C', 'N', width, width, nl, 1.0, 0.0, work, nl, work, nl, 0.0, 0.0, L->g,
+                      width));
+      CK(allreduce(L, L->g, 2LL * width * width));
+      if (pass == 0) {
+        CK(read_diag_re(ctx, L->g, width, width, d0.data()));
+        for (int i = 0; i < width; ++i) fro2 += d0[i];
+      }
+      int info = 0;
+      const int rc = chfsi_potrf_z(ctx, width, L->g, width, &info);  // G = R^H R, L = R^H
+      if (rc == CHFSI_ENOTPD) {
+        ok = false;
+        break;
+      }
+      CK(rc);
+      CK(read_diag_re(ctx, L->g, width, width, pass == 0 ? r1.data() : r2.data()));
+      CK(chfsi_trsm_z(ctx, 'R', 'C', nl, width, L->g, width, work, nl));  // W <- W R^-1
+    }
+    if (ok) {  // same acceptance as chfsi_qr_orthonormalize_z's Cholesky-QR2
+      const double fro = std::sqrt(fro2), safe = 1e-11 * fro;
+      for (int i = 0; ok && i < width; ++i)
+        ok = std::isfinite(fro) && r1[i] * r2[i] >= safe && std::fabs(r2[i] - 1.0) <= 1e-6;
+      if (ok) return CHFSI_OK;
+    }
+    // fallback: the full-matrix QR, replicated
+    CK_CUDA(cudaMemcpyAsync(work, L->hp_rot, (size_t)nl * width * sizeof(double2),
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+    void* fullp = nullptr;
+    if (!L->gather || L->gather(L->user, work, nl, width, &fullp) != 0 || !fullp)
+      return fail(CHFSI_EINVAL, "gather callback failed");
+    int ndead = 0;
+    const int rc = chfsi_qr_orthonormalize_z(ctx, n, width, fullp, n, dead.data(), &ndead);
+    if (rc == CHFSI_OK) {
+      CK_CUDA(cudaMemcpy2DAsync(work, (size_t)nl * sizeof(double2),
+                                static_cast<double2*>(fullp) + L->row0, (size_t)n * sizeof(double2),
+                                (size_t)nl * sizeof(double2), width, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+      return CHFSI_OK;
+    }
+    if (rc != CHFSI_ERANK) return rc;
+    if (attempt == retries || !L->fill) return rc;
+    if (L->fill(L->user, work, nl, nl, dead.data(), ndead) != 0)
+      return fail(CHFSI_EINVAL, "rank-repair fill callback failed");
+  }
+}
+
+// Rayleigh-Ritz on local rows: HP from the hp callback, G = P^H HP summed,
+// replicated eigensolver, local rotations, residual squares summed.
+int rayleigh_ritz_dist(chfsi_ctx* ctx, chfsi_loop* L, const void* q, void* rot_p, int width,
+                       double eig_tol, int* used_fast) {
+  const int nl = L->n_local;
+  if (L->hp_fn(L->user, q, L->hp, nl, width) != 0) return fail(CHFSI_EINVAL, "hp callback failed");
+  CK(chfsi_gemm_z(ctx, 'C', 'N', width, width, nl, 1.0, 0.0, q, nl, L->hp, nl, 0.0, 0.0, L->g, width));
+  CK(allreduce(L, L->g, 2LL * width * width));
+  CK(chfsi_symmetrize_z(ctx, width, L->g, width));
+  CK(chfsi_heev_rr_z(ctx, width, L->g, width, L->ritz_d, eig_tol, used_fast));
+  CK(chfsi_gemm_z(ctx, 'N', 'N', nl, width, width, 1.0, 0.0, q, nl, L->g, width, 0.0, 0.0, rot_p, nl));
+  CK(chfsi_gemm_z(ctx, 'N', 'N', nl, width, width, 1.0, 0.0, L->hp, nl, L->g, width, 0.0, 0.0,
+                  L->hp_rot, nl));
+  CK(chfsi_colnorm_residual_sq_z(ctx, nl, width, L->hp_rot, nl, rot_p, nl, L->ritz_d, L->res_d));
+  CK(allreduce(L, L->res_d, width));
+  return CHFSI_OK;
+}
+
 }  // namespace
 
 extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
@@ -114,10 +221,15 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
          "NULL host output");
   CK_ARG(L->pb == 0 || L->pb == 1, "bad panel buffer index");
   CK_ARG(L->off >= 0 && L->width >= 1 && L->off + L->width <= L->blk, "bad panel window");
+  const bool dist = L->allreduce != nullptr;
+  CK_ARG(!dist || (L->hp_fn && L->filter && L->n_local >= 1 && L->row0 >= 0 &&
+                   L->row0 + L->n_local <= L->n),
+         "row-sharded loop needs filter and hp callbacks and a valid row range");
   CK(ensure_events(ctx));
   cudaStream_t s = ctx->stream;
   cudaEvent_t* ev = ctx->loop_ev;
   const int n = L->n;
+  const int nl = dist ? L->n_local : n;  // rows (and ld) of every n x w block here
   CK_ARG(!L->adaptive || (L->degs && L->perm_d && 1 <= L->deg_min && L->deg_min <= L->deg),
          "adaptive degree needs degs, perm_d and 1 <= deg_min <= deg");
   // pinned staging: [ritz | res] readback, then the adaptive column order
@@ -128,7 +240,7 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
   while (L->inner_loops < L->max_repeats) {
     L->inner_loops += 1;
     const int width = L->width;
-    void* panel = col(L->bufs[L->pb], n, L->off);
+    void* panel = col(L->bufs[L->pb], nl, L->off);
     void* other = L->bufs[1 - L->pb];
 
     // ---- filter (chfsi.py:331-334)
@@ -136,7 +248,7 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
     void* result = nullptr;
     const int* degs = have_degs ? L->degs : nullptr;  // adaptive: sorted per-column degrees
     if (L->filter) {
-      if (L->filter(L->user, panel, other, n, width, L->deg, degs, L->win_a, L->win_b,
+      if (L->filter(L->user, panel, other, nl, width, L->deg, degs, L->win_a, L->win_b,
                     L->win_scale_ref, &result) != 0 || !result)
         return fail(CHFSI_EINVAL, "filter callback failed");
     } else if (degs) {
@@ -160,7 +272,7 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
     const bool q_in_other = result == other;
 
     // ---- orthonormalize (chfsi.py:335-336)
-    CK(orthonormalize(ctx, L, result, width));
+    CK(dist ? orthonormalize_dist(ctx, L, result, width) : orthonormalize(ctx, L, result, width));
     CK_CUDA(cudaEventRecord(ev[2], s));
 
     // ---- Rayleigh-Ritz into the buffer the filter left free (chfsi.py:337-350)
@@ -171,7 +283,8 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
     // zheevd runs instead (measured: 4 zheevd calls less per warm C2 problem).
     const double eig_tol = L->rr_fast_tol > 0.0 ? L->rr_fast_tol : 0.0;
     int used_fast = 0;
-    CK(rayleigh_ritz(ctx, L, result, rot_p, width, eig_tol, &used_fast));
+    CK(dist ? rayleigh_ritz_dist(ctx, L, result, rot_p, width, eig_tol, &used_fast)
+            : rayleigh_ritz(ctx, L, result, rot_p, width, eig_tol, &used_fast));
     CK_CUDA(cudaEventRecord(ev[3], s));
     L->rr_fast_eigs += used_fast;
     L->residual_check_matvecs += width;
@@ -184,6 +297,8 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
     L->t_filter += 1e-3 * elapsed(ev[0], ev[1]);
     L->t_ortho += 1e-3 * elapsed(ev[1], ev[2]);
     L->t_rr += 1e-3 * elapsed(ev[2], ev[3]);
+    if (dist)  // summed squares of the local row norms
+      for (int j = 0; j < width; ++j) host[width + j] = std::sqrt(host[width + j]);
     const double* ritz = host;
     const double* res = host + width;
     for (int j = 0; j < width; ++j) {
@@ -199,8 +314,8 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
         L->locked_vals[L->nlocked + j] = ritz[j];
         L->locked_res[L->nlocked + j] = res[j];
       }
-      CK_CUDA(cudaMemcpyAsync(col(L->locked, n, L->nlocked), rot_p,
-                              (size_t)n * n_lock * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+      CK_CUDA(cudaMemcpyAsync(col(L->locked, nl, L->nlocked), rot_p,
+                              (size_t)nl * n_lock * sizeof(double2), cudaMemcpyDeviceToDevice, s));
       L->nlocked += n_lock;
     }
     L->locked_per_loop[L->inner_loops - 1] = n_lock;
@@ -240,8 +355,8 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
         int* hperm = reinterpret_cast<int*>(static_cast<double*>(ctx->pinned) + 2 * (size_t)L->blk);
         for (int i = 0; i < wn; ++i) hperm[i] = order[i];
         CK_CUDA(cudaMemcpyAsync(L->perm_d, hperm, (size_t)wn * sizeof(int), cudaMemcpyHostToDevice, s));
-        CK_CUDA(chfsi::nd_gather_cols_launch(col(L->bufs[L->pb], n, L->off), n, n, wn, L->perm_d,
-                                             static_cast<double2*>(L->bufs[1 - L->pb]), n, s));
+        CK_CUDA(chfsi::nd_gather_cols_launch(col(L->bufs[L->pb], nl, L->off), nl, nl, wn, L->perm_d,
+                                             static_cast<double2*>(L->bufs[1 - L->pb]), nl, s));
         L->pb = 1 - L->pb;
         L->off = 0;
       }
@@ -250,13 +365,14 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
   }
   // chained-mode tail: [locked | unlocked remainder of the final panel]
   if (L->tail && L->inner_loops > 0) {
-    const size_t col_bytes = (size_t)n * sizeof(double2);
+    const size_t col_bytes = (size_t)nl * sizeof(double2);
     if (L->nlocked)
       CK_CUDA(cudaMemcpyAsync(L->tail, L->locked, col_bytes * L->nlocked, cudaMemcpyDeviceToDevice, s));
     const int rest = L->last_width - L->last_nlock;
     if (rest > 0)
-      CK_CUDA(cudaMemcpyAsync(col(L->tail, n, L->nlocked), col(L->bufs[L->last_rot_pb], n, L->last_nlock),
-                              col_bytes * rest, cudaMemcpyDeviceToDevice, s));
+      CK_CUDA(cudaMemcpyAsync(col(L->tail, nl, L->nlocked),
+                              col(L->bufs[L->last_rot_pb], nl, L->last_nlock), col_bytes * rest,
+                              cudaMemcpyDeviceToDevice, s));
   }
   return CHFSI_OK;
 }

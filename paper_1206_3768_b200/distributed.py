@@ -304,3 +304,70 @@ class RowShardedFilter:
         for g, (j0, j1, _) in enumerate(groups):
             from_blocked(part, pairs[g][cur[g]], out[:, j0:j1])
         return out
+
+
+# ------------------------------------------------------ row-sharded loop ---
+
+class RowComm:
+    """Collectives of the row-sharded ChFSI loop (chfsi_solve(shard=...)):
+    every n x w block lives as this rank's rows; products over rows are
+    summed with `allreduce_`, panels are made whole with `gather_rows` for
+    the filter and H*P (both run as row-sharded K1 steps). NCCL over
+    torch.distributed by default; `tests/test_gpu_distributed.py` drives the
+    same interface with host-mediated collectives among threads."""
+
+    def __init__(self, n, group=None, chunks=2):
+        self.group = group
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.part = RowPartition(n, world, rank)
+        self.chunks = chunks
+        self._filters = {}
+
+    # -- collectives
+    def allreduce_(self, t):
+        """In-place sum over the ranks (identical bytes everywhere)."""
+        if self.part.world > 1:
+            dist.all_reduce(t, group=self.group)
+
+    def gather_blocked(self, local, blocked):
+        """Local rows (nl x w F-block) -> full rank-blocked buffer on every rank."""
+        part = self.part
+        if part.rows:
+            blocked[part.rank, :, :part.rows].copy_(local.t())
+        nccl_allgather(blocked, part, self.group)
+        return blocked
+
+    def gather_rows(self, local, full):
+        """Local rows -> full n x w F-block on every rank."""
+        w = local.shape[1]
+        blocked = self.gather_blocked(local, blocked_empty(self.part, w, local.device))
+        return from_blocked(self.part, blocked, full)
+
+    # -- sharded operators
+    def filter(self, op, blk):
+        key = (id(op.tensor), op.tensor.data_ptr(), blk)
+        f = self._filters.get(key)
+        if f is None:
+            f = self._filters[key] = RowShardedFilter(op, self.part.n, group=self.group,
+                                                      chunks=self.chunks, max_cols=blk)
+        return f
+
+    def filter_local(self, op, blk, panel_local, deg, window, out_local):
+        """Filter the distributed panel; this rank's rows of the result."""
+        n, w = self.part.n, panel_local.shape[1]
+        full = torch.empty((w, n), dtype=panel_local.dtype, device=panel_local.device).t()
+        self.gather_rows(panel_local, full)
+        res = self.filter(op, blk).apply(full, deg, window)
+        part = self.part
+        out_local.copy_(res[part.r0:part.r0 + part.rows])
+        return out_local
+
+    def hp_local(self, op, panel_local, out_local):
+        """This rank's rows of H * P (one row-sharded K1 product step)."""
+        part, w = self.part, panel_local.shape[1]
+        blocked = self.gather_blocked(panel_local, blocked_empty(part, w, panel_local.device))
+        slab = torch.empty((w, part.kblk), dtype=panel_local.dtype, device=panel_local.device)
+        gpu_row_step(op, part, blocked, None, slab, w, 1.0, 0.0, 0.0)
+        out_local.copy_(slab[:, :part.rows].t())
+        return out_local
