@@ -319,6 +319,22 @@ typedef struct chfsi_loop {
 
 CHFSI_API int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* loop);
 
+/* Row-sharded Lanczos bound (multi-GPU, chfsi.py:125-162): this rank holds
+ * rows row0 .. row0+n_local-1 of H (H_rows, row-major rows, conj_h as for
+ * K1) and of the n x k basis (V_local, ld n_local); q0 is the full start
+ * vector (replicated). Per step: GEMV on local rows against the gathered
+ * vector, partial alpha / reorthogonalisation / norm sums completed by
+ * `allreduce` (in place, stream-ordered), the next vector gathered with
+ * `gather` (width 1). ws: chfsi_lanczos_rows_ws_bytes(n_local, k) device
+ * bytes owned by the caller (the allreduce callback receives pointers into
+ * it). Outputs as chfsi_lanczos_z, identical on every rank. */
+CHFSI_API long long chfsi_lanczos_rows_ws_bytes(int n_local, int k);
+CHFSI_API int chfsi_lanczos_rows_z(chfsi_ctx* ctx, int n, int k, const void* H_rows, long long ldh,
+                                   int conj_h, int row0, int n_local, const void* q0, void* V_local,
+                                   void* ws, chfsi_allreduce_cb allreduce, chfsi_gather_cb gather,
+                                   void* user, double* alphas, double* betas, double* beta_last,
+                                   int* steps);
+
 #ifdef __cplusplus
 }
 #endif

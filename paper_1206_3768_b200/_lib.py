@@ -128,8 +128,12 @@ class LoopState(ctypes.Structure):
 
 
 _SIGNATURES["chfsi_solve_loop_z"] = [_vp, ctypes.POINTER(LoopState)]
+_SIGNATURES["chfsi_lanczos_rows_ws_bytes"] = [_i, _i]
+_SIGNATURES["chfsi_lanczos_rows_z"] = [_vp, _i, _i, _vp, _ll, _i, _i, _i, _vp, _vp, _vp, ALLREDUCE_CB,
+                                       GATHER_CB, _vp, _pd, _pd, _pd, _pi]
 
-_RESTYPES = {"chfsi_last_error": ctypes.c_char_p, "chfsi_launch_count": ctypes.c_longlong}
+_RESTYPES = {"chfsi_last_error": ctypes.c_char_p, "chfsi_launch_count": ctypes.c_longlong,
+             "chfsi_lanczos_rows_ws_bytes": ctypes.c_longlong}
 
 
 def symbols():

@@ -208,14 +208,22 @@ def _draw_start_vector(rng, n):
     return rng.standard_normal(n) + 1j * rng.standard_normal(n)  # chfsi.py:137 draw order
 
 
-def _lanczos_estimates(op, k, rng, q0=None):
+def _lanczos_estimates(op, k, rng, q0=None, comm=None):
     """k-step Lanczos with full reorthogonalization on the device
     (chfsi.py:125-162). Returns (ritz, beta_last, steps). ``q0``: the start
-    vector when the caller already drew it."""
+    vector when the caller already drew it; ``comm``: row-sharded over the
+    ranks of a RowComm (same result on every rank)."""
     n = op.n
     k = min(k, n)
     if q0 is None:
         q0 = _draw_start_vector(rng, n)
+    if comm is not None and comm.part.world > 1:
+        from .distributed import lanczos_rows
+
+        alphas, betas, beta_last, s = lanczos_rows(comm, op, k, q0)
+        ritz = alphas[:1].copy() if s == 1 else scipy.linalg.eigvalsh_tridiagonal(alphas[:s],
+                                                                                  betas[: s - 1])
+        return ritz, beta_last, s
     q0d = torch.from_numpy(q0).to(op.tensor.device)
     basis = fblock(n, k)
     alphas = np.zeros(k)
@@ -545,7 +553,7 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
         shape = tuple(gv.shape)
         if shape not in ((n, blk), (rows, blk)):
             raise ValueError(f"guess block must be {n}x{blk}, got {shape}")
-        ritz, beta_last, steps = _lanczos_estimates(op, min(10, n), rng)
+        ritz, beta_last, steps = _lanczos_estimates(op, min(10, n), rng, comm=comm)
         b_up = float(ritz[-1] + beta_last)
         window = _safe_window(guess.lambda1, guess.lambda_blk_plus_1, b_up)
         gv = to_fblock(gv)
@@ -567,7 +575,7 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
         th = threading.Thread(target=draw, daemon=True)
         th.start()
         try:
-            ritz, beta_last, steps = _lanczos_estimates(op, lancz_k, rng, q0=q0)
+            ritz, beta_last, steps = _lanczos_estimates(op, lancz_k, rng, q0=q0, comm=comm)
         finally:
             th.join()
         if "err" in box:

@@ -63,11 +63,11 @@ __device__ __forceinline__ bool is_done(const int* done) { return done != nullpt
 template <bool CONJ>
 __global__ void gemv_rows_kernel(const double2* __restrict__ h, long long ldh,
                                  const double2* __restrict__ q, double2* __restrict__ u, int n,
-                                 const int* done) {
+                                 int rows, const int* done) {
   if (is_done(done)) return;
   const int lane = threadIdx.x & 31;
   const int warps = (blockDim.x >> 5) * gridDim.x;
-  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n; row += warps) {
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += warps) {
     const double2* hr = h + (long long)row * ldh;
     double sr = 0.0, si = 0.0;
     int k = lane;
@@ -126,8 +126,10 @@ __global__ void reduce_final_kernel(const double* __restrict__ partial, int np, 
   double acc = 0.0;
   for (int i = threadIdx.x; i < np; i += blockDim.x) acc += partial[i];
   acc = block_sum(acc, sh);
-  if (threadIdx.x == 0) *out = OP == 1 ? sqrt(acc) : acc;
+  if (threadIdx.x == 0) *out = OP == 1 ? sqrt(acc) : acc;  // OP 2: sum of squares
 }
+
+__global__ void sqrt_scalar_kernel(double* x) { *x = sqrt(*x); }
 
 // out[j] = V[:,j]^H r, one block per column
 __global__ void colsdot_kernel(const double2* __restrict__ v, long long ldv, int n,
@@ -393,12 +395,13 @@ inline int grid_for(long long total, int threads, int cap = kNumSMs * 16) {
 }  // namespace
 
 cudaError_t gemv_rows_launch(const double2* h, long long ldh, bool conj_h, const double2* q,
-                             double2* u, int n, const int* done, cudaStream_t s) {
+                             double2* u, int n, const int* done, cudaStream_t s, int rows) {
+  if (rows < 0) rows = n;
   const int threads = 256;
-  const int blocks = grid_for((long long)n * 32, threads, kNumSMs * 8);
+  const int blocks = grid_for((long long)rows * 32, threads, kNumSMs * 8);
   note_launch();
-  if (conj_h) gemv_rows_kernel<true><<<blocks, threads, 0, s>>>(h, ldh, q, u, n, done);
-  else gemv_rows_kernel<false><<<blocks, threads, 0, s>>>(h, ldh, q, u, n, done);
+  if (conj_h) gemv_rows_kernel<true><<<blocks, threads, 0, s>>>(h, ldh, q, u, n, rows, done);
+  else gemv_rows_kernel<false><<<blocks, threads, 0, s>>>(h, ldh, q, u, n, rows, done);
   return cudaGetLastError();
 }
 
@@ -417,6 +420,21 @@ cudaError_t norm2_launch(const double2* x, long long n, double* partial, double*
   reduce_partial_kernel<1><<<kRedBlocks, kRedThreads, 0, s>>>(x, nullptr, n, partial, done);
   note_launch();
   reduce_final_kernel<1><<<1, 1024, 0, s>>>(partial, kRedBlocks, out, done);
+  return cudaGetLastError();
+}
+
+cudaError_t norm2sq_launch(const double2* x, long long n, double* partial, double* out,
+                           const int* done, cudaStream_t s) {
+  note_launch();
+  reduce_partial_kernel<1><<<kRedBlocks, kRedThreads, 0, s>>>(x, nullptr, n, partial, done);
+  note_launch();
+  reduce_final_kernel<2><<<1, 1024, 0, s>>>(partial, kRedBlocks, out, done);
+  return cudaGetLastError();
+}
+
+cudaError_t sqrt_scalar_launch(double* x, cudaStream_t s) {
+  note_launch();
+  sqrt_scalar_kernel<<<1, 1, 0, s>>>(x);
   return cudaGetLastError();
 }
 

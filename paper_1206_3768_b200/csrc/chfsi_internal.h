@@ -65,7 +65,11 @@ cudaError_t cheb_step_rows_launch(const double2* h, long long ldh, bool conj_h, 
 // ---- auxiliary kernels (aux_kernels.cu) ----
 // u = op(H) q for a row-major H (conj_h: conj(H)).
 cudaError_t gemv_rows_launch(const double2* h, long long ldh, bool conj_h, const double2* q,
-                             double2* u, int n, const int* done, cudaStream_t s);
+                             double2* u, int n, const int* done, cudaStream_t s, int rows = -1);
+// ||x||^2 (no square root) and x <- sqrt(x) on one device scalar
+cudaError_t norm2sq_launch(const double2* x, long long n, double* partial, double* out,
+                           const int* done, cudaStream_t s);
+cudaError_t sqrt_scalar_launch(double* x, cudaStream_t s);
 // Deterministic reductions. partial buffers must hold kRedBlocks entries.
 constexpr int kRedBlocks = 296;
 constexpr int kRedThreads = 256;

@@ -376,3 +376,81 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
   }
   return CHFSI_OK;
 }
+
+// ------------------------------------------------------ row-sharded Lanczos ---
+// The k-step Lanczos chain (chfsi.py:125-162) with H, the basis and every
+// n-vector split by rows: per step the GEMV runs on this rank's rows of H
+// against the gathered full vector, and alpha, the reorthogonalisation
+// coefficients and ||r||^2 are partial sums completed by the allreduce
+// callback. The multi-kernel path of chfsi_lanczos_z on local rows, with the
+// same breakdown rule (device flag; every rank sees the same beta).
+
+extern "C" long long chfsi_lanczos_rows_ws_bytes(int n_local, int k) {
+  // u, r (n_local each), coef (k complex), alphas, betas (k), nrm (1), padding
+  return 2LL * n_local * sizeof(double2) + (long long)k * sizeof(double2) +
+         (2LL * k + 8) * sizeof(double) + 256;
+}
+
+extern "C" int chfsi_lanczos_rows_z(chfsi_ctx* ctx, int n, int k, const void* H_rows, long long ldh,
+                                    int conj_h, int row0, int n_local, const void* q0, void* V_local,
+                                    void* ws, chfsi_allreduce_cb allreduce_fn, chfsi_gather_cb gather_fn,
+                                    void* user, double* alphas, double* betas, double* beta_last,
+                                    int* steps) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(n >= 1 && k >= 1 && k <= n, "need 1 <= k <= n");
+  CK_ARG(n_local >= 1 && row0 >= 0 && row0 + n_local <= n, "bad row range");
+  CK_ARG(H_rows && q0 && V_local && ws && allreduce_fn && gather_fn && alphas && betas && beta_last &&
+             steps,
+         "NULL argument");
+  cudaStream_t s = ctx->stream;
+  const int nl = n_local;
+  char* base = static_cast<char*>(ws);
+  double2* u = reinterpret_cast<double2*>(base);
+  double2* r = u + nl;
+  double2* coef = r + nl;
+  double* al_d = reinterpret_cast<double*>(coef + k);
+  double* be_d = al_d + k;
+  double* nrm = be_d + k;
+  double2* V = static_cast<double2*>(V_local);
+  const double2* hh = static_cast<const double2*>(H_rows);
+  chfsi::LanczosState* st = ctx->lstate;
+  const int* done = &st->done;
+  auto reduce = [&](void* buf, long long count) -> int {
+    if (allreduce_fn(user, buf, count) != 0) return fail(CHFSI_ENCCL, "allreduce callback failed");
+    return CHFSI_OK;
+  };
+  CK_CUDA(cudaMemsetAsync(st, 0, sizeof(chfsi::LanczosState), s));
+  CK_CUDA(cudaMemsetAsync(be_d, 0, (size_t)k * sizeof(double), s));
+  // q = q0 / ||q0|| on the full (replicated) vector, then this rank's rows
+  CK_CUDA(chfsi::norm2_launch(static_cast<const double2*>(q0), n, ctx->partial, nrm, nullptr, s));
+  CK_CUDA(chfsi::div_scalar_launch(static_cast<const double2*>(q0) + row0, nrm, V, nl, s));
+  void* qfull = nullptr;
+  if (gather_fn(user, V, nl, 1, &qfull) != 0 || !qfull) return fail(CHFSI_EINVAL, "gather failed");
+  for (int i = 0; i < k; ++i) {
+    const double2* q = V + (long long)i * nl;
+    CK_CUDA(chfsi::gemv_rows_launch(hh, ldh, conj_h != 0, static_cast<const double2*>(qfull), u, n, done,
+                                    s, nl));
+    CK_CUDA(chfsi::dot_re_launch(q, u, nl, ctx->partial, al_d + i, done, s));
+    CK(reduce(al_d + i, 1));
+    CK_CUDA(chfsi::lanczos_residual_launch(u, q, i ? V + (long long)(i - 1) * nl : nullptr, al_d + i,
+                                           i ? be_d + i - 1 : nullptr, r, nl, done, s));
+    CK_CUDA(chfsi::colsdot_launch(V, nl, nl, i + 1, r, coef, done, s));
+    CK(reduce(coef, 2LL * (i + 1)));
+    CK_CUDA(chfsi::sub_vcoef_launch(V, nl, nl, i + 1, coef, r, done, s));
+    CK_CUDA(chfsi::norm2sq_launch(r, nl, ctx->partial, nrm, done, s));
+    CK(reduce(nrm, 1));
+    CK_CUDA(chfsi::sqrt_scalar_launch(nrm, s));
+    double2* qn = i + 1 < k ? V + (long long)(i + 1) * nl : nullptr;
+    CK_CUDA(chfsi::lanczos_advance_launch(r, nrm, qn, be_d + i, st, i, k, nl, s));
+    if (qn && (gather_fn(user, qn, nl, 1, &qfull) != 0 || !qfull))
+      return fail(CHFSI_EINVAL, "gather failed");
+  }
+  chfsi::LanczosState hst;
+  CK_CUDA(cudaMemcpyAsync(&hst, st, sizeof(hst), cudaMemcpyDeviceToHost, s));
+  CK_CUDA(cudaMemcpyAsync(alphas, al_d, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK_CUDA(cudaMemcpyAsync(betas, be_d, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK_CUDA(cudaStreamSynchronize(s));
+  *steps = hst.steps;
+  *beta_last = hst.beta_last;
+  return CHFSI_OK;
+}

@@ -371,3 +371,62 @@ class RowComm:
         gpu_row_step(op, part, blocked, None, slab, w, 1.0, 0.0, 0.0)
         out_local.copy_(slab[:, :part.rows].t())
         return out_local
+
+
+def lanczos_rows(comm, op, k, q0):
+    """Row-sharded k-step Lanczos (chfsi.py:125-162) over `comm` (a RowComm
+    or a stand-in): returns (alphas, betas, beta_last, steps) on the host,
+    identical on every rank. q0: the full start vector (numpy, replicated)."""
+    import ctypes
+
+    import scipy.linalg  # noqa: F401  (the caller evaluates the tridiagonal)
+
+    from ._device import fblock
+
+    part = comm.part
+    n, nl = part.n, part.rows
+    dev = op.tensor.device
+    k = min(k, n)
+    nbytes = int(lib().chfsi_lanczos_rows_ws_bytes(nl, k))
+    ws = torch.zeros((nbytes + 7) // 8, dtype=torch.float64, device=dev)
+    basis = fblock(nl, k, dev)
+    qfull = torch.empty((1, n), dtype=torch.complex128, device=dev).t()
+    q0d = torch.from_numpy(np.ascontiguousarray(q0)).to(dev)
+    err = []
+
+    def allreduce(user, buf, count):
+        try:
+            off = (buf - ws.data_ptr()) // 8
+            if not (0 <= off and off + count <= ws.numel() and ws.data_ptr() + 8 * off == buf):
+                raise ValueError("allreduce pointer outside the Lanczos workspace")
+            comm.allreduce_(ws[off:off + count])
+            return 0
+        except BaseException as exc:  # noqa: BLE001
+            err.append(exc)
+            return -1
+
+    def gather(user, local, ld, width, out):
+        try:
+            j = (local - basis.data_ptr()) // (16 * nl)
+            comm.gather_rows(basis[:, j:j + 1], qfull)
+            out[0] = qfull.data_ptr()
+            return 0
+        except BaseException as exc:  # noqa: BLE001
+            err.append(exc)
+            return -1
+
+    from ._lib import ALLREDUCE_CB, GATHER_CB
+
+    cb_ar, cb_g = ALLREDUCE_CB(allreduce), GATHER_CB(gather)
+    alphas, betas = np.zeros(k), np.zeros(k)
+    beta_last, steps = ctypes.c_double(), ctypes.c_int()
+    pd = ctypes.POINTER(ctypes.c_double)
+    h_rows = ctypes.c_void_p(op.tensor.data_ptr() + part.r0 * op.ld * 16)
+    status = lib().chfsi_lanczos_rows_z(ctx(), n, k, h_rows, op.ld, op.conj, part.r0, nl,
+                                        dptr(q0d), dptr(basis), dptr(ws), cb_ar, cb_g, None,
+                                        alphas.ctypes.data_as(pd), betas.ctypes.data_as(pd),
+                                        ctypes.byref(beta_last), ctypes.byref(steps))
+    if err:
+        raise err[0]
+    check(status, "lanczos (row-sharded)")
+    return alphas, betas, beta_last.value, steps.value
