@@ -34,10 +34,8 @@ import json
 import os
 import statistics
 import sys
-import threading
 import time
 
-import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:

@@ -16,7 +16,6 @@ import math
 from dataclasses import dataclass, field, replace
 
 import numpy as np
-import torch
 
 from ._device import fblock, ld_of, to_fblock
 from ._lib import check, ctx, dptr, lib

@@ -29,7 +29,7 @@ import numpy as np
 import scipy.linalg
 import torch
 
-from ._device import C128, Operator, fblock, ld_of, to_fblock
+from ._device import Operator, fblock, ld_of, to_fblock
 from ._lib import ALLREDUCE_CB, FILL_CB, FILTER_CB, GATHER_CB, HP_CB, LoopState, check, ctx, dptr, lib
 from .linalg import qr_orthonormalize_inplace
 from .reduction import EigenSolution

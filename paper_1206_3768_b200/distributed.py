@@ -379,8 +379,6 @@ def lanczos_rows(comm, op, k, q0):
     identical on every rank. q0: the full start vector (numpy, replicated)."""
     import ctypes
 
-    import scipy.linalg  # noqa: F401  (the caller evaluates the tridiagonal)
-
     from ._device import fblock
 
     part = comm.part

@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import C128, Operator, fblock, ld_of, to_device_matrix, to_fblock
+from ._device import Operator, fblock, ld_of, to_device_matrix, to_fblock
 from ._lib import check, ctx, dptr, lib
 from .linalg_errors import (
     EigenSolverError,

@@ -16,7 +16,7 @@ import torch
 
 from oracle import chfsi_oracle as orc
 from tests.conftest import subspace_sines
-from tests.golden.recipes import SOLVE_CASES, build_solve_case, random_hermitian, sha
+from tests.golden.recipes import SOLVE_CASES, build_solve_case, random_hermitian
 
 pytestmark = pytest.mark.gpu
 
@@ -297,3 +297,21 @@ def test_sequence_driver_raises_reference_errors_for_staged_problems(pkg):
     # and a clean sequence afterwards still solves
     res = pkg.solve_sequence(seq, cfg)
     assert all(r.report.converged for r in res)
+
+
+def test_c2_chained_sequence_bitwise_reproducible(pkg):
+    """The whole chained C2 sequence (cold start, 9 warm starts, two-chain
+    filter, stream-K folds, adaptive Rayleigh-Ritz, Cholesky-QR2, staging
+    on the side stream) is bitwise identical run to run (reference
+    test_chfsi.py:234-241 asks it of one solve)."""
+    cfg_b = pkg.BASELINE_CONFIGS["C2"]
+    cfg = pkg.ChfsiConfig(nev=cfg_b.nev, nex=cfg_b.nex, deg=cfg_b.deg, tol=cfg_b.tol)
+    seq = list(pkg.iter_baseline_sequence(cfg_b.n, 4, seed=0))
+    dev = torch.device("cuda", 0)
+    pencils = [pkg.EigenPencil(a=torch.from_numpy(a).to(dev), b=torch.from_numpy(b).to(dev),
+                               label=lab) for lab, a, b in seq]
+    runs = [pkg.solve_sequence(pencils, cfg, seed=0) for _ in range(2)]
+    for r1, r2 in zip(*runs):
+        assert r1.report.locked_per_loop == r2.report.locked_per_loop
+        assert np.array_equal(r1.values, r2.values)
+        assert torch.equal(r1.solution.vectors, r2.solution.vectors)

@@ -7,8 +7,7 @@ import pytest
 import scipy.io
 
 from paper_1206_3768_b200.analysis import greedy_match
-from paper_1206_3768_b200.pencil_io import (FormatError, iter_sequence, load_sequence,
-                                            read_pencil, save_sequence)
+from paper_1206_3768_b200.pencil_io import FormatError, load_sequence, read_pencil, save_sequence
 from paper_1206_3768_b200.sequence import iter_baseline_sequence
 from tests.golden.recipes import random_hermitian, random_spd
 
