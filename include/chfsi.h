@@ -65,6 +65,9 @@ CHFSI_API int chfsi_ctx_set_tiling(chfsi_ctx* ctx, int bm, int bn, int grid);
 /* With a forced tiling: groups = 2 selects the one-CTA-per-SM K1 whose two
  * 8-warp groups take alternate k-slabs of the same tile (64x16, 64x32). */
 CHFSI_API int chfsi_ctx_set_step_groups(chfsi_ctx* ctx, int groups);
+/* With a forced tiling: warps per tile group (4, 8 or 16; 0 = the default
+ * variant of that tiling). A combination without a kernel fails at launch. */
+CHFSI_API int chfsi_ctx_set_step_warps(chfsi_ctx* ctx, int warps);
 /* Filter launch chains (default 2): with 2, chfsi_filter_z runs balanced
  * column halves as two concurrent launch chains (the context's stream and an
  * internal one, joined before returning) when the automatic tiling allows;
@@ -137,6 +140,14 @@ CHFSI_API int chfsi_debug_k1_trace(unsigned long long* host, int max_ctas);
 
 /* Introspection of the K1 tile choice for an (n, w) step. */
 CHFSI_API int chfsi_step_tiling(int n, int w, int* bm, int* bn, int* split);
+
+/* Complex-product formulation of K1 (process-wide; default 3 unless the
+ * environment sets CHFSI_K1_PRODUCT=4): 3 = Gauss/3M, three real FP64 MMAs
+ * per complex block (Cr = T1 - T2, Ci = T3 - T1 - T2), 4 = four real MMAs.
+ * Both round like a complex GEMM to O(u) normwise; the 8-flop-per-complex-MAC
+ * count of the metric is unchanged. Returns the previous setting (3 or 4),
+ * or CHFSI_EINVAL; product = 0 only queries. */
+CHFSI_API int chfsi_set_complex_product(int product);
 
 /* ---------------------------------------------------------------- K2 ---
  * k-step Lanczos with full reorthogonalization (chfsi.py:125-162): q0 is

@@ -60,6 +60,7 @@ _SIGNATURES = {
     "chfsi_ctx_set_stream": [_vp, _vp],
     "chfsi_ctx_set_tiling": [_vp, _i, _i, _i],
     "chfsi_ctx_set_step_groups": [_vp, _i],
+    "chfsi_ctx_set_step_warps": [_vp, _i],
     "chfsi_ctx_set_filter_chains": [_vp, _i],
     "chfsi_cheb_step_z": [_vp, _i, _i, _vp, _ll, _i, _vp, _ll, _vp, _ll, _vp, _ll, _d, _d, _d],
     "chfsi_cheb_step_rows_z": [_vp, _i, _i, _i, _vp, _ll, _i, _vp, _ll, _i, _i, _vp, _ll, _vp, _ll,
@@ -72,6 +73,7 @@ _SIGNATURES = {
     "chfsi_filter_degrees_z": [_vp, _i, _i, _vp, _ll, _i, _vp, _ll, _vp, _vp, _ll, _pi, _d, _d, _d,
                                ctypes.POINTER(_vp)],
     "chfsi_step_tiling": [_i, _i, _pi, _pi, _pi],
+    "chfsi_set_complex_product": [_i],
     "chfsi_debug_k1_trace": [ctypes.POINTER(ctypes.c_ulonglong), _i],
     "chfsi_lanczos_z": [_vp, _i, _i, _vp, _ll, _i, _vp, _vp, _pd, _pd, _pd, _pi],
     "chfsi_gemm_z": [_vp, _c, _c, _i, _i, _i, _d, _d, _vp, _ll, _vp, _ll, _d, _d, _vp, _ll],

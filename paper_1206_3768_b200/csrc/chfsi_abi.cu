@@ -183,6 +183,14 @@ int chfsi_ctx_set_step_groups(chfsi_ctx* ctx, int groups) {
   return CHFSI_OK;
 }
 
+int chfsi_ctx_set_step_warps(chfsi_ctx* ctx, int warps) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(warps == 0 || warps == 4 || warps == 8 || warps == 16, "warps must be 0, 4, 8 or 16");
+  CK_ARG(warps == 0 || ctx->tiling.bm != 0, "set a tiling first (chfsi_ctx_set_tiling)");
+  ctx->tiling.warps = warps;
+  return CHFSI_OK;
+}
+
 int chfsi_ctx_set_stream(chfsi_ctx* ctx, void* stream) {
   CK_ARG(ctx, "ctx is NULL");
   ctx->stream = static_cast<cudaStream_t>(stream);
@@ -418,11 +426,17 @@ int chfsi_filter_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, i
     // each chain: the 8-warp 64-row tile (64x16 when it pads >10 % less)
     auto chain_tiling = [](int wc) {
       const int p16 = ((wc + 15) / 16) * 16, p32 = ((wc + 31) / 32) * 32;
-      return p16 * 10 < p32 * 9 ? chfsi::StepTiling{64, 16, 0} : chfsi::StepTiling{64, 32, 0};
+      chfsi::StepTiling t = p16 * 10 < p32 * 9 ? chfsi::StepTiling{64, 16, 0} : chfsi::StepTiling{64, 32, 0};
+      if (chfsi::complex_product() == 3) t.warps = 4;  // the 3M kernels' 4-warp 64-row tiles
+      return t;
     };
     chfsi::StepTiling t0 = chain_tiling(w0), t1 = chain_tiling(w1);
-    // (n >= 10000: the single 16-warp 128x32 chain is ahead, 34.9 vs 34.2 at C4)
-    if (n < 10000) {
+    // (n >= 10000: the single 16-warp 128x32 chain is ahead, 34.9 vs 34.2 at C4.
+    // The 3M kernels — two warps per sub-partition, no co-resident-CTA
+    // imbalance — gain from two chains only at C1-like sizes: 512x48 5.2 ->
+    // 5.8, level at 2048x64..5000x250, behind at 2048x160 34.5 vs 32.2,
+    // profiles/r01_k1_3m_sweep.log.)
+    if (n < (chfsi::complex_product() == 3 ? 1500 : 10000)) {
       CK(ensure_aux_stream(ctx));
       t0.split = chfsi::kNumSMs;
       t1.split = chfsi::kNumSMs;
@@ -457,6 +471,12 @@ int chfsi_step_tiling(int n, int w, int* bm, int* bn, int* split) {
   *bn = t.bn;
   *split = t.split;
   return CHFSI_OK;
+}
+
+int chfsi_set_complex_product(int product) {
+  if (product == 0) return chfsi::complex_product();
+  CK_ARG(product == 3 || product == 4, "complex product must be 3 or 4");
+  return chfsi::set_complex_product(product);
 }
 
 // ------------------------------------------------------------------- K2 ---

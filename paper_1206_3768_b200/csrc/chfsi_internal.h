@@ -16,6 +16,8 @@ struct StepTiling {
   int bn;     // 16, 32 or 64 columns per CTA tile
   int split;  // grid override for tests/tuning (0 = all resident CTAs)
   int groups = 1;  // 1: one 8/16-warp tile group per CTA; 2: two 8-warp groups splitting k
+  int product = 0; // complex product: 0 = process default, 3 = Gauss/3M, 4 = four real MMAs
+  int warps = 0;   // warps per tile group: 0 = the registry's default for (bm, bn, groups)
 };
 
 // Stream-K scratch owned by the context: partial tiles + ready flags.
@@ -27,6 +29,9 @@ struct StepWorkspace {
 };
 
 StepTiling choose_step_tiling(int n, int w);
+// process-wide K1 complex-product default (3 or 4); returns the previous one, -1 if invalid
+int set_complex_product(int product);
+int complex_product();
 size_t step_workspace_doubles(int max_grid);
 // CHFSI_K1_DEBUG & 8 diagnostics: copy the last K1 launch's per-CTA trace
 // ([start, wait begin, wait end, end] globaltimer ns, smid) to host.

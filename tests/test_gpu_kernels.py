@@ -47,11 +47,28 @@ def _lib():
     return _lib
 
 
-def set_tiling(bm, bn, split, groups=1):
+def set_tiling(bm, bn, split, groups=1, warps=0):
     L = _lib()
     L.check(L.lib().chfsi_ctx_set_tiling(L.ctx(), bm, bn, split))
     if bm and groups != 1:
         L.check(L.lib().chfsi_ctx_set_step_groups(L.ctx(), groups))
+    if bm and warps:
+        L.check(L.lib().chfsi_ctx_set_step_warps(L.ctx(), warps))
+
+
+@pytest.fixture(params=[3, 4], ids=["3m", "4m"])
+def product(request):
+    """K1 complex product: 3 = Gauss/3M (the default), 4 = four real MMAs."""
+    L = _lib()
+    old = L.lib().chfsi_set_complex_product(request.param)
+    assert old in (3, 4)
+    yield request.param
+    L.lib().chfsi_set_complex_product(old)
+
+
+# 3M-only variants: 32x16 warp tiles (4-warp 64-row, 8-warp 128-row CTAs)
+TILINGS_3M = {(64, 32, 0, 1, 4), (64, 32, 7, 1, 4), (64, 16, 0, 1, 4), (64, 16, 13, 1, 4),
+              (128, 32, 0, 1, 8), (128, 32, 5, 1, 8), (64, 32, 150, 1, 4)}
 
 
 def cheb_step(h_dev, conj, ycur, yprev, ynext, alpha, c, beta):
@@ -76,13 +93,17 @@ def fb(x):
 # data-parallel / stream-K splits and multi-peer fix-ups
 TILINGS = [(64, 64, 0), (64, 32, 0), (64, 16, 0), (64, 64, 1), (64, 32, 7), (64, 16, 13),
            (64, 64, 150), (64, 32, 296), (128, 32, 0), (128, 32, 5), (128, 16, 0), (128, 16, 77),
-           (64, 32, 0, 2), (64, 32, 9, 2), (64, 16, 0, 2), (64, 16, 31, 2)]
+           (64, 32, 0, 2), (64, 32, 9, 2), (64, 16, 0, 2), (64, 16, 31, 2)] + sorted(TILINGS_3M)
 
 
 @pytest.mark.parametrize("tiling", TILINGS)
 @pytest.mark.parametrize("n,w", [(64, 32), (131, 7), (257, 33), (512, 48), (1000, 97)])
 @pytest.mark.parametrize("conj", [False, True])
-def test_cheb_step_matches_numpy(pkg, tiling, n, w, conj):
+def test_cheb_step_matches_numpy(pkg, product, tiling, n, w, conj):
+    if tiling in TILINGS_3M and product == 4:
+        pytest.skip("3M-only tile variant")
+    if tiling[:2] in ((64, 64), (32, 32), (32, 64)) and product == 3:
+        pytest.skip("4M-only tile variant (3M falls back to it)")
     rng = np.random.default_rng(n * 7 + w)
     h = random_hermitian(rng, n)
     y = rng.standard_normal((n, w)) + 1j * rng.standard_normal((n, w))
@@ -103,7 +124,7 @@ def test_cheb_step_matches_numpy(pkg, tiling, n, w, conj):
     assert np.abs(out - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
-def test_cheb_step_plain_product_and_determinism(pkg):
+def test_cheb_step_plain_product_and_determinism(pkg, product):
     rng = np.random.default_rng(3)
     n, w = 700, 45
     h = random_hermitian(rng, n)
@@ -120,7 +141,8 @@ def test_cheb_step_plain_product_and_determinism(pkg):
 @pytest.mark.parametrize("n,w,grid,bm,groups", [
     (2048, 160, 0, 64, 1), (2048, 131, 0, 64, 1), (2048, 97, 0, 64, 1), (1500, 40, 37, 64, 1),
     (700, 33, 0, 64, 1), (4096, 160, 0, 64, 1), (2048, 160, 0, 128, 1), (3000, 70, 0, 128, 1),
-    (2048, 160, 0, 64, 2), (1500, 40, 37, 64, 2), (3000, 131, 0, 64, 2)])
+    (2048, 160, 0, 64, 2), (1500, 40, 37, 64, 2), (3000, 131, 0, 64, 2),
+    (2048, 160, 0, 64, -4), (2048, 97, 0, 64, -4), (1500, 40, 37, 64, -4), (5000, 250, 0, 128, -8)])
 def test_cheb_step_bitwise_repeatable(pkg, n, w, grid, bm, groups):
     """Stream-K fix-ups, TMA/mbarrier pipeline and warp convergence: 40
     back-to-back filters must agree bit for bit. (This caught two real
@@ -130,7 +152,8 @@ def test_cheb_step_bitwise_repeatable(pkg, n, w, grid, bm, groups):
     h = torch.from_numpy(random_hermitian(rng, n)).cuda()
     y = fb(rng.standard_normal((n, w)) + 1j * rng.standard_normal((n, w)))
     win = pkg.FilterWindow(a=-1.0, b=1.5, scale_ref=-1.6)
-    set_tiling(bm, 32, grid, groups)
+    # groups < 0: one group of -groups warps (the 3M 32x16-warp-tile kernels)
+    set_tiling(bm, 32, grid, max(groups, 1), -groups if groups < 0 else 0)
     try:
         outs = [pkg.chebyshev_filter(h, y, 4, win) for _ in range(40)]
     finally:
@@ -139,7 +162,8 @@ def test_cheb_step_bitwise_repeatable(pkg, n, w, grid, bm, groups):
         assert torch.equal(o, outs[0])
 
 
-@pytest.mark.parametrize("n,w", [(2048, 160), (2048, 64), (3000, 123), (5000, 250)])
+@pytest.mark.parametrize("n,w", [(512, 48), (1000, 97), (2048, 160), (2048, 64), (3000, 123),
+                                 (5000, 250)])
 def test_two_chain_filter_matches_one_chain_and_oracle(pkg, n, w):
     """The default filter runs balanced column halves as two concurrent
     launch chains: same result as one chain (to rounding) and as the oracle,

@@ -24,6 +24,8 @@ ap.add_argument("--quick", action="store_true")
 ap.add_argument("--variants", default="auto")
 ap.add_argument("--shapes", default="")
 ap.add_argument("--no-cublas", action="store_true")
+ap.add_argument("--chains", default="2", help="filter launch chains for the auto tiling (1, 2 or 1,2)")
+ap.add_argument("--products", default="3,4", help="K1 complex products to compare (3 = Gauss/3M, 4 = 4M)")
 a = ap.parse_args()
 shapes = [(512, 48), (2048, 160), (2048, 100), (2048, 40), (5000, 600), (5000, 250),
           (12000, 1400)]
@@ -66,18 +68,24 @@ for n, w in shapes:
         yy = torch.randn(n, w, dtype=torch.complex128, device="cuda")
         ms_c = timed(lambda: h @ yy, reps * 2)
         cub = 8.0 * n * n * w / ms_c / 1e9
-    for v in variants:
+    for v, prod, ch in [(v, pr, ch) for v in variants for pr in a.products.split(",")
+                        for ch in (a.chains.split(",") if v == "auto" else ["1"])]:
+        _lib.lib().chfsi_set_complex_product(int(prod))
+        _lib.check(_lib.lib().chfsi_ctx_set_filter_chains(_lib.ctx(), int(ch)))
         if v == "auto":
             _lib.check(_lib.lib().chfsi_ctx_set_tiling(_lib.ctx(), 0, 0, 0))
         else:
-            dual = v.endswith("d")  # "64x32d": two 8-warp groups per CTA
-            bm, bn = (int(t) for t in v.rstrip("d").split("x"))
+            # "64x32d": two 8-warp groups per CTA; "128x32w8": 8 warps per group
+            vv, _, wp = v.partition("w")
+            dual = vv.endswith("d")
+            bm, bn = (int(t) for t in vv.rstrip("d").split("x"))
             _lib.check(_lib.lib().chfsi_ctx_set_tiling(_lib.ctx(), bm, bn, 0))
             if dual:
                 _lib.check(_lib.lib().chfsi_ctx_set_step_groups(_lib.ctx(), 2))
+            _lib.check(_lib.lib().chfsi_ctx_set_step_warps(_lib.ctx(), int(wp) if wp else 0))
         ms = timed(lambda: _filter_into(op, y, x, y, deg, win), reps) / deg
         fl = 8.0 * n * n * w
-        print(json.dumps({"n": n, "w": w, "variant": v, "k1_us": round(ms * 1e3, 2),
+        print(json.dumps({"n": n, "w": w, "variant": v, "product": int(prod), "chains": int(ch), "k1_us": round(ms * 1e3, 2),
                           "k1_tflops": round(fl / ms / 1e9, 2),
                           "cublas_tflops": None if cub is None else round(cub, 2)}), flush=True)
     _lib.check(_lib.lib().chfsi_ctx_set_tiling(_lib.ctx(), 0, 0, 0))
