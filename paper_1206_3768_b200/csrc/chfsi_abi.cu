@@ -630,8 +630,11 @@ int qr_cholqr(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdia
   cudaStream_t s = ctx->stream;
   *fallback = false;
   *last_dev = 0.0;
+  // The factor is taken LOWER (G = L L^H, L = R^H) and Y <- Y L^-H: cuSOLVER's
+  // lower potrf is ~1.8x faster than its upper one at the panel sizes (w=160:
+  // 74 vs 135 us, tools/microbench/qr_bench.cu); the TRSM costs the same.
   int lwork = 0;
-  CK_SOLVER(cusolverDnZpotrf_bufferSize(ctx->solver, CUBLAS_FILL_MODE_UPPER, n,
+  CK_SOLVER(cusolverDnZpotrf_bufferSize(ctx->solver, CUBLAS_FILL_MODE_LOWER, n,
                                         reinterpret_cast<cuDoubleComplex*>(g), n, &lwork));
   CK(ensure_ws(ctx, (size_t)lwork * sizeof(cuDoubleComplex)));
   const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
@@ -643,12 +646,12 @@ int qr_cholqr(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdia
                         reinterpret_cast<const cuDoubleComplex*>(y), m, &zero,
                         reinterpret_cast<cuDoubleComplex*>(g), n));
     if (shifted && pass == 0) CK_CUDA(chfsi::add_diag_shift_launch(g, n, n, fro, shift_coef, s));
-    CK_SOLVER(cusolverDnZpotrf(ctx->solver, CUBLAS_FILL_MODE_UPPER, n,
+    CK_SOLVER(cusolverDnZpotrf(ctx->solver, CUBLAS_FILL_MODE_LOWER, n,
                                reinterpret_cast<cuDoubleComplex*>(g), n,
                                static_cast<cuDoubleComplex*>(ctx->ws), lwork, ctx->dinfo + pass));
     CK_CUDA(chfsi::diag_accumulate_launch(g, n, n, rdiag_acc, pass == 0, s));
     if (pass == passes - 1) CK_CUDA(chfsi::diag_accumulate_launch(g, n, n, rlast, true, s));
-    CK_BLAS(cublasZtrsm(ctx->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
+    CK_BLAS(cublasZtrsm(ctx->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C,
                         CUBLAS_DIAG_NON_UNIT, m, n, &one, reinterpret_cast<const cuDoubleComplex*>(g),
                         n, reinterpret_cast<cuDoubleComplex*>(y), m));
   }
