@@ -189,6 +189,13 @@ CHFSI_API int chfsi_qr_orthonormalize_z(chfsi_ctx* ctx, int m, int n, void* Y, l
  * Householder; 1 = Householder only; 2 = shifted Cholesky-QR3, then
  * Householder. All return the same (unique) Q with positive-real R diagonal. */
 CHFSI_API int chfsi_ctx_set_qr_mode(chfsi_ctx* ctx, int mode);
+/* Cholesky-QR2's second pass (default on): after the first pass
+ * eps = max|Q1^H Q1 - I| ~ u cond(Y)^2; when eps <= 1e-8 the second factor is
+ * taken to first order, R2 = I + tri(E) (strict upper + diag/2 of
+ * E = Q1^H Q1 - I), and Q = Q1 (I - tri(E)) by one ZGEMM — the same
+ * positive-diagonal QR to O(eps^2) without a second potrf + ZTRSM. eps > 1e-8
+ * reruns the exact pass. on = 0 always runs the exact pass. */
+CHFSI_API int chfsi_ctx_set_qr_linear2(chfsi_ctx* ctx, int on);
 
 /* Dense Hermitian eigensolver (linalg.py:181-206): ascending values to the
  * DEVICE array w, eigenvectors overwrite A. */

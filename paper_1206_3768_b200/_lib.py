@@ -80,6 +80,7 @@ _SIGNATURES = {
     "chfsi_cgs_project_z": [_vp, _i, _i, _i, _vp, _ll, _vp, _ll, _vp],
     "chfsi_qr_orthonormalize_z": [_vp, _i, _i, _vp, _ll, _pi, _pi],
     "chfsi_ctx_set_qr_mode": [_vp, _i],
+    "chfsi_ctx_set_qr_linear2": [_vp, _i],
     "chfsi_ctx_set_lanczos_mode": [_vp, _i],
     "chfsi_heevd_z": [_vp, _i, _vp, _ll, _vp],
     "chfsi_heev_rr_z": [_vp, _i, _vp, _ll, _vp, _d, _pi],

@@ -28,6 +28,7 @@ struct chfsi_ctx {
   chfsi::StepTiling tiling{0, 0, 0};  // K1 tile override (bm == 0: automatic)
   chfsi::StepWorkspace step_ws{nullptr, nullptr, nullptr, 0};
   int qr_mode = 0;  // 0: shifted Cholesky-QR3 with Householder fallback; 1: Householder
+  bool qr_linear2 = true;  // Cholesky-QR2: linearised second pass when |Q1^H Q1 - I| <= 1e-8
   int lanczos_mode = 0;  // 0: cooperative single kernel; 1: one launch per operation
   unsigned step_epoch = 0;
   cudaEvent_t loop_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // chfsi_solve_loop_z phase timers

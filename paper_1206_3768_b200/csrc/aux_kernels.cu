@@ -386,6 +386,51 @@ __global__ void diag_accumulate_kernel(const double2* r, long long ldr, int n, d
   if (i < n) acc[i] = (first ? 1.0 : acc[i]) * r[(long long)i * ldr + i].x;
 }
 
+// Second Cholesky-QR pass linearised (see chfsi_internal.h): G = I + E in,
+// M = I - tri(E) out (in place, upper triangle; strict lower zeroed), where
+// tri(E) = strict-upper(E) + diag(E)/2, so Q1 M has Q^H Q = I + O(|E|^2).
+// out[0] = max |E_ij| (NaN propagates), acc[i] *= 1 + E_ii/2 (~ R2_ii),
+// last[i] = 1 + E_ii/2. One block: the matrix is at most a few hundred wide.
+constexpr int kNiThreads = 1024;
+__global__ void __launch_bounds__(kNiThreads) near_identity_update_kernel(
+    double2* g, long long ldg, int n, double* acc, double* last, double* out) {
+  __shared__ double red[kNiThreads / 32];
+  double emax = 0.0;
+  const long long total = (long long)n * n;
+  for (long long e = threadIdx.x; e < total; e += kNiThreads) {
+    const int j = (int)(e / n), i = (int)(e - (long long)j * n);  // column-major (i, j)
+    double2* p = g + (long long)j * ldg + i;
+    if (i > j) {
+      *p = make_double2(0.0, 0.0);
+      continue;
+    }
+    const double2 v = *p;
+    if (i == j) {
+      const double d = v.x - 1.0, m = fmax(fabs(d), fabs(v.y));
+      emax = (m > emax || m != m) ? m : emax;
+      const double r2 = 1.0 + 0.5 * d;
+      acc[i] *= r2;
+      last[i] = r2;
+      *p = make_double2(1.0 - 0.5 * d, 0.0);
+    } else {
+      const double m = fmax(fabs(v.x), fabs(v.y));
+      emax = (m > emax || m != m) ? m : emax;
+      *p = make_double2(-v.x, -v.y);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double t = __shfl_down_sync(0xffffffffu, emax, o);
+    emax = (t > emax || t != t) ? t : emax;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = emax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w = 0; w < kNiThreads / 32; ++w) m = (red[w] > m || red[w] != red[w]) ? red[w] : m;
+    out[0] = m;
+  }
+}
+
 inline int grid_for(long long total, int threads, int cap = kNumSMs * 16) {
   long long g = (total + threads - 1) / threads;
   if (g > cap) g = cap;
@@ -554,6 +599,14 @@ cudaError_t diag_accumulate_launch(const double2* r, long long ldr, int n, doubl
   if (n <= 0) return cudaSuccess;
   note_launch();
   diag_accumulate_kernel<<<(n + 255) / 256, 256, 0, s>>>(r, ldr, n, acc, first ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t near_identity_update_launch(double2* g, long long ldg, int n, double* acc, double* last,
+                                        double* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  note_launch();
+  near_identity_update_kernel<<<1, kNiThreads, 0, s>>>(g, ldg, n, acc, last, out);
   return cudaGetLastError();
 }
 

@@ -624,12 +624,23 @@ int qr_householder(chfsi_ctx* ctx, int m, int n, double2* y, const double2* back
   return CHFSI_OK;
 }
 
+// linear2: the second of two passes is linearised — after a first pass Q1 is
+// orthonormal to eps = max|Q1^H Q1 - I| ~ u cond(Y)^2 (~1e-13 for the filtered
+// panels), and for G = I + E the Cholesky factor is R2 = I + tri(E) + O(eps^2)
+// (tri = strict upper + diag/2), so Q = Q1 (I - tri(E)) has Q^H Q = I +
+// O(eps^2): one ZGEMM Gram, one small kernel and one ZGEMM replace
+// potrf + ZTRSM (2048 x 160: ~145 -> ~35 us). Accepted only when eps <= 1e-8
+// (*linear_reject otherwise; the caller reruns the exact pass).
 int qr_cholqr(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdiag_acc,
               double* rlast, const double* fro, int passes, bool shifted, bool* fallback,
-              double* last_dev) {
+              double* last_dev, bool linear2 = false, bool* linear_reject = nullptr,
+              double2* tmp = nullptr) {
   cudaStream_t s = ctx->stream;
   *fallback = false;
   *last_dev = 0.0;
+  if (linear_reject) *linear_reject = false;
+  linear2 = linear2 && passes == 2 && !shifted && tmp != nullptr;
+  double* eps_dev = ctx->scalars + 8;
   // The factor is taken LOWER (G = L L^H, L = R^H) and Y <- Y L^-H: cuSOLVER's
   // lower potrf is ~1.8x faster than its upper one at the panel sizes (w=160:
   // 74 vs 135 us, tools/microbench/qr_bench.cu); the TRSM costs the same.
@@ -646,6 +657,17 @@ int qr_cholqr(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdia
                         reinterpret_cast<const cuDoubleComplex*>(y), m, &zero,
                         reinterpret_cast<cuDoubleComplex*>(g), n));
     if (shifted && pass == 0) CK_CUDA(chfsi::add_diag_shift_launch(g, n, n, fro, shift_coef, s));
+    if (linear2 && pass == 1) {
+      CK_CUDA(chfsi::near_identity_update_launch(g, n, n, rdiag_acc, rlast, eps_dev, s));
+      // Q = Q1 M out of place (ZGEMM + copy back: 2048 x 160 27 us vs 47 us
+      // for cuBLAS's in-place ZTRMM; M's strict lower triangle is zero)
+      CK_BLAS(cublasZgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, m, n, n, &one,
+                          reinterpret_cast<const cuDoubleComplex*>(y), m,
+                          reinterpret_cast<const cuDoubleComplex*>(g), n, &zero,
+                          reinterpret_cast<cuDoubleComplex*>(tmp), m));
+      CK_CUDA(cudaMemcpyAsync(y, tmp, (size_t)m * n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+      continue;
+    }
     CK_SOLVER(cusolverDnZpotrf(ctx->solver, CUBLAS_FILL_MODE_LOWER, n,
                                reinterpret_cast<cuDoubleComplex*>(g), n,
                                static_cast<cuDoubleComplex*>(ctx->ws), lwork, ctx->dinfo + pass));
@@ -655,10 +677,12 @@ int qr_cholqr(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdia
                         CUBLAS_DIAG_NON_UNIT, m, n, &one, reinterpret_cast<const cuDoubleComplex*>(g),
                         n, reinterpret_cast<cuDoubleComplex*>(y), m));
   }
-  CK(chfsi::ensure_pinned(ctx, (size_t)(2 * n + 1) * sizeof(double) + 4 * sizeof(int)));
+  CK(chfsi::ensure_pinned(ctx, (size_t)(2 * n + 2) * sizeof(double) + 4 * sizeof(int)));
   double* hd = static_cast<double*>(ctx->pinned);
   double* hl = hd + n + 1;
-  int* info = reinterpret_cast<int*>(hl + n);
+  double* heps = hl + n;
+  int* info = reinterpret_cast<int*>(heps + 1);
+  if (linear2) CK_CUDA(cudaMemcpyAsync(heps, eps_dev, sizeof(double), cudaMemcpyDeviceToHost, s));
   CK_CUDA(cudaMemcpyAsync(hd, rdiag_acc, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s));
   CK_CUDA(cudaMemcpyAsync(hd + n, fro, sizeof(double), cudaMemcpyDeviceToHost, s));
   CK_CUDA(cudaMemcpyAsync(hl, rlast, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -666,7 +690,7 @@ int qr_cholqr(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdia
   CK_CUDA(cudaStreamSynchronize(s));
   const double hfro = hd[n];
   bool bad = !std::isfinite(hfro);
-  for (int pass = 0; pass < passes; ++pass) bad = bad || info[pass] != 0;
+  for (int pass = 0; pass < (linear2 ? 1 : passes); ++pass) bad = bad || info[pass] != 0;
   if (bad) {
     *fallback = true;
     return CHFSI_OK;
@@ -681,6 +705,10 @@ int qr_cholqr(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdia
     dev = std::max(dev, std::fabs(hl[j] - 1.0));
   }
   *last_dev = std::isfinite(dev) ? dev : INFINITY;
+  if (linear2 && !(*heps <= 1e-8)) {  // also NaN: rerun the pass exactly
+    *fallback = true;
+    if (linear_reject) *linear_reject = true;
+  }
   return CHFSI_OK;
 }
 
@@ -701,13 +729,14 @@ int chfsi_qr_orthonormalize_z(chfsi_ctx* ctx, int m, int n, void* Y, long long l
   // scratch: backup copy of Y (m*n), tau (n), rdiag (n), Gram (n*n), diag accumulator (n),
   // last pass's diagonal (n)
   const size_t blk = (size_t)m * n * sizeof(double2);
-  CK(ensure_scratch(ctx, blk + 2 * (size_t)n * sizeof(double2) + (size_t)n * n * sizeof(double2) +
+  CK(ensure_scratch(ctx, 2 * blk + 2 * (size_t)n * sizeof(double2) + (size_t)n * n * sizeof(double2) +
                              2 * (size_t)n * sizeof(double)));
   double2* backup = static_cast<double2*>(ctx->scratch);
   double2* tau = backup + (size_t)m * n;
   double2* rdiag = tau + n;
   double2* g = rdiag + n;
   double* racc = reinterpret_cast<double*>(g + (size_t)n * n);
+  double2* tmp = reinterpret_cast<double2*>(racc + 2 * (size_t)n);  // m x n (linearised pass 2)
   double* fro = ctx->scalars + 1;
   CK_CUDA(cudaMemcpyAsync(backup, y, blk, cudaMemcpyDeviceToDevice, s));
   CK_CUDA(chfsi::norm2_launch(y, (long long)m * n, ctx->partial, fro, nullptr, s));
@@ -721,9 +750,16 @@ int chfsi_qr_orthonormalize_z(chfsi_ctx* ctx, int m, int n, void* Y, long long l
     // the C2 sequence), so this is the common case; otherwise the shifted
     // Cholesky-QR3 runs from the backup, and Householder after that.
     if (ctx->qr_mode == 0) {
-      CK(qr_cholqr(ctx, m, n, y, g, racc, racc + n, fro, 2, false, &fallback, &dev));
+      bool lin_reject = false;
+      CK(qr_cholqr(ctx, m, n, y, g, racc, racc + n, fro, 2, false, &fallback, &dev,
+                   ctx->qr_linear2, &lin_reject, tmp));
       if (!fallback && dev <= 1e-6) return CHFSI_OK;
       CK_CUDA(cudaMemcpyAsync(y, backup, blk, cudaMemcpyDeviceToDevice, s));
+      if (lin_reject) {  // the first pass was fine but left |Q1^H Q1 - I| > 1e-8: exact pass 2
+        CK(qr_cholqr(ctx, m, n, y, g, racc, racc + n, fro, 2, false, &fallback, &dev));
+        if (!fallback && dev <= 1e-6) return CHFSI_OK;
+        CK_CUDA(cudaMemcpyAsync(y, backup, blk, cudaMemcpyDeviceToDevice, s));
+      }
     }
     CK(qr_cholqr(ctx, m, n, y, g, racc, racc + n, fro, 3, true, &fallback, &dev));
     if (!fallback) return CHFSI_OK;
@@ -736,6 +772,12 @@ int chfsi_ctx_set_lanczos_mode(chfsi_ctx* ctx, int mode) {
   CK_ARG(ctx, "ctx is NULL");
   CK_ARG(mode == 0 || mode == 1, "lanczos mode must be 0 (cooperative) or 1 (multi-kernel)");
   ctx->lanczos_mode = mode;
+  return CHFSI_OK;
+}
+
+int chfsi_ctx_set_qr_linear2(chfsi_ctx* ctx, int on) {
+  CK_ARG(ctx, "ctx is NULL");
+  ctx->qr_linear2 = on != 0;
   return CHFSI_OK;
 }
 

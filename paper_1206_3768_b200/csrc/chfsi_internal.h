@@ -147,6 +147,11 @@ cudaError_t nd_gather_cols_launch(const double2* src, long long lds, int m, int 
                                   double2* out, long long ldo, cudaStream_t s);
 // y = x / *d (complex / real, round-to-nearest division)
 cudaError_t div_scalar_launch(const double2* x, const double* d, double2* y, int n, cudaStream_t s);
+// Linearised second Cholesky-QR pass: G = Q1^H Q1 = I + E -> M = I - tri(E)
+// in place (upper; tri = strict upper + diag/2), out[0] = max|E_ij|,
+// acc[i] *= 1 + E_ii/2, last[i] = 1 + E_ii/2 (the R2 diagonal to O(|E|^2)).
+cudaError_t near_identity_update_launch(double2* g, long long ldg, int n, double* acc, double* last,
+                                        double* out, cudaStream_t s);
 // Y[:, j] = X[:, j]
 cudaError_t copy_cols_launch(const double2* x, long long ldx, double2* y, long long ldy, int m,
                              int n, cudaStream_t s);

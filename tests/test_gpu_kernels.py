@@ -341,6 +341,38 @@ def test_cholqr3_matches_householder(pkg, kind, mode):
     assert np.abs(qc - ref).max() <= 1e-13 * cond * 10
 
 
+@pytest.mark.parametrize("kind", ["random", "moderate", "graded", "tall_wide"])
+def test_cholqr2_linearised_second_pass(pkg, kind):
+    """Cholesky-QR2's linearised second pass (Q = Q1 (I - tri(Q1^H Q1 - I)),
+    taken when the first pass leaves |Q1^H Q1 - I| <= 1e-8; the graded panel
+    (cond 1e9) exceeds that and reruns the exact pass): same Q as the exact
+    pass and as Householder to rounding x cond, orthonormal to 1e-13."""
+    L = _lib()
+    rng = np.random.default_rng(77)
+    m, n = {"tall_wide": (2048, 160)}.get(kind, (600, 48))
+    y = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
+    cond = 1.0
+    if kind == "moderate":  # the filtered panels' regime: R diagonal ranging over ~50
+        y = y * np.logspace(0, -1.7, n)
+        cond = 50.0
+    elif kind == "graded":
+        y = y * np.logspace(0, -9, n)
+        cond = 1e9
+    try:
+        L.check(L.lib().chfsi_ctx_set_qr_linear2(L.ctx(), 0))
+        q_exact = pkg.qr_orthonormalize(y).cpu().numpy()
+        L.check(L.lib().chfsi_ctx_set_qr_linear2(L.ctx(), 1))
+        q_lin = pkg.qr_orthonormalize(y).cpu().numpy()
+        set_qr_mode(1)
+        qh = pkg.qr_orthonormalize(y).cpu().numpy()
+    finally:
+        set_qr_mode(0)
+        L.check(L.lib().chfsi_ctx_set_qr_linear2(L.ctx(), 1))
+    assert np.abs(q_lin.conj().T @ q_lin - np.eye(n)).max() <= 1e-13
+    assert np.abs(q_lin - q_exact).max() <= 1e-13 * cond * 10
+    assert np.abs(q_lin - qh).max() <= 1e-13 * cond * 10
+
+
 def test_qr_idempotent_on_orthonormal_input(pkg):
     rng = np.random.default_rng(17)
     q0 = orc.qr_orthonormalize(rng.standard_normal((90, 12)) + 1j * rng.standard_normal((90, 12)))

@@ -122,6 +122,18 @@ int main() {
       cudaMemcpyAsync(dr, dg, sizeof(cuDoubleComplex) * w * w, cudaMemcpyDeviceToDevice, s);
       cusolverDnXtrtri(h, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, w, CUDA_C_64F, dr, w, dwork, dws, hwork.data(), hws, dinfo);
     });
+    {
+      cuDoubleComplex* did;
+      cudaMalloc(&did, sizeof(cuDoubleComplex) * w * w);
+      std::vector<cuDoubleComplex> eye((size_t)w * w, zero);
+      for (int i = 0; i < w; ++i) eye[(size_t)i * w + i] = one;
+      timeit("copy+trsm_identity_w", [&] {
+        cudaMemcpyAsync(did, eye.data(), 0, cudaMemcpyHostToDevice, s);
+        cublasZtrsm(b, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, w, w, &one, dg, w, did, w);
+      });
+      timeit("trmm_inplace", [&] { cublasZtrmm(b, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, m, w, &one, dr, w, dy2, m, dy2, m); });
+      cudaFree(did);
+    }
     timeit("gemm_y_rinv", [&] { cublasZgemm(b, CUBLAS_OP_N, CUBLAS_OP_N, m, w, w, &one, dy, m, dr, w, &zero, dy2, m); });
     timeit("trmm_y_rinv", [&] { cublasZtrmm(b, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, m, w, &one, dr, w, dy, m, dy2, m); });
     cudaFree(dy); cudaFree(dy2); cudaFree(dg); cudaFree(dg0); cudaFree(dr); cudaFree(work); cudaFree(dwork);
