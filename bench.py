@@ -304,17 +304,22 @@ def run_ours(args):
     # step's solutions would grow the allocator (cudaMalloc) every step
     step_stats = []
     res = None
+    step_ev = [e0]
     for _ in range(args.steps):
         res = None  # release the previous step's solutions first
         res = device_step()
         step_stats.append([(r.report.t_filter, r.report.filter_flops, r.report.filter_launches)
                            for r in res])
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        step_ev.append(ev)
     results = [res]
     e1.record()
     barrier()
     launches = _lib.lib().chfsi_launch_count() - lc0
     clk = clocks.stop()
     t_dev = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    step_ms = [round(a.elapsed_time(b), 3) for a, b in zip(step_ev[:-1], step_ev[1:])]
 
     flops_seq = sum(r.report.filter_flops for r in results[-1])
     f_time = sum(t for st in step_stats for t, _, _ in st)
@@ -412,6 +417,7 @@ def run_ours(args):
                             else f"replicas x{world}" if world > 1 else "single GPU"),
         },
         "time_to_solution_s": t_dev / args.steps,
+        "step_ms": step_ms,
         "filter_kernel_gflops": achieved * 1e3,
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

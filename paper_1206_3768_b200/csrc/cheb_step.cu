@@ -162,17 +162,19 @@ int step_grid_size(int bn, bool conj) {
 cudaError_t cheb_step_launch(const double2* h, long long ldh, bool conj_h, const double2* ycur,
                              long long ldc, const double2* yprev, long long ldp, double2* ynext,
                              long long ldn, int n, int w, double alpha, double c, double beta,
-                             StepTiling tiling, const StepWorkspace& ws, cudaStream_t stream) {
+                             StepTiling tiling, const StepWorkspace& ws, cudaStream_t stream,
+                             bool pdl) {
   const RowShard whole{n, 0, 0, nullptr, 0};
   return cheb_step_rows_launch(h, ldh, conj_h, ycur, ldc, yprev, ldp, ynext, ldn, n, w, alpha, c,
-                               beta, whole, tiling, ws, stream, nullptr, 0);
+                               beta, whole, tiling, ws, stream, nullptr, 0, pdl);
 }
 
 cudaError_t cheb_step_rows_launch(const double2* h, long long ldh, bool conj_h, const double2* ycur,
                                   long long ldc, const double2* yprev, long long ldp, double2* ynext,
                                   long long ldn, int n, int w, double alpha, double c, double beta,
                                   const RowShard& shard, StepTiling tiling, const StepWorkspace& ws,
-                                  cudaStream_t stream, const long long* peer_shift, int npeer) {
+                                  cudaStream_t stream, const long long* peer_shift, int npeer,
+                                  bool pdl) {
   if (npeer < 0 || npeer > kMaxPeers) return cudaErrorInvalidValue;
   const int m = shard.rows;
   if (n <= 0 || w <= 0 || m <= 0) return cudaSuccess;
@@ -244,7 +246,26 @@ cudaError_t cheb_step_rows_launch(const double2* h, long long ldh, bool conj_h, 
   p.epoch = ++*ws.epoch;
   void* args[] = {&tmA, &tmB, &p};
   note_launch();
-  return cudaLaunchKernel(v.fn, dim3(grid), dim3(v.threads), args, v.smem, stream);
+  // Programmatic dependent launch between consecutive steps of one filter
+  // chain (the kernel waits on griddepcontrol before touching the previous
+  // step's outputs). Only there: a PDL launch after other work let K1 CTAs
+  // park on SM slots early and cost 8 % at C2. CHFSI_K1_PDL=0 disables it.
+  static const bool pdl_env = [] {
+    const char* e = getenv("CHFSI_K1_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  pdl = pdl && pdl_env;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(v.threads);
+  cfg.dynamicSmemBytes = v.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelExC(&cfg, v.fn, args);
 }
 
 int set_complex_product(int product) {

@@ -244,10 +244,6 @@ __global__ void __launch_bounds__(GROUPS* WM* WN * 32, MINB)
   const int total = dp_iters + (se - sb);
   if (total == 0) return;
   const bool tr = (p.dbg & 8) && threadIdx.x == 0;
-  if (tr) {
-    p.trace[cta * 5 + 0] = gtimer();
-    p.trace[cta * 5 + 4] = smid() | ((unsigned long long)blockIdx.x << 16);
-  }
   // Local order: [publish] [data-parallel tiles] [middle] [owner tail].
   //   publish: the head of the last SK tile when the range ends inside it —
   //            done first, so peers' partials are ready early;
@@ -324,6 +320,17 @@ __global__ void __launch_bounds__(GROUPS* WM* WN * 32, MINB)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  // Programmatic dependent launch: the launch and the prologue above overlap
+  // the previous step's tail; nothing the previous grid writes (Ycur, Yprev,
+  // the stream-K partials and flags) is touched before this wait returns
+  // (it returns at once when the launch had no programmatic dependency).
+  // Dependents may be scheduled from here on: they wait the same way.
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  if (tr) {
+    p.trace[cta * 5 + 0] = gtimer();
+    p.trace[cta * 5 + 4] = smid() | ((unsigned long long)blockIdx.x << 16);
+  }
 
   // producer cursor (the group's thread 0): the group's iterations are
   // j = group, group + GROUPS, ... and stage j % STAGES is always its own

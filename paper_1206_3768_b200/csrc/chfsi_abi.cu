@@ -306,7 +306,8 @@ int chfsi_filter_degrees_z(chfsi_ctx* ctx, int n, int w, const void* H, long lon
     const chfsi::StepTiling tiling = ctx->tiling.bm ? ctx->tiling : chfsi::choose_step_tiling(n, wa);
     CK_CUDA(chfsi::cheb_step_launch(hh, ldh, conj_h != 0, cur + first * ldcur, ldcur,
                                     prev ? prev + first * ldp : nullptr, ldp, dst + first * ldb, ldb,
-                                    n, wa, al[j], c, be[j], tiling, ctx->step_ws, ctx->stream));
+                                    n, wa, al[j], c, be[j], tiling, ctx->step_ws, ctx->stream,
+                                    /*pdl=*/j > 0));
     prev = cur;
     ldp = ldcur;
     cur = dst;
@@ -364,7 +365,7 @@ int filter_range(chfsi_ctx* ctx, cudaStream_t stream, const chfsi::StepWorkspace
   for (int j = 0; j < deg; ++j) {
     double2* dst = ((j % 2 == 0) ? buf_a : buf_b) + (long long)c0 * ldb;
     CK_CUDA(chfsi::cheb_step_launch(hh, ldh, conj, cur, ldcur, prev, ldp, dst, ldb, n, w, al[j], c,
-                                    be[j], tiling, ws, stream));
+                                    be[j], tiling, ws, stream, /*pdl=*/j > 0));
     prev = cur;
     ldp = ldcur;
     cur = dst;

@@ -43,7 +43,8 @@ int step_grid_size(int bn, bool conj);
 cudaError_t cheb_step_launch(const double2* h, long long ldh, bool conj_h, const double2* ycur,
                              long long ldc, const double2* yprev, long long ldp, double2* ynext,
                              long long ldn, int n, int w, double alpha, double c, double beta,
-                             StepTiling tiling, const StepWorkspace& ws, cudaStream_t stream);
+                             StepTiling tiling, const StepWorkspace& ws, cudaStream_t stream,
+                             bool pdl = false);
 
 // Row shard of K1 for the multi-GPU filter: compute `rows` output rows
 // (H points at the shard's first row); Ycur may be in the rank-blocked
@@ -65,7 +66,7 @@ cudaError_t cheb_step_rows_launch(const double2* h, long long ldh, bool conj_h, 
                                   long long ldn, int n, int w, double alpha, double c, double beta,
                                   const RowShard& shard, StepTiling tiling, const StepWorkspace& ws,
                                   cudaStream_t stream, const long long* peer_shift = nullptr,
-                                  int npeer = 0);
+                                  int npeer = 0, bool pdl = false);
 
 // ---- auxiliary kernels (aux_kernels.cu) ----
 // u = op(H) q for a row-major H (conj_h: conj(H)).
