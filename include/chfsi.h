@@ -333,6 +333,15 @@ typedef struct chfsi_loop {
   long long filter_degree_sum;  /* sum over passes and columns of the filter degree */
   double filter_flops;
   double t_filter, t_ortho, t_rr; /* seconds */
+  /* in: 1 = from the second pass on, the filter's first step reuses H*P of the
+   * previous Rayleigh-Ritz (rotated, unlocked columns == H * the next panel
+   * to rounding), so it is elementwise instead of a K1 product (single GPU,
+   * fixed degree; ignored with `filter`, `allreduce` or `adaptive`) */
+  int reuse_hp;
+  /* out: K1 launches / FLOPs the filter actually executed (filter_launches
+   * and filter_flops stay the algorithmic deg-per-pass counts) */
+  long long filter_k1_launches;
+  double filter_k1_flops;
 } chfsi_loop;
 
 CHFSI_API int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* loop);

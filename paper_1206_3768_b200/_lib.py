@@ -127,6 +127,7 @@ class LoopState(ctypes.Structure):
         ("filter_launches", _ll), ("rr_fast_eigs", _ll), ("filter_degree_sum", _ll),
         ("filter_flops", _d),
         ("t_filter", _d), ("t_ortho", _d), ("t_rr", _d),
+        ("reuse_hp", _i), ("filter_k1_launches", _ll), ("filter_k1_flops", _d),
     ]
 
 

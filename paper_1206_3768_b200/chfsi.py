@@ -21,6 +21,7 @@ Generator in exactly the reference order so iteration counts match.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 import time
 from dataclasses import dataclass, field
@@ -150,6 +151,10 @@ class SolveReport:
     t_rr: float = 0.0
     filter_flops: float = 0.0
     filter_launches: int = 0
+    # K1 work the filter actually executed: from the second pass on its first
+    # step reuses the previous Rayleigh-Ritz's H*P (elementwise, no product)
+    filter_k1_flops: float = 0.0
+    filter_k1_launches: int = 0
     rr_fast_eigs: int = 0
     filter_degree_sum: int = 0  # sum of per-column degrees (= deg * filtered_vectors unless adaptive)
     tail_vectors: object = None
@@ -601,6 +606,7 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     # near-diagonal Rayleigh-Ritz eigensolver first (bails out to zheevd when
     # the projection is not close to diagonal)
     st.rr_fast_tol = RR_FAST_TOL if tol >= 1e-11 else 0.0
+    st.reuse_hp = 0 if os.environ.get("CHFSI_REUSE_HP") == "0" else 1
     st.H, st.ldh, st.conj_h = op.tensor.data_ptr(), op.ld, int(op.conj)
     st.bufs[0], st.bufs[1] = bufs[0].data_ptr(), bufs[1].data_ptr()
     st.hp, st.hp_rot, st.locked = hp_buf.data_ptr(), hp_rot.data_ptr(), locked.data_ptr()
@@ -644,6 +650,8 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     report.residual_check_matvecs = int(st.residual_check_matvecs)
     report.filter_launches = int(st.filter_launches)
     report.filter_flops = float(st.filter_flops)
+    report.filter_k1_launches = int(st.filter_k1_launches)
+    report.filter_k1_flops = float(st.filter_k1_flops)
     report.filter_degree_sum = int(st.filter_degree_sum)
     report.rr_fast_eigs = int(st.rr_fast_eigs)
     report.converged = bool(st.converged)

@@ -47,6 +47,13 @@ namespace chfsi {
 // Page-locked host buffer of at least `bytes` owned by the context (for the
 // small device->host readbacks that drive host decisions).
 int ensure_pinned(chfsi_ctx* ctx, size_t bytes);
+// chfsi_filter_z with an optional known first product hy0 = H y0 (ld ldhy0):
+// the first recurrence step is then elementwise (the native loop passes the
+// previous Rayleigh-Ritz's rotated H P)
+int filter_z_impl(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, int conj_h,
+                  const void* y0, long long ldy0, const void* hy0, long long ldhy0, void* buf_a,
+                  void* buf_b, long long ldb, int deg, double a, double b, double scale_ref,
+                  void** result);
 // Records `msg` as this thread's chfsi_last_error() and returns `code`.
 int fail(int code, const std::string& msg);
 }  // namespace chfsi

@@ -431,6 +431,26 @@ __global__ void __launch_bounds__(kNiThreads) near_identity_update_kernel(
   }
 }
 
+// First Chebyshev step from a known product HY = H Y0 (columns j of n x w
+// blocks): Y1 = alpha (HY - c Y0), K1's epilogue arithmetic in the same
+// order (the step has no Yprev term).
+__global__ void cheb_first_step_kernel(const double2* hy, long long ldhy, const double2* y0,
+                                       long long ldy, double2* out, long long ldo, int n, int w,
+                                       double alpha, double c) {
+  const long long total = (long long)n * w;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(e / n), i = (int)(e - (long long)j * n);
+    const double2 a = hy[(long long)j * ldhy + i], y = y0[(long long)j * ldy + i];
+    double tr = a.x, ti = a.y;
+    if (c != 0.0) {
+      tr = __dsub_rn(tr, __dmul_rn(c, y.x));
+      ti = __dsub_rn(ti, __dmul_rn(c, y.y));
+    }
+    out[(long long)j * ldo + i] = make_double2(__dmul_rn(alpha, tr), __dmul_rn(alpha, ti));
+  }
+}
+
 inline int grid_for(long long total, int threads, int cap = kNumSMs * 16) {
   long long g = (total + threads - 1) / threads;
   if (g > cap) g = cap;
@@ -599,6 +619,16 @@ cudaError_t diag_accumulate_launch(const double2* r, long long ldr, int n, doubl
   if (n <= 0) return cudaSuccess;
   note_launch();
   diag_accumulate_kernel<<<(n + 255) / 256, 256, 0, s>>>(r, ldr, n, acc, first ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t cheb_first_step_launch(const double2* hy, long long ldhy, const double2* y0, long long ldy,
+                                   double2* out, long long ldo, int n, int w, double alpha, double c,
+                                   cudaStream_t s) {
+  if (n <= 0 || w <= 0) return cudaSuccess;
+  note_launch();
+  cheb_first_step_kernel<<<grid_for((long long)n * w, 256), 256, 0, s>>>(hy, ldhy, y0, ldy, out, ldo,
+                                                                         n, w, alpha, c);
   return cudaGetLastError();
 }
 

@@ -357,15 +357,20 @@ namespace {
 int filter_range(chfsi_ctx* ctx, cudaStream_t stream, const chfsi::StepWorkspace& ws,
                  chfsi::StepTiling tiling, int n, int c0, int w, const double2* hh, long long ldh,
                  bool conj, const double2* y0, long long ldy0, double2* buf_a, double2* buf_b,
-                 long long ldb, int deg, const double* al, const double* be, double c) {
+                 long long ldb, int deg, const double* al, const double* be, double c,
+                 const double2* hy0 = nullptr, long long ldhy0 = 0) {
   const double2* prev = nullptr;
   long long ldp = 0;
   const double2* cur = y0 + (long long)c0 * ldy0;
   long long ldcur = ldy0;
   for (int j = 0; j < deg; ++j) {
     double2* dst = ((j % 2 == 0) ? buf_a : buf_b) + (long long)c0 * ldb;
-    CK_CUDA(chfsi::cheb_step_launch(hh, ldh, conj, cur, ldcur, prev, ldp, dst, ldb, n, w, al[j], c,
-                                    be[j], tiling, ws, stream, /*pdl=*/j > 0));
+    if (j == 0 && hy0)  // H Y0 known (the previous Rayleigh-Ritz's rotated H P)
+      CK_CUDA(chfsi::cheb_first_step_launch(hy0 + (long long)c0 * ldhy0, ldhy0, cur, ldcur, dst, ldb,
+                                            n, w, al[0], c, stream));
+    else
+      CK_CUDA(chfsi::cheb_step_launch(hh, ldh, conj, cur, ldcur, prev, ldp, dst, ldb, n, w, al[j], c,
+                                      be[j], tiling, ws, stream, /*pdl=*/j > 1 || (j == 1 && !hy0)));
     prev = cur;
     ldp = ldcur;
     cur = dst;
@@ -393,6 +398,18 @@ int ensure_aux_stream(chfsi_ctx* ctx) {
 int chfsi_filter_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, int conj_h,
                    const void* y0, long long ldy0, void* buf_a, void* buf_b, long long ldb,
                    int deg, double a, double b, double scale_ref, void** result) {
+  return chfsi::filter_z_impl(ctx, n, w, H, ldh, conj_h, y0, ldy0, nullptr, 0, buf_a, buf_b, ldb, deg,
+                              a, b, scale_ref, result);
+}
+
+}  // extern "C"
+
+namespace chfsi {
+
+int filter_z_impl(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, int conj_h,
+                  const void* y0, long long ldy0, const void* hy0_, long long ldhy0, void* buf_a,
+                  void* buf_b, long long ldb, int deg, double a, double b, double scale_ref,
+                  void** result) {
   CK_ARG(ctx, "ctx is NULL");
   CK_ARG(deg >= 1, "polynomial degree must be >= 1");
   CK_ARG(n >= 0 && w >= 0, "negative size");
@@ -407,6 +424,7 @@ int chfsi_filter_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, i
   const double2* yy = static_cast<const double2*>(y0);
   double2* ba = static_cast<double2*>(buf_a);
   double2* bb = static_cast<double2*>(buf_b);
+  const double2* hy0 = static_cast<const double2*>(hy0_);
   static const int env_chains = [] {
     const char* e = getenv("CHFSI_FILTER_STREAMS");  // 1 disables the two-chain filter
     return e ? atoi(e) : 2;
@@ -444,9 +462,9 @@ int chfsi_filter_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, i
       CK_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
       CK_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ctx->fork_ev, 0));
       CK(filter_range(ctx, ctx->stream, ctx->step_ws, t0, n, 0, w0, hh, ldh, conj_h != 0, yy, ldy0,
-                      ba, bb, ldb, deg, al.data(), be.data(), c));
+                      ba, bb, ldb, deg, al.data(), be.data(), c, hy0, ldhy0));
       CK(filter_range(ctx, ctx->aux_stream, ctx->step_ws2, t1, n, w0, w1, hh, ldh, conj_h != 0, yy,
-                      ldy0, ba, bb, ldb, deg, al.data(), be.data(), c));
+                      ldy0, ba, bb, ldb, deg, al.data(), be.data(), c, hy0, ldhy0));
       CK_CUDA(cudaEventRecord(ctx->join_ev, ctx->aux_stream));
       CK_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
       return CHFSI_OK;
@@ -455,8 +473,12 @@ int chfsi_filter_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, i
   const chfsi::StepTiling tiling =
       ctx->tiling.bm ? ctx->tiling : chfsi::choose_step_tiling(n, w);
   return filter_range(ctx, ctx->stream, ctx->step_ws, tiling, n, 0, w, hh, ldh, conj_h != 0, yy,
-                      ldy0, ba, bb, ldb, deg, al.data(), be.data(), c);
+                      ldy0, ba, bb, ldb, deg, al.data(), be.data(), c, hy0, ldhy0);
 }
+
+}  // namespace chfsi
+
+extern "C" {
 
 int chfsi_debug_k1_trace(unsigned long long* host, int max_ctas) {
   CK_ARG(host && max_ctas >= 0, "bad argument");

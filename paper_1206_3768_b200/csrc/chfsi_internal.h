@@ -148,6 +148,10 @@ cudaError_t nd_gather_cols_launch(const double2* src, long long lds, int m, int 
                                   double2* out, long long ldo, cudaStream_t s);
 // y = x / *d (complex / real, round-to-nearest division)
 cudaError_t div_scalar_launch(const double2* x, const double* d, double2* y, int n, cudaStream_t s);
+// Y1 = alpha (HY - c Y0): the first filter step when H Y0 is already known
+cudaError_t cheb_first_step_launch(const double2* hy, long long ldhy, const double2* y0, long long ldy,
+                                   double2* out, long long ldo, int n, int w, double alpha, double c,
+                                   cudaStream_t s);
 // Linearised second Cholesky-QR pass: G = Q1^H Q1 = I + E -> M = I - tri(E)
 // in place (upper; tri = strict upper + diag/2), out[0] = max|E_ij|,
 // acc[i] *= 1 + E_ii/2, last[i] = 1 + E_ii/2 (the R2 diagonal to O(|E|^2)).

@@ -236,6 +236,10 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
   CK(chfsi::ensure_pinned(ctx, 2 * (size_t)L->blk * sizeof(double) + (size_t)L->blk * sizeof(int)));
   bool have_degs = false;
   std::vector<int> dtmp, order;
+  // H * (next panel) from the previous pass's Rayleigh-Ritz: hp_rot columns
+  // [n_lock, width) are H P_rot for exactly the columns the next panel keeps
+  const bool reuse = L->reuse_hp && !dist && !L->filter && !L->adaptive;
+  bool hp_ready = false;
 
   while (L->inner_loops < L->max_repeats) {
     L->inner_loops += 1;
@@ -255,9 +259,15 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
       CK(chfsi_filter_degrees_z(ctx, n, width, L->H, L->ldh, L->conj_h, panel, n, other, panel, n,
                                 degs, L->win_a, L->win_b, L->win_scale_ref, &result));
     } else {
-      CK(chfsi_filter_z(ctx, n, width, L->H, L->ldh, L->conj_h, panel, n, other, panel, n, L->deg,
-                        L->win_a, L->win_b, L->win_scale_ref, &result));
+      const void* hy0 = hp_ready ? col(L->hp_rot, nl, L->off) : nullptr;
+      CK(chfsi::filter_z_impl(ctx, n, width, L->H, L->ldh, L->conj_h, panel, n, hy0, n, other, panel,
+                              n, L->deg, L->win_a, L->win_b, L->win_scale_ref, &result));
+      if (hy0) {  // one elementwise step instead of a K1 product
+        L->filter_k1_launches -= 1;
+        L->filter_k1_flops -= 8.0 * (double)n * (double)n * (double)width;
+      }
     }
+    hp_ready = false;
     CK_CUDA(cudaEventRecord(ev[1], s));
     long long dsum = (long long)L->deg * width;
     if (degs) {
@@ -269,6 +279,8 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
     L->matvecs += dsum;
     L->filter_degree_sum += dsum;
     L->filter_flops += 8.0 * (double)n * (double)n * (double)dsum;
+    L->filter_k1_launches += degs ? degs[width - 1] : L->deg;
+    L->filter_k1_flops += 8.0 * (double)n * (double)n * (double)dsum;
     const bool q_in_other = result == other;
 
     // ---- orthonormalize (chfsi.py:335-336)
@@ -328,6 +340,7 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
     }
 
     // ---- next panel and window (chfsi.py:367-373)
+    hp_ready = reuse;  // hp_rot[:, n_lock:width] = H * the next panel
     L->pb = rot_pb;
     L->off = n_lock;
     L->width = width - n_lock;

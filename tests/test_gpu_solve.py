@@ -92,6 +92,33 @@ def test_deterministic_given_seed(pkg):
     assert torch.equal(s1.vectors, s2.vectors)
 
 
+@pytest.mark.parametrize("n,nev,blk,deg", [(300, 20, 36, 10), (700, 48, 64, 14)])
+def test_hp_reuse_matches_fresh_first_step(pkg, monkeypatch, n, nev, blk, deg):
+    """From the second pass on the filter's first step reuses the previous
+    Rayleigh-Ritz's rotated H*P (== H * next panel to rounding): the solve
+    matches the one that recomputes it, loop for loop, and the report's K1
+    work drops by one step per pass after the first."""
+    rng = np.random.default_rng(n + blk)
+    h = random_hermitian(rng, n)
+    cfg = pkg.ChfsiConfig(nev=nev, blk=blk, deg=deg)
+    monkeypatch.setenv("CHFSI_REUSE_HP", "0")
+    s0, r0 = pkg.chfsi_solve(h, cfg, rng=5)
+    monkeypatch.setenv("CHFSI_REUSE_HP", "1")
+    s1, r1 = pkg.chfsi_solve(h, cfg, rng=5)
+    assert r0.converged and r1.converged
+    assert r1.locked_per_loop == r0.locked_per_loop and r1.matvecs == r0.matvecs
+    assert np.abs(s1.values - s0.values).max() <= 1e-12 * np.abs(s0.values).max()
+    assert subspace_sines(s0.vectors_host(), s1.vectors_host()).max() <= 1e-8
+    assert r0.filter_k1_flops == r0.filter_flops
+    widths = [0] * r1.inner_loops  # panel width per pass: blk, then minus the locked
+    w = blk
+    for i, k in enumerate(r1.locked_per_loop):
+        widths[i] = w
+        w -= k
+    assert r1.filter_k1_flops == r1.filter_flops - 8.0 * n * n * sum(widths[1:])
+    assert r1.filter_k1_launches == r1.filter_launches - (r1.inner_loops - 1)
+
+
 def test_guess_width_validated(pkg):
     h = random_hermitian(np.random.default_rng(1), 40)
     bad = pkg.ChfsiGuess(vectors=np.ones((40, 9), dtype=complex), lambda1=0.0,
