@@ -305,6 +305,7 @@ def run_ours(args):
     step_stats = []
     res = None
     step_ev = [e0]
+    step_detail = []  # per step: each problem's solve time (host wall, ms)
     for _ in range(args.steps):
         res = None  # release the previous step's solutions first
         res = device_step()
@@ -312,6 +313,7 @@ def run_ours(args):
         # the previous Rayleigh-Ritz's H*P and runs no product)
         step_stats.append([(r.report.t_filter, r.report.filter_k1_flops, r.report.filter_k1_launches)
                            for r in res])
+        step_detail.append([round(r.t_solve * 1e3, 1) for r in res])
         ev = torch.cuda.Event(enable_timing=True)
         ev.record()
         step_ev.append(ev)
@@ -420,6 +422,7 @@ def run_ours(args):
         },
         "time_to_solution_s": t_dev / args.steps,
         "step_ms": step_ms,
+        "step_problem_ms": step_detail,
         "filter_kernel_gflops": achieved * 1e3,
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

@@ -54,6 +54,11 @@ int filter_z_impl(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, in
                   const void* y0, long long ldy0, const void* hy0, long long ldhy0, void* buf_a,
                   void* buf_b, long long ldb, int deg, double a, double b, double scale_ref,
                   void** result);
+// chfsi_filter_degrees_z with the same optional known first product
+int filter_degrees_impl(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, int conj_h,
+                        const void* y0, long long ldy0, const void* hy0, long long ldhy0,
+                        void* buf_a, void* buf_b, long long ldb, const int* degs, double a, double b,
+                        double scale_ref, void** result);
 // Records `msg` as this thread's chfsi_last_error() and returns `code`.
 int fail(int code, const std::string& msg);
 }  // namespace chfsi

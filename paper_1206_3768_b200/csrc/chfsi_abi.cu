@@ -272,6 +272,18 @@ int chfsi_cheb_step_rows_peers_z(chfsi_ctx* ctx, int n, int rows, int w, const v
 int chfsi_filter_degrees_z(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, int conj_h,
                            const void* y0, long long ldy0, void* buf_a, void* buf_b, long long ldb,
                            const int* degs, double a, double b, double scale_ref, void** result) {
+  return chfsi::filter_degrees_impl(ctx, n, w, H, ldh, conj_h, y0, ldy0, nullptr, 0, buf_a, buf_b,
+                                    ldb, degs, a, b, scale_ref, result);
+}
+
+}  // extern "C"
+
+namespace chfsi {
+
+int filter_degrees_impl(chfsi_ctx* ctx, int n, int w, const void* H, long long ldh, int conj_h,
+                        const void* y0, long long ldy0, const void* hy0_, long long ldhy0,
+                        void* buf_a, void* buf_b, long long ldb, const int* degs, double a, double b,
+                        double scale_ref, void** result) {
   CK_ARG(ctx, "ctx is NULL");
   CK_ARG(n >= 0 && w >= 0, "negative size");
   CK_ARG(result, "result is NULL");
@@ -304,10 +316,15 @@ int chfsi_filter_degrees_z(chfsi_ctx* ctx, int n, int w, const void* H, long lon
     double2* dst = static_cast<double2*>((j % 2 == 0) ? buf_a : buf_b);
     const int wa = w - first;
     const chfsi::StepTiling tiling = ctx->tiling.bm ? ctx->tiling : chfsi::choose_step_tiling(n, wa);
-    CK_CUDA(chfsi::cheb_step_launch(hh, ldh, conj_h != 0, cur + first * ldcur, ldcur,
-                                    prev ? prev + first * ldp : nullptr, ldp, dst + first * ldb, ldb,
-                                    n, wa, al[j], c, be[j], tiling, ctx->step_ws, ctx->stream,
-                                    /*pdl=*/j > 0));
+    const double2* hy0 = static_cast<const double2*>(hy0_);
+    if (j == 0 && hy0)  // H Y0 known: elementwise first step
+      CK_CUDA(chfsi::cheb_first_step_launch(hy0 + first * ldhy0, ldhy0, cur + first * ldcur, ldcur,
+                                            dst + first * ldb, ldb, n, wa, al[0], c, ctx->stream));
+    else
+      CK_CUDA(chfsi::cheb_step_launch(hh, ldh, conj_h != 0, cur + first * ldcur, ldcur,
+                                      prev ? prev + first * ldp : nullptr, ldp, dst + first * ldb,
+                                      ldb, n, wa, al[j], c, be[j], tiling, ctx->step_ws, ctx->stream,
+                                      /*pdl=*/j > 1 || (j == 1 && !hy0)));
     prev = cur;
     ldp = ldcur;
     cur = dst;
@@ -329,6 +346,10 @@ int chfsi_filter_degrees_z(chfsi_ctx* ctx, int n, int w, const void* H, long lon
   }
   return CHFSI_OK;
 }
+
+}  // namespace chfsi
+
+extern "C" {
 
 int chfsi_filter_coeffs(int deg, double a, double b, double scale_ref, double* c, double* alphas,
                         double* betas) {

@@ -238,7 +238,8 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
   std::vector<int> dtmp, order;
   // H * (next panel) from the previous pass's Rayleigh-Ritz: hp_rot columns
   // [n_lock, width) are H P_rot for exactly the columns the next panel keeps
-  const bool reuse = L->reuse_hp && !dist && !L->filter && !L->adaptive;
+  const bool reuse = L->reuse_hp && !dist && !L->filter;
+  const void* hy_next = nullptr;  // H * (next panel): hp_rot columns, or hp after an adaptive gather
   bool hp_ready = false;
 
   while (L->inner_loops < L->max_repeats) {
@@ -256,10 +257,15 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
                     L->win_scale_ref, &result) != 0 || !result)
         return fail(CHFSI_EINVAL, "filter callback failed");
     } else if (degs) {
-      CK(chfsi_filter_degrees_z(ctx, n, width, L->H, L->ldh, L->conj_h, panel, n, other, panel, n,
-                                degs, L->win_a, L->win_b, L->win_scale_ref, &result));
+      const void* hy0 = hp_ready ? hy_next : nullptr;
+      CK(chfsi::filter_degrees_impl(ctx, n, width, L->H, L->ldh, L->conj_h, panel, n, hy0, n, other,
+                                    panel, n, degs, L->win_a, L->win_b, L->win_scale_ref, &result));
+      if (hy0) {
+        L->filter_k1_launches -= 1;
+        L->filter_k1_flops -= 8.0 * (double)n * (double)n * (double)width;
+      }
     } else {
-      const void* hy0 = hp_ready ? col(L->hp_rot, nl, L->off) : nullptr;
+      const void* hy0 = hp_ready ? hy_next : nullptr;
       CK(chfsi::filter_z_impl(ctx, n, width, L->H, L->ldh, L->conj_h, panel, n, hy0, n, other, panel,
                               n, L->deg, L->win_a, L->win_b, L->win_scale_ref, &result));
       if (hy0) {  // one elementwise step instead of a K1 product
@@ -341,6 +347,7 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
 
     // ---- next panel and window (chfsi.py:367-373)
     hp_ready = reuse;  // hp_rot[:, n_lock:width] = H * the next panel
+    hy_next = col(L->hp_rot, nl, n_lock);
     L->pb = rot_pb;
     L->off = n_lock;
     L->width = width - n_lock;
@@ -370,6 +377,11 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
         CK_CUDA(cudaMemcpyAsync(L->perm_d, hperm, (size_t)wn * sizeof(int), cudaMemcpyHostToDevice, s));
         CK_CUDA(chfsi::nd_gather_cols_launch(col(L->bufs[L->pb], nl, L->off), nl, nl, wn, L->perm_d,
                                              static_cast<double2*>(L->bufs[1 - L->pb]), nl, s));
+        if (hp_ready) {  // H * panel in the same column order (hp is free until Rayleigh-Ritz)
+          CK_CUDA(chfsi::nd_gather_cols_launch(static_cast<const double2*>(hy_next), nl, nl, wn,
+                                               L->perm_d, static_cast<double2*>(L->hp), nl, s));
+          hy_next = L->hp;
+        }
         L->pb = 1 - L->pb;
         L->off = 0;
       }

@@ -92,15 +92,16 @@ def test_deterministic_given_seed(pkg):
     assert torch.equal(s1.vectors, s2.vectors)
 
 
-@pytest.mark.parametrize("n,nev,blk,deg", [(300, 20, 36, 10), (700, 48, 64, 14)])
-def test_hp_reuse_matches_fresh_first_step(pkg, monkeypatch, n, nev, blk, deg):
+@pytest.mark.parametrize("n,nev,blk,deg,adaptive", [(300, 20, 36, 10, False), (700, 48, 64, 14, False),
+                                                    (700, 48, 64, 24, True)])
+def test_hp_reuse_matches_fresh_first_step(pkg, monkeypatch, n, nev, blk, deg, adaptive):
     """From the second pass on the filter's first step reuses the previous
     Rayleigh-Ritz's rotated H*P (== H * next panel to rounding): the solve
     matches the one that recomputes it, loop for loop, and the report's K1
     work drops by one step per pass after the first."""
     rng = np.random.default_rng(n + blk)
     h = random_hermitian(rng, n)
-    cfg = pkg.ChfsiConfig(nev=nev, blk=blk, deg=deg)
+    cfg = pkg.ChfsiConfig(nev=nev, blk=blk, deg=deg, adaptive_degree=adaptive)
     monkeypatch.setenv("CHFSI_REUSE_HP", "0")
     s0, r0 = pkg.chfsi_solve(h, cfg, rng=5)
     monkeypatch.setenv("CHFSI_REUSE_HP", "1")
