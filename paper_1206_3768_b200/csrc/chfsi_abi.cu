@@ -695,20 +695,39 @@ int qr_cholqr(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdia
   const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
   // unit roundoff 2^-53; Fukaya's shift 11 (mn + n(n+1)) u ||Y||_2^2 with ||Y||_F >= ||Y||_2
   const double shift_coef = 11.0 * ((double)m * n + (double)n * (n + 1)) * 1.1102230246251565e-16;
+  // Shape-dependent library choices (profiles/r01_qr_bench.log): the Gram by
+  // ZHERK from w >= 1000 (12000 x 1400: 3.2 vs 5.3 ms; ZGEMM wins below, e.g.
+  // 2048 x 160: 25 vs 76 us), and the linearised pass's Q1 M by out-of-place
+  // ZTRMM from w >= 400 (5000 x 600: 0.28 vs 0.43 ms; 2048 x 160: ZGEMM 23 vs 26 us).
+  const bool herk = n >= 1000, trmm = n >= 400;
   for (int pass = 0; pass < passes; ++pass) {
-    CK_BLAS(cublasZgemm(ctx->blas, CUBLAS_OP_C, CUBLAS_OP_N, n, n, m, &one,
-                        reinterpret_cast<const cuDoubleComplex*>(y), m,
-                        reinterpret_cast<const cuDoubleComplex*>(y), m, &zero,
-                        reinterpret_cast<cuDoubleComplex*>(g), n));
+    const bool lin = linear2 && pass == 1;
+    if (herk) {  // lower triangle for potrf, upper for the near-identity kernel
+      const double done = 1.0, dzero = 0.0;
+      CK_BLAS(cublasZherk(ctx->blas, lin ? CUBLAS_FILL_MODE_UPPER : CUBLAS_FILL_MODE_LOWER,
+                          CUBLAS_OP_C, n, m, &done, reinterpret_cast<const cuDoubleComplex*>(y), m,
+                          &dzero, reinterpret_cast<cuDoubleComplex*>(g), n));
+    } else {
+      CK_BLAS(cublasZgemm(ctx->blas, CUBLAS_OP_C, CUBLAS_OP_N, n, n, m, &one,
+                          reinterpret_cast<const cuDoubleComplex*>(y), m,
+                          reinterpret_cast<const cuDoubleComplex*>(y), m, &zero,
+                          reinterpret_cast<cuDoubleComplex*>(g), n));
+    }
     if (shifted && pass == 0) CK_CUDA(chfsi::add_diag_shift_launch(g, n, n, fro, shift_coef, s));
     if (linear2 && pass == 1) {
       CK_CUDA(chfsi::near_identity_update_launch(g, n, n, rdiag_acc, rlast, eps_dev, s));
       // Q = Q1 M out of place (ZGEMM + copy back: 2048 x 160 27 us vs 47 us
       // for cuBLAS's in-place ZTRMM; M's strict lower triangle is zero)
-      CK_BLAS(cublasZgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, m, n, n, &one,
-                          reinterpret_cast<const cuDoubleComplex*>(y), m,
-                          reinterpret_cast<const cuDoubleComplex*>(g), n, &zero,
-                          reinterpret_cast<cuDoubleComplex*>(tmp), m));
+      if (trmm)
+        CK_BLAS(cublasZtrmm(ctx->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
+                            CUBLAS_DIAG_NON_UNIT, m, n, &one, reinterpret_cast<const cuDoubleComplex*>(g),
+                            n, reinterpret_cast<const cuDoubleComplex*>(y), m,
+                            reinterpret_cast<cuDoubleComplex*>(tmp), m));
+      else
+        CK_BLAS(cublasZgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, m, n, n, &one,
+                            reinterpret_cast<const cuDoubleComplex*>(y), m,
+                            reinterpret_cast<const cuDoubleComplex*>(g), n, &zero,
+                            reinterpret_cast<cuDoubleComplex*>(tmp), m));
       CK_CUDA(cudaMemcpyAsync(y, tmp, (size_t)m * n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
       continue;
     }

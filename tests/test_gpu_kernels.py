@@ -341,7 +341,7 @@ def test_cholqr3_matches_householder(pkg, kind, mode):
     assert np.abs(qc - ref).max() <= 1e-13 * cond * 10
 
 
-@pytest.mark.parametrize("kind", ["random", "moderate", "graded", "tall_wide"])
+@pytest.mark.parametrize("kind", ["random", "moderate", "graded", "tall_wide", "herk_trmm"])
 def test_cholqr2_linearised_second_pass(pkg, kind):
     """Cholesky-QR2's linearised second pass (Q = Q1 (I - tri(Q1^H Q1 - I)),
     taken when the first pass leaves |Q1^H Q1 - I| <= 1e-8; the graded panel
@@ -349,7 +349,8 @@ def test_cholqr2_linearised_second_pass(pkg, kind):
     pass and as Householder to rounding x cond, orthonormal to 1e-13."""
     L = _lib()
     rng = np.random.default_rng(77)
-    m, n = {"tall_wide": (2048, 160)}.get(kind, (600, 48))
+    # herk_trmm: w >= 1000 takes the ZHERK Gram and the out-of-place ZTRMM
+    m, n = {"tall_wide": (2048, 160), "herk_trmm": (2500, 1024)}.get(kind, (600, 48))
     y = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
     cond = 1.0
     if kind == "moderate":  # the filtered panels' regime: R diagonal ranging over ~50
