@@ -23,7 +23,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .chfsi import ChfsiConfig, ChfsiGuess, chfsi_solve
+from .chfsi import ChfsiConfig, ChfsiGuess, PrefetchedStart, chfsi_solve
 from .linalg import hermitian_eig
 from .reduction import EigenPencil, EigenSolution, back_transform, stage_standard, to_standard
 
@@ -160,8 +160,14 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
     it = iter(pencils)
     first = next(it, None)
     staged = _stage(first, side) if first is not None else None
+    prefetch = None
     if staged is not None:
         _reserve_outputs(staged[0], cfg, pencils)
+        # problem 1 is a cold start: its draws (q0, then the n x blk block)
+        # run on a host thread from here on, behind its upload and reduction
+        p0 = staged[0]
+        prefetch = PrefetchedStart(np.random.default_rng((seed, p0.label, 0)), p0.n,
+                                   cfg.resolve(p0.n)[0])
     while staged is not None:
         t0 = time.perf_counter()
         pencil, sp, ev, checks = staged
@@ -180,6 +186,8 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
             raise ValueError(f"chfsi warm starts need blk < n (blk={blk}, n={n})")
         start = 0 if guess is None else 1
         rng = np.random.default_rng((seed, pencil.label, start))
+        if prefetch is not None:  # (always problem 1: guess is None there)
+            rng, prefetch = prefetch, None
         sol, rep = chfsi_solve(sp.h, cfg, guess=guess, rng=rng, label=pencil.label, shard=shard)
         t2 = time.perf_counter()
         gsol = back_transform(sp.cholesky_factor, sol, inplace=not keep_standard)
