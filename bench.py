@@ -317,7 +317,7 @@ def run_ours(args):
     step_stats = []
     res = None
     step_ev = [e0]
-    step_detail = []  # per step: each problem's solve time (host wall, ms)
+    step_detail = []  # per step: each problem's solve time, then the rest of the driver (host wall, ms)
     for _ in range(args.steps):
         res = None  # release the previous step's solutions first
         res = device_step()
@@ -325,7 +325,9 @@ def run_ours(args):
         # the previous Rayleigh-Ritz's H*P and runs no product)
         step_stats.append([(r.report.t_filter, r.report.filter_k1_flops, r.report.filter_k1_launches)
                            for r in res])
-        step_detail.append([round(r.t_solve * 1e3, 1) for r in res])
+        step_detail.append([round(r.t_solve * 1e3, 1) for r in res]
+                           + [round(sum(r.t_reduce + r.t_back + r.extra.get("t_stage_next", 0.0)
+                                        for r in res) * 1e3, 1)])
         ev = torch.cuda.Event(enable_timing=True)
         ev.record()
         step_ev.append(ev)

@@ -180,6 +180,8 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
         t1 = time.perf_counter()
         nxt = next(it, None)
         staged = _stage(nxt, side) if nxt is not None else None
+        t_stage = time.perf_counter() - t1
+        t1 = time.perf_counter()
         n = pencil.n
         blk = cfg.resolve(n)[0]
         if mode == "harness" and blk >= n:
@@ -195,7 +197,8 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
         t3 = time.perf_counter()
         res = ProblemResult(label=pencil.label, values=sol.values, solution=gsol,
                             standard_vectors=sol.vectors if keep_standard else None, report=rep,
-                            t_reduce=t1 - t0, t_solve=t2 - t1, t_back=t3 - t2)
+                            t_reduce=t1 - t0 - t_stage, t_solve=t2 - t1, t_back=t3 - t2)
+        res.extra["t_stage_next"] = t_stage
         if mode == "harness":
             dv, dvec = hermitian_eig(sp.h)
             res.dense_values = dv
