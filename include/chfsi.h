@@ -245,9 +245,16 @@ CHFSI_API int chfsi_to_standard_z(chfsi_ctx* ctx, int n, void* A, long long lda,
  * point; the caller raises the reference's exceptions then. */
 CHFSI_API int chfsi_to_standard_async_z(chfsi_ctx* ctx, int n, void* A, long long lda, void* B,
                                         long long ldb, int rowmajor_in, int* info_host);
+/* The same reduction with both triangular solves as block substitutions
+ * whose off-diagonal products run on K1 (3M DMMA) and whose nb x nb diagonal
+ * blocks use ZTRSM: Z = L^-1 A, then H = L^-1 Z^H (= Z L^-H). `work` is
+ * caller-owned device memory for 2 n^2 complex (L^H and Z^H). */
+CHFSI_API int chfsi_to_standard_k1_z(chfsi_ctx* ctx, int n, void* A, long long lda, void* B,
+                                     long long ldb, int rowmajor_in, void* work, int* info_host);
 CHFSI_API int chfsi_herm_defect_async_z(chfsi_ctx* ctx, int n, const void* A, long long lda,
                                         double* out_host);
-/* back_transform (reduction.py:122-134): Y <- L^-H Y in place. */
+/* back_transform (reduction.py:122-134): Y <- L^-H Y in place (backward block
+ * substitution, off-diagonal products on K1). */
 CHFSI_API int chfsi_back_transform_z(chfsi_ctx* ctx, int n, int nev, const void* L, long long ldl, void* Y,
                            long long ldy);
 

@@ -93,6 +93,7 @@ _SIGNATURES = {
     "chfsi_trsm_z": [_vp, _c, _c, _i, _i, _vp, _ll, _vp, _ll],
     "chfsi_to_standard_z": [_vp, _i, _vp, _ll, _vp, _ll, _i, _pi],
     "chfsi_to_standard_async_z": [_vp, _i, _vp, _ll, _vp, _ll, _i, _vp],
+    "chfsi_to_standard_k1_z": [_vp, _i, _vp, _ll, _vp, _ll, _i, _vp, _vp],
     "chfsi_herm_defect_async_z": [_vp, _i, _vp, _ll, _vp],
     "chfsi_back_transform_z": [_vp, _i, _i, _vp, _ll, _vp, _ll],
 }

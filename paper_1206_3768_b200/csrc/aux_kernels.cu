@@ -312,6 +312,27 @@ __global__ void herm_defect_kernel(const double2* __restrict__ a, long long lda,
   }
 }
 
+// dst = src^H (n x n, column-major both), tiled through shared memory
+__global__ void conj_transpose_kernel(const double2* src, long long lds, double2* dst, long long ldd,
+                                      int n) {
+  __shared__ double2 t[TS][TS + 1];
+  const int bi = blockIdx.y, bj = blockIdx.x;  // source tile (row block bi, col block bj)
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int c = ty; c < TS; c += 8) {
+    const int r = bi * TS + tx, col = bj * TS + c;
+    if (r < n && col < n) t[tx][c] = src[(long long)col * lds + r];
+  }
+  __syncthreads();
+  // dst tile (bj, bi): dst[r'][c'] = conj(src[c'][r'])
+  for (int c = ty; c < TS; c += 8) {
+    const int r = bj * TS + tx, col = bi * TS + c;
+    if (r < n && col < n) {
+      const double2 v = t[c][tx];
+      dst[(long long)col * ldd + r] = make_double2(v.x, -v.y);
+    }
+  }
+}
+
 __global__ void conj_inplace_kernel(double2* a, long long lda, int m, int n) {
   const long long total = (long long)m * n;
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -566,6 +587,15 @@ cudaError_t herm_defect_launch(const double2* a, long long lda, int n, double* o
   note_launch();
   herm_defect_kernel<<<dim3(nb, nb), dim3(32, 8), 0, s>>>(
       a, lda, n, reinterpret_cast<unsigned long long*>(out));
+  return cudaGetLastError();
+}
+
+cudaError_t conj_transpose_launch(const double2* src, long long lds, double2* dst, long long ldd, int n,
+                                  cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int nb = (n + TS - 1) / TS;
+  note_launch();
+  conj_transpose_kernel<<<dim3(nb, nb), dim3(32, 8), 0, s>>>(src, lds, dst, ldd, n);
   return cudaGetLastError();
 }
 

@@ -953,6 +953,79 @@ int heev_near_diag(chfsi_ctx* ctx, int n, double2* a, long long lda, double* w, 
 
 }  // namespace
 
+namespace {
+
+// Block size of the K1-based triangular solves (tuning: CHFSI_TRSM_NB).
+int trsm_nb() {
+  static const int nb = [] {
+    const char* e = getenv("CHFSI_TRSM_NB");
+    const int v = e ? atoi(e) : 256;
+    return v >= 32 ? v : 256;
+  }();
+  return nb;
+}
+
+// One K1 update on rows [r0, r0 + rows) of the n x m block R:
+//   R[r0:r0+rows, :] -= op(A) R[k0:k0+kc, :],  op(A)[r][k] = conj(S[(r0+r)*lds + k])
+// (S's column r0 + r, rows k0.., conjugated: the rows of L read through L^H's
+// column-major storage, or the rows of L^H through L's) — the epilogue
+// Ynext = alpha (acc - 0) - beta Yprev with alpha = beta = -1, in place.
+int k1_block_update(chfsi_ctx* ctx, int n, int m, const double2* S, long long lds, int r0, int rows,
+                    int k0, int kc, double2* R, long long ldr) {
+  if (kc <= 0 || rows <= 0 || m <= 0) return CHFSI_OK;
+  const chfsi::RowShard shard{rows, 0, 0, nullptr, 0};
+  chfsi::StepTiling tiling = chfsi::choose_step_tiling(n, m);
+  // few output tiles over a long contraction (the back-transform's 256 x nev
+  // blocks): cap the stream-K split at 4 CTAs per tile — spread over every
+  // resident CTA each owner folds dozens of partial tiles (37 -> ~15 us)
+  const long long tiles = (long long)((rows + tiling.bm - 1) / tiling.bm) * ((m + tiling.bn - 1) / tiling.bn);
+  if (tiles * 4 < chfsi::kNumSMs) tiling.split = (int)(tiles * 4);
+  CK_CUDA(chfsi::cheb_step_rows_launch(S + (long long)r0 * lds + k0, lds, /*conj=*/true, R + k0, ldr,
+                                       R + r0, ldr, R + r0, ldr, kc, m, -1.0, 0.0, -1.0, shard, tiling,
+                                       ctx->step_ws, ctx->stream));
+  return CHFSI_OK;
+}
+
+// L X = R in place (L lower, n x n; R n x m): forward block substitution,
+// the off-diagonal products on K1 (3M DMMA) reading the rows of L from
+// Lh = L^H, the nb x nb diagonal solves by cuBLAS ZTRSM (~0.45 us per row:
+// the latency of its sequential steps is the floor at n = 2048; a warp-per-
+// column substitution kernel measured slower still).
+int trsm_lower_k1(chfsi_ctx* ctx, int n, int m, const double2* L, long long ldl, const double2* Lh,
+                  long long ldlh, double2* R, long long ldr) {
+  const int nb = trsm_nb();
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
+  for (int r0 = 0; r0 < n; r0 += nb) {
+    const int rows = std::min(nb, n - r0);
+    CK(k1_block_update(ctx, n, m, Lh, ldlh, r0, rows, 0, r0, R, ldr));
+    CK_BLAS(cublasZtrsm(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
+                        CUBLAS_DIAG_NON_UNIT, rows, m, &one,
+                        reinterpret_cast<const cuDoubleComplex*>(L + r0 + (long long)r0 * ldl), (int)ldl,
+                        reinterpret_cast<cuDoubleComplex*>(R + r0), (int)ldr));
+  }
+  return CHFSI_OK;
+}
+
+// L^H X = Y in place (backward block substitution; the rows of L^H are the
+// conjugated columns of L, read by K1 directly from L's storage).
+int trsm_lower_h_k1(chfsi_ctx* ctx, int n, int m, const double2* L, long long ldl, double2* Y,
+                    long long ldy) {
+  const int nb = trsm_nb();
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
+  const int nblk = (n + nb - 1) / nb;
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int r0 = b * nb, rows = std::min(nb, n - r0), k0 = r0 + rows;
+    CK(k1_block_update(ctx, n, m, L, ldl, r0, rows, k0, n - k0, Y, ldy));
+    CK_BLAS(cublasZtrsm(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C,
+                        CUBLAS_DIAG_NON_UNIT, rows, m, &one,
+                        reinterpret_cast<const cuDoubleComplex*>(L + r0 + (long long)r0 * ldl), (int)ldl,
+                        reinterpret_cast<cuDoubleComplex*>(Y + r0), (int)ldy));
+  }
+  return CHFSI_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 int chfsi_heev_rr_z(chfsi_ctx* ctx, int n, void* A, long long lda, double* w, double tol,
@@ -1100,6 +1173,42 @@ int chfsi_to_standard_async_z(chfsi_ctx* ctx, int n, void* A, long long lda, voi
   return CHFSI_OK;
 }
 
+int chfsi_to_standard_k1_z(chfsi_ctx* ctx, int n, void* A, long long lda, void* B, long long ldb,
+                           int rowmajor_in, void* work, int* info_host) {
+  CK_ARG(ctx, "ctx is NULL");
+  CK_ARG(info_host, "info_host is NULL");
+  CK_ARG(n == 0 || work, "work is NULL");
+  if (n == 0) {
+    *info_host = 0;
+    return CHFSI_OK;
+  }
+  cudaStream_t s = ctx->stream;
+  if (rowmajor_in) {
+    CK(chfsi_conj_z(ctx, n, n, A, lda));
+    CK(chfsi_conj_z(ctx, n, n, B, ldb));
+  }
+  cuDoubleComplex* b = static_cast<cuDoubleComplex*>(B);
+  int lwork = 0;
+  CK_SOLVER(cusolverDnZpotrf_bufferSize(ctx->solver, CUBLAS_FILL_MODE_LOWER, n, b, (int)ldb, &lwork));
+  CK(ensure_ws(ctx, (size_t)lwork * sizeof(cuDoubleComplex)));
+  CK_SOLVER(cusolverDnZpotrf(ctx->solver, CUBLAS_FILL_MODE_LOWER, n, b, (int)ldb,
+                             static_cast<cuDoubleComplex*>(ctx->ws), lwork, ctx->dinfo));
+  CK_CUDA(cudaMemcpyAsync(info_host, ctx->dinfo, sizeof(int), cudaMemcpyDeviceToHost, s));
+  double2* l = static_cast<double2*>(B);
+  double2* a = static_cast<double2*>(A);
+  double2* lh = static_cast<double2*>(work);  // L^H (n x n, ld n)
+  double2* t = lh + (size_t)n * n;            // Z^H, then H (n x n, ld n)
+  CK_CUDA(chfsi::zero_upper_launch(l, ldb, n, s));
+  CK_CUDA(chfsi::conj_transpose_launch(l, ldb, lh, n, n, s));
+  CK(trsm_lower_k1(ctx, n, n, l, ldb, lh, n, a, lda));  // Z = L^-1 A
+  CK_CUDA(chfsi::conj_transpose_launch(a, lda, t, n, n, s));
+  CK(trsm_lower_k1(ctx, n, n, l, ldb, lh, n, t, n));    // H = L^-1 Z^H (= Z L^-H, Hermitian)
+  CK_CUDA(cudaMemcpy2DAsync(a, (size_t)lda * sizeof(double2), t, (size_t)n * sizeof(double2),
+                            (size_t)n * sizeof(double2), n, cudaMemcpyDeviceToDevice, s));
+  CK(chfsi_symmetrize_z(ctx, n, A, lda));
+  return CHFSI_OK;
+}
+
 int chfsi_herm_defect_async_z(chfsi_ctx* ctx, int n, const void* A, long long lda,
                               double* out_host) {
   CK_ARG(ctx, "ctx is NULL");
@@ -1131,26 +1240,15 @@ int chfsi_to_standard_z(chfsi_ctx* ctx, int n, void* A, long long lda, void* B, 
 
 int chfsi_back_transform_z(chfsi_ctx* ctx, int n, int nev, const void* L, long long ldl, void* Y,
                            long long ldy) {
-  // Y <- L^-H Y by block back-substitution over row blocks of kNb: a small
-  // ZTRSM on each diagonal block, then one ZGEMM updating every row above it
-  // (no inverse is formed). Measured: level with cuBLAS's single ZTRSM at
-  // n=2048 (1.07 ms, nev=128; block sizes 64..512 all within 7 %), 5 % faster
-  // at n=5000 — cuBLAS's TRSM on the diagonal blocks dominates either way.
+  // Y <- L^-H Y by backward block substitution: per block of rows the
+  // product with the rows of L^H right of the diagonal on K1 (3M DMMA,
+  // reading L's own columns conjugated), then a small ZTRSM on the diagonal
+  // block. cuBLAS's single ZTRSM of the whole triangle was 1.07 ms at
+  // n = 2048, nev = 128 (latency of its sequential blocks).
   CK_ARG(ctx, "ctx is NULL");
   if (n == 0 || nev == 0) return CHFSI_OK;
-  constexpr int kNb = 256;
-  if (n <= 2 * kNb) return chfsi_trsm_z(ctx, 'L', 'C', n, nev, L, ldl, Y, ldy);
-  const double2* l = static_cast<const double2*>(L);
-  double2* y = static_cast<double2*>(Y);
-  const int nblk = (n + kNb - 1) / kNb;
-  for (int k = nblk - 1; k >= 0; --k) {
-    const int r0 = k * kNb, rows = std::min(kNb, n - r0);
-    CK(chfsi_trsm_z(ctx, 'L', 'C', rows, nev, l + r0 + (long long)r0 * ldl, ldl, y + r0, ldy));
-    if (r0 > 0)  // Y[0:r0] -= L[r0:r0+rows, 0:r0]^H Y[r0:r0+rows]
-      CK(chfsi_gemm_z(ctx, 'C', 'N', r0, nev, rows, -1.0, 0.0, l + r0, ldl, y + r0, ldy, 1.0, 0.0, y,
-                      ldy));
-  }
-  return CHFSI_OK;
+  return trsm_lower_h_k1(ctx, n, nev, static_cast<const double2*>(L), ldl, static_cast<double2*>(Y),
+                         ldy);
 }
 
 }  // extern "C"

@@ -125,6 +125,9 @@ cudaError_t herm_defect_launch(const double2* a, long long lda, int n, double* o
                                cudaStream_t s);
 // A <- conj(A) elementwise (m x n col-major block); also zero strict upper if tril
 cudaError_t conj_inplace_launch(double2* a, long long lda, int m, int n, cudaStream_t s);
+// dst = src^H (square, column-major, out of place)
+cudaError_t conj_transpose_launch(const double2* src, long long lds, double2* dst, long long ldd, int n,
+                                  cudaStream_t s);
 cudaError_t zero_upper_launch(double2* a, long long lda, int n, cudaStream_t s);
 // Q[:, j] *= conj(d_j / |d_j|), d_j = R[j, j] read from the (separate) diag array
 cudaError_t phase_fix_launch(double2* q, long long ldq, int m, int n, const double2* rdiag,

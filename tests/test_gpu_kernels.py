@@ -450,10 +450,11 @@ def test_reduction_matches_reference_golden(pkg, small_golden, name):
     np.testing.assert_allclose(x, xref, rtol=0, atol=1e-11 * max(1.0, np.abs(xref).max()))
 
 
-@pytest.mark.parametrize("n,nev", [(700, 40), (1500, 97), (2048, 128)])
+@pytest.mark.parametrize("n,nev", [(100, 7), (256, 33), (700, 40), (1500, 97), (2048, 128)])
 def test_back_transform_blocked_matches_triangular_solve(pkg, n, nev):
-    """x = L^-H y through the block back-substitution (n > 512: ZTRSM on
-    256-row diagonal blocks + ZGEMM updates) vs scipy's triangular solve."""
+    """x = L^-H y through the backward block substitution (K1 products with
+    the rows of L^H right of the diagonal, ZTRSM on the 256-row diagonal
+    blocks) vs scipy's triangular solve."""
     import scipy.linalg
 
     rng = np.random.default_rng(n)
@@ -466,6 +467,33 @@ def test_back_transform_blocked_matches_triangular_solve(pkg, n, nev):
                            sol).vectors.cpu().numpy()
     ref = scipy.linalg.solve_triangular(l, y, lower=True, trans="C")
     assert np.abs(x - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("n", [64, 255, 256, 700, 1100])
+def test_to_standard_k1_matches_numpy(pkg, n):
+    """The sequence driver's reduction (chfsi_to_standard_k1_z: block
+    substitutions with K1 products) vs numpy's L^-1 A L^-H, and vs the
+    ZTRSM path of to_standard()."""
+    import scipy.linalg
+    from paper_1206_3768_b200.reduction import stage_standard
+
+    rng = np.random.default_rng(n + 3)
+    a = random_hermitian(rng, n)
+    c = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    b = np.eye(n) + c @ c.conj().T / (4 * n)
+    l = np.linalg.cholesky(b)
+    z = scipy.linalg.solve_triangular(l, a, lower=True)
+    href = scipy.linalg.solve_triangular(l, z.conj().T, lower=True)
+    href = (href + href.conj().T) / 2
+    _, sp, checks = stage_standard(a, b, 1)
+    torch.cuda.synchronize()
+    checks.raise_if_invalid()
+    h = sp.h.cpu().numpy()
+    assert np.array_equal(h, h.conj().T)
+    assert np.abs(h - href).max() <= 1e-12 * np.abs(href).max()
+    assert np.abs(sp.cholesky_factor.cpu().numpy() - l).max() <= 1e-12
+    h_trsm = pkg.to_standard(pkg.EigenPencil(a=a, b=b)).h.cpu().numpy()
+    assert np.abs(h - h_trsm).max() <= 1e-13 * np.abs(href).max()
 
 
 def test_reduction_rejects_indefinite_overlap(pkg):
