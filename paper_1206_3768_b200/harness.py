@@ -17,6 +17,7 @@ runs to_standard -> chfsi_solve -> back_transform on the device.
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -146,7 +147,9 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
     With ``overlap`` the upload + reduction to standard form of problem l+1
     runs on a side stream while problem l is being solved (the reduction
     does not depend on the previous solve), hiding it behind the solver's
-    latency-bound phases. Results are identical either way. ``shard`` is
+    latency-bound phases; the back-transform of problem l runs on the same
+    side stream behind problem l+1's solve (``CHFSI_BACK_ON_SIDE=0`` keeps
+    it on the caller's stream). Results are identical either way. ``shard`` is
     passed to chfsi_solve (row-sharded multi-GPU filter).
     """
     if mode not in ("chained", "harness"):
@@ -157,6 +160,7 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
     side = side_stream() if overlap else main
     if side is not main:
         side.wait_stream(main)  # inputs produced on the caller's stream are visible
+    back_side = side is not main and os.environ.get("CHFSI_BACK_ON_SIDE", "1") != "0"
     it = iter(pencils)
     first = next(it, None)
     staged = _stage(first, side) if first is not None else None
@@ -192,7 +196,23 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
             rng, prefetch = prefetch, None
         sol, rep = chfsi_solve(sp.h, cfg, guess=guess, rng=rng, label=pencil.label, shard=shard)
         t2 = time.perf_counter()
-        gsol = back_transform(sp.cholesky_factor, sol, inplace=not keep_standard)
+        if back_side:
+            # x = L^-H y of problem l on the side stream: it overlaps problem
+            # l+1's solve (the chained guess is the standard-form tail, not x)
+            # and fills the solver's latency-bound gaps instead of extending
+            # the critical path; the caller's stream waits for it at the end.
+            solved = torch.cuda.Event()
+            solved.record(main)
+            with torch.cuda.stream(side):
+                side.wait_event(solved)
+                gsol = back_transform(sp.cholesky_factor, sol, inplace=not keep_standard)
+                back_done = torch.cuda.Event()
+                back_done.record(side)
+            sp.cholesky_factor.record_stream(side)
+            gsol.vectors.record_stream(side)
+        else:
+            gsol = back_transform(sp.cholesky_factor, sol, inplace=not keep_standard)
+            back_done = None
         main.synchronize()
         t3 = time.perf_counter()
         res = ProblemResult(label=pencil.label, values=sol.values, solution=gsol,
@@ -212,6 +232,8 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
                 guess = None
         out.append(res)
         if on_problem is not None:
+            if back_done is not None:
+                back_done.synchronize()
             on_problem(res)
         del sp
     main.wait_stream(side)
