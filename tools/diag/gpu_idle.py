@@ -75,3 +75,34 @@ for (p, n), (c, t) in sorted(gaps.items(), key=lambda kv: -kv[1][1])[: a.top]:
 print("\nkernels by total device time (ms, count):")
 for name, (c, t) in sorted(per_kernel.items(), key=lambda kv: -kv[1][1])[: a.top]:
     print(f"{t / 1e3:9.3f} {c:6d}  {name[:110]}")
+
+# host activity during device-idle gaps: CPU ops / runtime calls overlapping
+# each gap of >= 20 us, overlap time summed per name (nested ops both count)
+cpu = sorted((e.time_range.start, e.time_range.end, e.name) for e in prof.events()
+             if e.device_type == torch.autograd.DeviceType.CPU)
+idle = []
+cur_e = evs[0][1]
+for s, e, name in evs[1:]:
+    if s > cur_e + 20:
+        idle.append((cur_e, s))
+    cur_e = max(cur_e, e)
+host = collections.defaultdict(lambda: [0, 0.0])
+import bisect
+starts = [c[0] for c in cpu]
+maxlen = max((c[1] - c[0] for c in cpu), default=0)
+for gs, ge in idle:
+    i = bisect.bisect_left(starts, gs - maxlen)
+    seen = set()
+    while i < len(cpu) and cpu[i][0] < ge:
+        cs, ce, name = cpu[i]
+        ov = min(ce, ge) - max(cs, gs)
+        if ov > 0:
+            host[name][1] += ov
+            if name not in seen:
+                host[name][0] += 1
+                seen.add(name)
+        i += 1
+print(f"\nhost ops overlapping device-idle gaps >= 20 us ({len(idle)} gaps, "
+      f"{sum(g - s for s, g in idle) / 1e3:.2f} ms):")
+for name, (c, t) in sorted(host.items(), key=lambda kv: -kv[1][1])[: a.top]:
+    print(f"{t / 1e3:9.3f} {c:6d}  {name[:110]}")
