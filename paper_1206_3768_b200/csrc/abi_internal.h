@@ -31,7 +31,7 @@ struct chfsi_ctx {
   bool qr_linear2 = true;  // Cholesky-QR2: linearised second pass when |Q1^H Q1 - I| <= 1e-8
   int lanczos_mode = 0;  // 0: cooperative single kernel; 1: one launch per operation
   unsigned step_epoch = 0;
-  cudaEvent_t loop_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // chfsi_solve_loop_z phase timers
+  cudaEvent_t loop_ev[8] = {};  // chfsi_solve_loop_z phase timers (two sets, alternating passes)
   // second filter stream (two column halves of the filter run concurrently,
   // one CTA per SM each) with its own stream-K scratch
   cudaStream_t aux_stream = nullptr;

@@ -227,7 +227,18 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
          "row-sharded loop needs filter and hp callbacks and a valid row range");
   CK(ensure_events(ctx));
   cudaStream_t s = ctx->stream;
+  // phase timers: pass p records into event set p % 2; a pass's elapsed
+  // times are read once the next pass's filter is queued (not inside the
+  // device-idle gap after the per-pass sync)
   cudaEvent_t* ev = ctx->loop_ev;
+  cudaEvent_t* pending = nullptr;
+  auto read_timers = [&]() {
+    if (!pending) return;
+    L->t_filter += 1e-3 * elapsed(pending[0], pending[1]);
+    L->t_ortho += 1e-3 * elapsed(pending[1], pending[2]);
+    L->t_rr += 1e-3 * elapsed(pending[2], pending[3]);
+    pending = nullptr;
+  };
   const int n = L->n;
   const int nl = dist ? L->n_local : n;  // rows (and ld) of every n x w block here
   CK_ARG(!L->adaptive || (L->degs && L->perm_d && 1 <= L->deg_min && L->deg_min <= L->deg),
@@ -247,6 +258,7 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
     const int width = L->width;
     void* panel = col(L->bufs[L->pb], nl, L->off);
     void* other = L->bufs[1 - L->pb];
+    ev = ctx->loop_ev + 4 * (L->inner_loops & 1);
 
     // ---- filter (chfsi.py:331-334)
     CK_CUDA(cudaEventRecord(ev[0], s));
@@ -275,6 +287,7 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
     }
     hp_ready = false;
     CK_CUDA(cudaEventRecord(ev[1], s));
+    read_timers();  // the previous pass's (its events completed at its sync)
     long long dsum = (long long)L->deg * width;
     if (degs) {
       dsum = 0;
@@ -312,9 +325,7 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
     CK_CUDA(cudaMemcpyAsync(host + width, L->res_d, (size_t)width * sizeof(double),
                             cudaMemcpyDeviceToHost, s));
     CK_CUDA(cudaStreamSynchronize(s));
-    L->t_filter += 1e-3 * elapsed(ev[0], ev[1]);
-    L->t_ortho += 1e-3 * elapsed(ev[1], ev[2]);
-    L->t_rr += 1e-3 * elapsed(ev[2], ev[3]);
+    pending = ev;
     if (dist)  // summed squares of the local row norms
       for (int j = 0; j < width; ++j) host[width + j] = std::sqrt(host[width + j]);
     const double* ritz = host;
@@ -388,6 +399,7 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
       have_degs = true;
     }
   }
+  read_timers();
   // chained-mode tail: [locked | unlocked remainder of the final panel]
   if (L->tail && L->inner_loops > 0) {
     const size_t col_bytes = (size_t)nl * sizeof(double2);
