@@ -174,11 +174,21 @@ def as_rng(seed_or_rng):
     return np.random.default_rng(seed_or_rng)
 
 
-def _draw_block(rng, n, cols):
+def _draw_block(rng, n, cols, pinned=False):
     """Complex Gaussian block drawn on the host in the reference order
-    (_util.py:15-18), as numpy."""
-    re = rng.standard_normal((n, cols))
-    return re + 1j * rng.standard_normal((n, cols))
+    (_util.py:15-18: real parts, then imaginary parts, each C-ordered), as a
+    CPU complex128 tensor, page-locked with ``pinned``. The two draws go
+    through one float scratch straight into the complex storage: the same
+    bytes as ``re + 1j * im`` without its complex temporaries (~3 ms less
+    host time at C2) or a separate copy into page-locked memory."""
+    out = torch.empty((n, cols), dtype=torch.complex128, pin_memory=pinned)
+    z = out.numpy()
+    tmp = np.empty((n, cols))
+    rng.standard_normal(out=tmp)
+    z.real = tmp
+    rng.standard_normal(out=tmp)
+    z.imag = tmp
+    return out
 
 
 class PrefetchedStart:
@@ -201,7 +211,7 @@ class PrefetchedStart:
         try:
             self._box["q0"] = _draw_start_vector(self.rng, self.n)
             self._q0_ready.set()
-            self._box["z"] = torch.from_numpy(_draw_block(self.rng, self.n, self.blk)).pin_memory()
+            self._box["z"] = _draw_block(self.rng, self.n, self.blk, pinned=True)
         except BaseException as exc:  # noqa: BLE001 - re-raised by the consumer
             self._box["err"] = exc
             self._q0_ready.set()
@@ -224,7 +234,7 @@ class PrefetchedStart:
 def random_block(rng, n, cols):
     """`_draw_block`, uploaded as a device F-block."""
     # page-locked staging: one DMA instead of a pageable copy (~10 ms at C2)
-    return to_fblock(torch.from_numpy(_draw_block(rng, n, cols)).pin_memory())
+    return to_fblock(_draw_block(rng, n, cols, pinned=True))
 
 
 class _PhaseTimer:

@@ -72,3 +72,19 @@ def test_greedy_matching_equals_reference_loop(m, seed, ties):
     if ties:
         gram = np.round(gram, 1)  # many equal entries: tie order must match argmax's
     assert np.array_equal(greedy_match(gram), reference_greedy(gram))
+
+
+def test_host_block_draw_is_bitwise_the_oracle_draw():
+    """The solver's start/repair block draw (two float draws written into
+    complex storage) gives the oracle's `re + 1j*im` bytes and leaves the
+    generator in the same state (chfsi.py:323, _util.py:15-18)."""
+    from oracle.chfsi_oracle import random_block
+    from paper_1206_3768_b200.chfsi import _draw_block
+
+    for n, cols in ((1, 1), (37, 5), (512, 48)):
+        r1, r2 = np.random.default_rng((0, n, 0)), np.random.default_rng((0, n, 0))
+        got = _draw_block(r1, n, cols).numpy()
+        want = np.ascontiguousarray(random_block(r2, n, cols))
+        assert got.shape == (n, cols)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+        assert r1.standard_normal() == r2.standard_normal()
