@@ -30,6 +30,7 @@ value = N x sequence FLOPs / max-over-ranks time.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -301,6 +302,10 @@ def run_ours(args):
 
     for _ in range(args.warmup):
         device_step()
+    # the long-lived objects (modules, inputs) leave the collector's view:
+    # cyclic GC passes between steps then scan only the per-step garbage
+    gc.collect()
+    gc.freeze()
     barrier()
     clocks = ClockSampler(local)
     if not args.no_clocks:

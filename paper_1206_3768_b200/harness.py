@@ -17,8 +17,10 @@ runs to_standard -> chfsi_solve -> back_transform on the device.
 
 from __future__ import annotations
 
+import gc
 import os
 import time
+from concurrent.futures import Future, ThreadPoolExecutor, wait
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -98,6 +100,20 @@ def side_stream(device=None):
     return st
 
 
+_SIDE_WORKERS = {}
+
+
+def side_worker(device):
+    """One persistent worker thread per device that issues the side stream's
+    work (its libchfsi contexts are per thread, so a thread per call would
+    build new cuBLAS/cuSOLVER handles per call)."""
+    w = _SIDE_WORKERS.get(device)
+    if w is None:
+        w = _SIDE_WORKERS[device] = ThreadPoolExecutor(max_workers=1,
+                                                       thread_name_prefix="chfsi-side")
+    return w
+
+
 def _stage(item, side):
     """Upload, validate and reduce one pencil on the side stream without any
     host synchronisation (the validation results land in page-locked memory
@@ -172,70 +188,129 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
         p0 = staged[0]
         prefetch = PrefetchedStart(np.random.default_rng((seed, p0.label, 0)), p0.n,
                                    cfg.resolve(p0.n)[0])
-    while staged is not None:
-        t0 = time.perf_counter()
-        pencil, sp, ev, checks = staged
-        ev.synchronize()  # long done for l >= 2: staged while l-1 was solved
-        checks.raise_if_invalid()
-        main.wait_event(ev)
-        if side is not main:
-            for t in (sp.h, sp.cholesky_factor, pencil.a, pencil.b):
-                t.record_stream(main)
-        t1 = time.perf_counter()
-        nxt = next(it, None)
-        staged = _stage(nxt, side) if nxt is not None else None
-        t_stage = time.perf_counter() - t1
-        t1 = time.perf_counter()
-        n = pencil.n
-        blk = cfg.resolve(n)[0]
-        if mode == "harness" and blk >= n:
-            raise ValueError(f"chfsi warm starts need blk < n (blk={blk}, n={n})")
-        start = 0 if guess is None else 1
-        rng = np.random.default_rng((seed, pencil.label, start))
-        if prefetch is not None:  # (always problem 1: guess is None there)
-            rng, prefetch = prefetch, None
-        sol, rep = chfsi_solve(sp.h, cfg, guess=guess, rng=rng, label=pencil.label, shard=shard)
-        t2 = time.perf_counter()
-        if back_side:
-            # x = L^-H y of problem l on the side stream: it overlaps problem
-            # l+1's solve (the chained guess is the standard-form tail, not x)
-            # and fills the solver's latency-bound gaps instead of extending
-            # the critical path; the caller's stream waits for it at the end.
-            solved = torch.cuda.Event()
-            solved.record(main)
-            with torch.cuda.stream(side):
-                side.wait_event(solved)
+    # Side-stream work (staging of problem l+1, back-transform of problem l)
+    # is ISSUED by one worker thread: its host-side launch cost (~1 ms per
+    # problem) then overlaps the solve instead of leaving the main stream
+    # idle between problems (the native loop runs without the GIL). The
+    # worker's FIFO keeps the side stream's order: stage(l+1), back(l), ...
+    dev = torch.cuda.current_device()
+    threaded = side is not main and os.environ.get("CHFSI_SIDE_WORKER", "1") != "0"
+    worker = side_worker(dev) if threaded else None
+    issued = []
+
+    def on_device(fn, *args):
+        with torch.cuda.device(dev):
+            return fn(*args)
+
+    def submit(fn, *args):
+        if worker is None:  # CHFSI_SIDE_WORKER=0: issued inline, same stream order
+            fut = Future()
+            fut.set_result(fn(*args))
+            return fut
+        fut = worker.submit(on_device, fn, *args)
+        issued.append(fut)
+        return fut
+
+    def back_on_side(solved, l_factor, sol):
+        # x = L^-H y of problem l on the side stream, behind its solve: it
+        # overlaps problem l+1's solve (the chained guess is the standard-form
+        # tail, not x); the caller's stream joins at the end.
+        with torch.cuda.stream(side):
+            side.wait_event(solved)
+            gsol = back_transform(l_factor, sol, inplace=not keep_standard)
+            done = torch.cuda.Event()
+            done.record(side)
+        l_factor.record_stream(side)
+        gsol.vectors.record_stream(side)
+        return gsol, done
+
+    pending = []  # (result, future of the side-stream back-transform)
+    # No cyclic GC passes inside the sequence: a full collection of a
+    # torch-sized heap holds the GIL for 50-400 ms, and whichever thread
+    # triggers it stalls the other's return from the native loop (measured
+    # with the side worker: problem 9 of C2 sequences +15..360 ms in 5 of
+    # 24 steps; none in 24 steps without collections). Cycles are collected
+    # as usual once the call returns.
+    gc_on = gc.isenabled()
+    gc.disable()
+
+    def settle(res, fut):
+        res.solution, done = fut.result()
+        return done
+
+    try:
+        while staged is not None:
+            t0 = time.perf_counter()
+            if not isinstance(staged, tuple):
+                staged = staged.result()  # issued by the worker during the last solve
+            pencil, sp, ev, checks = staged
+            ev.synchronize()  # long done for l >= 2: staged while l-1 was solved
+            checks.raise_if_invalid()
+            main.wait_event(ev)
+            if side is not main:
+                for t in (sp.h, sp.cholesky_factor, pencil.a, pencil.b):
+                    t.record_stream(main)
+            t1 = time.perf_counter()
+            nxt = next(it, None)
+            if nxt is None:
+                staged = None
+            elif side is not main:
+                staged = submit(_stage, nxt, side)
+            else:
+                staged = _stage(nxt, side)
+            t_stage = time.perf_counter() - t1
+            t1 = time.perf_counter()
+            n = pencil.n
+            blk = cfg.resolve(n)[0]
+            if mode == "harness" and blk >= n:
+                raise ValueError(f"chfsi warm starts need blk < n (blk={blk}, n={n})")
+            start = 0 if guess is None else 1
+            rng = np.random.default_rng((seed, pencil.label, start))
+            if prefetch is not None:  # (always problem 1: guess is None there)
+                rng, prefetch = prefetch, None
+            sol, rep = chfsi_solve(sp.h, cfg, guess=guess, rng=rng, label=pencil.label,
+                                   shard=shard)
+            t2 = time.perf_counter()
+            back = None
+            if back_side:
+                solved = torch.cuda.Event()
+                solved.record(main)
+                back = submit(back_on_side, solved, sp.cholesky_factor, sol)
+                gsol = None  # filled from `back`
+            else:
                 gsol = back_transform(sp.cholesky_factor, sol, inplace=not keep_standard)
-                back_done = torch.cuda.Event()
-                back_done.record(side)
-            sp.cholesky_factor.record_stream(side)
-            gsol.vectors.record_stream(side)
-        else:
-            gsol = back_transform(sp.cholesky_factor, sol, inplace=not keep_standard)
-            back_done = None
-        main.synchronize()
-        t3 = time.perf_counter()
-        res = ProblemResult(label=pencil.label, values=sol.values, solution=gsol,
-                            standard_vectors=sol.vectors if keep_standard else None, report=rep,
-                            t_reduce=t1 - t0 - t_stage, t_solve=t2 - t1, t_back=t3 - t2)
-        res.extra["t_stage_next"] = t_stage
-        if mode == "harness":
-            dv, dvec = hermitian_eig(sp.h)
-            res.dense_values = dv
-            guess = ChfsiGuess(vectors=dvec[:, :blk], lambda1=float(dv[0]),
-                               lambda_blk_plus_1=float(dv[blk]))
-        else:
-            if rep.tail_vectors is not None and rep.tail_vectors.shape[1] == blk and sol.nev:
-                guess = ChfsiGuess(vectors=rep.tail_vectors, lambda1=float(sol.values[0]),
-                                   lambda_blk_plus_1=float(rep.lambda_blk_plus_1))
-            else:  # a partial solve leaves no full block: restart cold
-                guess = None
-        out.append(res)
-        if on_problem is not None:
-            if back_done is not None:
-                back_done.synchronize()
-            on_problem(res)
-        del sp
+            main.synchronize()
+            t3 = time.perf_counter()
+            res = ProblemResult(label=pencil.label, values=sol.values, solution=gsol,
+                                standard_vectors=sol.vectors if keep_standard else None,
+                                report=rep, t_reduce=t1 - t0 - t_stage, t_solve=t2 - t1,
+                                t_back=t3 - t2)
+            res.extra["t_stage_next"] = t_stage
+            if mode == "harness":
+                dv, dvec = hermitian_eig(sp.h)
+                res.dense_values = dv
+                guess = ChfsiGuess(vectors=dvec[:, :blk], lambda1=float(dv[0]),
+                                   lambda_blk_plus_1=float(dv[blk]))
+            else:
+                if rep.tail_vectors is not None and rep.tail_vectors.shape[1] == blk and sol.nev:
+                    guess = ChfsiGuess(vectors=rep.tail_vectors, lambda1=float(sol.values[0]),
+                                       lambda_blk_plus_1=float(rep.lambda_blk_plus_1))
+                else:  # a partial solve leaves no full block: restart cold
+                    guess = None
+            out.append(res)
+            if back is not None:
+                pending.append((res, back))
+            if on_problem is not None:
+                if back is not None:
+                    settle(res, back).synchronize()
+                on_problem(res)
+            del sp
+    finally:
+        wait(issued)  # nothing the worker issues outlives this call
+        if gc_on:
+            gc.enable()
+    for res, fut in pending:
+        settle(res, fut)  # re-raises a failed back-transform
     main.wait_stream(side)
     return out
 
