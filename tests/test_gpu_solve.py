@@ -343,3 +343,31 @@ def test_c2_chained_sequence_bitwise_reproducible(pkg):
         assert r1.report.locked_per_loop == r2.report.locked_per_loop
         assert np.array_equal(r1.values, r2.values)
         assert torch.equal(r1.solution.vectors, r2.solution.vectors)
+
+
+@pytest.mark.gpu
+def test_sequence_side_worker_matches_inline_and_serial(pkg, monkeypatch):
+    """The side stream's work issued by the worker thread (default), inline
+    (CHFSI_SIDE_WORKER=0) and with no side stream at all (overlap=False)
+    give bitwise the same sequence; on_problem sees finished generalized
+    vectors equal to the returned ones."""
+    cfg_b = pkg.BASELINE_CONFIGS["C1"]
+    cfg = pkg.ChfsiConfig(nev=cfg_b.nev, nex=cfg_b.nex, deg=cfg_b.deg, tol=cfg_b.tol)
+    seq = list(pkg.iter_baseline_sequence(cfg_b.n, 4, seed=0))
+    seen = []
+
+    def cb(r):
+        seen.append(r.solution.vectors.clone())
+
+    threaded = pkg.solve_sequence(seq, cfg, seed=0, on_problem=cb)
+    monkeypatch.setenv("CHFSI_SIDE_WORKER", "0")
+    inline = pkg.solve_sequence(seq, cfg, seed=0)
+    serial = pkg.solve_sequence(seq, cfg, seed=0, overlap=False)
+    assert len(seen) == len(threaded) == len(seq)
+    for k, (a, b, c) in enumerate(zip(threaded, inline, serial)):
+        assert a.solution.form == "generalized"
+        assert torch.equal(seen[k], a.solution.vectors)
+        for other in (b, c):
+            assert a.report.locked_per_loop == other.report.locked_per_loop
+            assert np.array_equal(a.values, other.values)
+            assert torch.equal(a.solution.vectors, other.solution.vectors)
