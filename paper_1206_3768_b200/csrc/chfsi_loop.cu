@@ -14,6 +14,8 @@
 // stream synchronisation per pass, plus the near-diagonal eigensolver's
 // regime checks). Device phase times are taken with events on the stream.
 #include <algorithm>
+#include <cstdlib>
+#include <utility>
 #include <cmath>
 #include <vector>
 
@@ -59,6 +61,15 @@ int ensure_events(chfsi_ctx* ctx) {
   return CHFSI_OK;
 }
 
+// CHFSI_ROTATE_PAIR=0: the two Rayleigh-Ritz rotations as separate ZGEMMs (A/B)
+bool rotate_pair_off() {
+  static const bool off = [] {
+    const char* e = getenv("CHFSI_ROTATE_PAIR");
+    return e && atoi(e) == 0;
+  }();
+  return off;
+}
+
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
   return cudaEventElapsedTime(&ms, a, b) == cudaSuccess ? ms : 0.f;
@@ -85,6 +96,30 @@ int orthonormalize(chfsi_ctx* ctx, chfsi_loop* L, void* work, int width) {
 
 // HP = H P; G = P^H HP symmetrised; eigenpairs (near-diagonal solver when
 // allowed, else zheevd); P W, HP W; residual norms (chfsi.py:337-350).
+// P_rot = Q W and HP_rot = HP W (n x w each, ld n) as ONE strided-batched
+// ZGEMM (batch 2, W shared) when the two pairs of blocks are equally ordered
+// in memory (the batch strides must be non-negative); two ZGEMMs otherwise.
+int rotate_pair(chfsi_ctx* ctx, int n, int w, const void* q, const void* hp, const void* W,
+                long long ldw, void* rot_p, void* hp_rot) {
+  const auto* a0 = static_cast<const cuDoubleComplex*>(q);
+  const auto* a1 = static_cast<const cuDoubleComplex*>(hp);
+  auto* c0 = static_cast<cuDoubleComplex*>(rot_p);
+  auto* c1 = static_cast<cuDoubleComplex*>(hp_rot);
+  if ((a1 < a0) != (c1 < c0) || rotate_pair_off()) {
+    CK(chfsi_gemm_z(ctx, 'N', 'N', n, w, w, 1.0, 0.0, q, n, W, ldw, 0.0, 0.0, rot_p, n));
+    return chfsi_gemm_z(ctx, 'N', 'N', n, w, w, 1.0, 0.0, hp, n, W, ldw, 0.0, 0.0, hp_rot, n);
+  }
+  if (a1 < a0) {
+    std::swap(a0, a1);
+    std::swap(c0, c1);
+  }
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+  CK_BLAS(cublasZgemmStridedBatched(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, n, w, w, &one, a0, n,
+                                    (long long)(a1 - a0), static_cast<const cuDoubleComplex*>(W),
+                                    (int)ldw, 0, &zero, c0, n, (long long)(c1 - c0), 2));
+  return CHFSI_OK;
+}
+
 int rayleigh_ritz(chfsi_ctx* ctx, chfsi_loop* L, const void* q, void* rot_p, int width, double eig_tol,
                   int* used_fast) {
   const int n = L->n;
@@ -94,9 +129,7 @@ int rayleigh_ritz(chfsi_ctx* ctx, chfsi_loop* L, const void* q, void* rot_p, int
   CK(chfsi_gemm_z(ctx, 'C', 'N', width, width, n, 1.0, 0.0, q, n, L->hp, n, 0.0, 0.0, L->g, ldg));
   CK(chfsi_symmetrize_z(ctx, width, L->g, ldg));
   CK(chfsi_heev_rr_z(ctx, width, L->g, ldg, L->ritz_d, eig_tol, used_fast));
-  CK(chfsi_gemm_z(ctx, 'N', 'N', n, width, width, 1.0, 0.0, q, n, L->g, ldg, 0.0, 0.0, rot_p, n));
-  CK(chfsi_gemm_z(ctx, 'N', 'N', n, width, width, 1.0, 0.0, L->hp, n, L->g, ldg, 0.0, 0.0,
-                  L->hp_rot, n));
+  CK(rotate_pair(ctx, n, width, q, L->hp, L->g, ldg, rot_p, L->hp_rot));
   CK(chfsi_colnorm_residual_z(ctx, n, width, L->hp_rot, n, rot_p, n, L->ritz_d, L->res_d));
   return CHFSI_OK;
 }
