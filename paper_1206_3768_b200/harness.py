@@ -101,6 +101,7 @@ def side_stream(device=None):
 
 
 _SIDE_WORKERS = {}
+_BACK_SIDE_MAX_N = 8192  # side-stream back-transform up to this n (memory, see solve_sequence)
 
 
 def side_worker(device):
@@ -194,7 +195,10 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
     # idle between problems (the native loop runs without the GIL). The
     # worker's FIFO keeps the side stream's order: stage(l+1), back(l), ...
     dev = torch.cuda.current_device()
-    threaded = side is not main and os.environ.get("CHFSI_SIDE_WORKER", "1") != "0"
+    # (large n: seconds per problem make the worker's ~1 ms moot, and issuing
+    # inline keeps the allocator's frees ordered as at C5's memory limit)
+    threaded = (side is not main and os.environ.get("CHFSI_SIDE_WORKER", "1") != "0"
+                and (staged is None or staged[0].n <= _BACK_SIDE_MAX_N))
     worker = side_worker(dev) if threaded else None
     issued = []
 
@@ -241,8 +245,10 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
     try:
         while staged is not None:
             t0 = time.perf_counter()
-            if not isinstance(staged, tuple):
-                staged = staged.result()  # issued by the worker during the last solve
+            if not isinstance(staged, tuple):  # issued by the worker during the last solve
+                fut, staged = staged, staged.result()
+                if fut in issued:  # a done future holds its result: drop it, or every
+                    issued.remove(fut)  # problem's H and L would live until the call ends
             pencil, sp, ev, checks = staged
             ev.synchronize()  # long done for l >= 2: staged while l-1 was solved
             checks.raise_if_invalid()
@@ -272,7 +278,9 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
                                    shard=shard)
             t2 = time.perf_counter()
             back = None
-            if back_side:
+            # at large n the side-stream back-transform would keep L of problem
+            # l (6.4 GB at C5) alive next to the staged l+1: run it inline there
+            if back_side and n <= _BACK_SIDE_MAX_N:
                 solved = torch.cuda.Event()
                 solved.record(main)
                 back = submit(back_on_side, solved, sp.cholesky_factor, sol)

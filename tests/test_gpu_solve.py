@@ -371,3 +371,24 @@ def test_sequence_side_worker_matches_inline_and_serial(pkg, monkeypatch):
             assert a.report.locked_per_loop == other.report.locked_per_loop
             assert np.array_equal(a.values, other.values)
             assert torch.equal(a.solution.vectors, other.solution.vectors)
+
+
+@pytest.mark.gpu
+def test_sequence_driver_releases_its_operators(pkg):
+    """Nothing of a finished sequence call stays on the device once its
+    results are dropped (the worker's completed futures must not keep the
+    staged H and L): device memory in use is the same after every call."""
+    import gc
+
+    cfg_b = pkg.BASELINE_CONFIGS["C1"]
+    cfg = pkg.ChfsiConfig(nev=cfg_b.nev, nex=cfg_b.nex, deg=cfg_b.deg, tol=cfg_b.tol)
+    dev = torch.device("cuda", 0)
+    seq = [pkg.EigenPencil(a=torch.from_numpy(a).to(dev), b=torch.from_numpy(b).to(dev), label=lab)
+           for lab, a, b in pkg.iter_baseline_sequence(cfg_b.n, 6, seed=0)]
+    used = []
+    for _ in range(4):
+        pkg.solve_sequence(seq, cfg, seed=0)
+        gc.collect()
+        torch.cuda.synchronize()
+        used.append(torch.cuda.memory_allocated(dev))
+    assert len(set(used[1:])) == 1, used
