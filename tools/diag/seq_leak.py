@@ -35,6 +35,6 @@ inputs = {id(p.a) for p in seq} | {id(p.b) for p in seq}
 for t in ts:
     if id(t) in inputs:
         continue
-    refs = [type(r).__name__ + (":" + ",".join(list(r.keys())[:6]) if isinstance(r, dict) else "")
+    refs = [type(r).__name__ + (":" + ",".join(str(k) for k in list(r.keys())[:6]) if isinstance(r, dict) else "")
             for r in gc.get_referrers(t) if r is not ts]
     print("tensor", tuple(t.shape), t.untyped_storage().nbytes() >> 10, "KB held by", refs[:5])
