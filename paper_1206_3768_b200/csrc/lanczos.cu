@@ -31,7 +31,7 @@ struct LanczosParams {
   double2* V;         // n x k basis, column-major, ld n
   double2* u;         // n
   double2* r;         // n
-  double* part;       // [grid] scalar partials
+  double* part;       // [2][grid] scalar partials: alpha (and ||q0||^2) in [0, G), beta in [G, 2G)
   double2* cpart;     // [grid][k] reorthogonalisation partials
   double2* coef;      // [k]
   double* alphas;     // [k]
@@ -237,10 +237,14 @@ __global__ void __launch_bounds__(LZ_THREADS) lanczos_coop_kernel(const LanczosP
       }
     }
     bp = block_sum_all(bp, sh);
-    if (tid == 0) p.part[b] = bp;
+    // beta partials in their own half: a block leaving barrier (4) early
+    // writes its next alpha partial into [0, G) while a lagging block may
+    // still be summing these (single-buffered, that mixed alpha and beta
+    // partials and gave blocks different betas)
+    if (tid == 0) p.part[G + b] = bp;
     grid.sync();  // (4) beta partials
 
-    const double beta = sqrt(grid_total(p.part, G, sh));
+    const double beta = sqrt(grid_total(p.part + G, G, sh));
     const bool stop = (beta < 1e-14) || (it == p.k - 1);  // chfsi.py:152
     if (b == 0 && tid == 0) {
       p.st->steps = it + 1;
@@ -255,7 +259,10 @@ __global__ void __launch_bounds__(LZ_THREADS) lanczos_coop_kernel(const LanczosP
       qn[i] = make_double2(__ddiv_rn(x.x, beta), __ddiv_rn(x.y, beta));
     }
     beta_prev = beta;
-    // no barrier: the next GEMV reads r (complete since barrier (4)), and r
+    // q_next's rows are read by other threads of this block (lane 0 of the
+    // row's warp, alpha partial of the next GEMV)
+    __syncthreads();
+    // no grid barrier: the next GEMV reads r (complete since barrier (4)), and r
     // is rewritten only after the next barrier (1)
   }
 }
@@ -264,7 +271,7 @@ __global__ void __launch_bounds__(LZ_THREADS) lanczos_coop_kernel(const LanczosP
 
 size_t lanczos_coop_workspace_bytes(int n, int k) {
   const int G = lanczos_coop_grid(n);
-  return 2 * (size_t)n * sizeof(double2) + (size_t)G * sizeof(double) +
+  return 2 * (size_t)n * sizeof(double2) + 2 * (size_t)G * sizeof(double) +
          (size_t)G * k * sizeof(double2) + (size_t)k * sizeof(double2) + 256;
 }
 

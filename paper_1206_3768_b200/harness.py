@@ -115,13 +115,24 @@ def side_worker(device):
     return w
 
 
-def _stage(item, side):
+def _stage(item, side, ready=None):
     """Upload, validate and reduce one pencil on the side stream without any
     host synchronisation (the validation results land in page-locked memory
     and are checked when the problem is about to be solved, raising the
     reference's exceptions then); returns (pencil, StandardProblem, ready
-    event, pending checks)."""
+    event, pending checks).
+
+    ``ready`` is an event recorded on the caller's stream right after the
+    item was produced: a lazy device generator queues the work that writes
+    A and B on that stream inside ``next()``, so the side stream must wait
+    for it before reading them."""
     with torch.cuda.stream(side):
+        if ready is not None:
+            side.wait_event(ready)
+        a_b = (item.a, item.b) if isinstance(item, EigenPencil) else tuple(item[1:3])
+        for t in a_b:  # allocated on another stream, read on this one
+            if isinstance(t, torch.Tensor) and t.is_cuda:
+                t.record_stream(side)
         if isinstance(item, EigenPencil):  # validated at construction
             pencil, sp, checks = stage_standard(item.a, item.b, item.label, check_hermitian=False)
         else:
@@ -175,12 +186,21 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
     guess = None
     main = torch.cuda.current_stream()
     side = side_stream() if overlap else main
-    if side is not main:
-        side.wait_stream(main)  # inputs produced on the caller's stream are visible
     back_side = side is not main and os.environ.get("CHFSI_BACK_ON_SIDE", "1") != "0"
+
+    def produced():
+        # every input is handed to the side stream behind an event recorded
+        # on the caller's stream AFTER the iterator produced it (device work
+        # a lazy generator queues inside next() is then visible to the side)
+        if side is main:
+            return None
+        ev = torch.cuda.Event()
+        ev.record(main)
+        return ev
+
     it = iter(pencils)
     first = next(it, None)
-    staged = _stage(first, side) if first is not None else None
+    staged = _stage(first, side, produced()) if first is not None else None
     prefetch = None
     if staged is not None:
         _reserve_outputs(staged[0], cfg, pencils)
@@ -261,7 +281,7 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
             if nxt is None:
                 staged = None
             elif side is not main:
-                staged = submit(_stage, nxt, side)
+                staged = submit(_stage, nxt, side, produced())
             else:
                 staged = _stage(nxt, side)
             t_stage = time.perf_counter() - t1
