@@ -408,3 +408,19 @@ def run_sequence(pencils, nev, nex, deg, tol=1e-10, seed=0, mode="chained",
         out.append(dict(label=label, values=vals, vectors=vecs, x=x, report=rep, wall=wall,
                         filter_flops=8.0 * h.shape[0] ** 2 * rep.filter_degree_sum))
     return out
+
+
+def match_eigenvectors(y_prev, y_next):
+    """Greedy one-to-one matching of standard-form vectors by the cross-Gram
+    |Y_prev^H Y_next|, largest entry first via repeated argmax; restates
+    sequence.py:187-220. Returns (sigma, theta)."""
+    m = min(y_prev.shape[1], y_next.shape[1])
+    gram = np.abs(y_prev[:, :m].conj().T @ y_next[:, :m])
+    work = gram.copy()
+    sigma = np.full(m, -1, dtype=int)
+    for _ in range(m):
+        i, j = np.unravel_index(np.argmax(work), work.shape)
+        sigma[i] = j
+        work[i, :] = -1.0
+        work[:, j] = -1.0
+    return sigma, np.arccos(np.minimum(1.0, gram[np.arange(m), sigma]))

@@ -13,6 +13,10 @@ Layout rules of the device path:
 
 from __future__ import annotations
 
+import contextlib
+import os
+import threading
+
 import numpy as np
 import torch
 
@@ -121,3 +125,59 @@ def to_host(x):
     if isinstance(x, torch.Tensor):
         return x.detach().cpu().numpy()
     return np.asarray(x)
+
+
+# ------------------------------------------------------ array payloads ---
+# The reference returns numpy arrays (linalg.py:5-6: "outputs are fresh
+# arrays") and its callers do numpy arithmetic on them (harness.py:263-265,
+# sequence.py:209). Policy for the n-sized outputs of the drop-in functions:
+#   "auto"  (default) numpy out when every array input was host memory
+#           (numpy / lists), CUDA tensors out when any input was a CUDA
+#           tensor — a numpy caller gets the reference's types, a device
+#           caller keeps everything in HBM;
+#   "numpy" always numpy;   "torch" always device tensors.
+# The arithmetic runs on the device either way; "numpy" only adds the D2H.
+_OUTPUT_MODES = ("auto", "numpy", "torch")
+_output_default = os.environ.get("CHFSI_ARRAY_OUTPUT", "auto")
+if _output_default not in _OUTPUT_MODES:
+    raise ValueError(f"CHFSI_ARRAY_OUTPUT must be one of {_OUTPUT_MODES}, got {_output_default!r}")
+_output_local = threading.local()
+
+
+def set_array_output(mode):
+    """Set the process-wide payload policy ("auto", "numpy" or "torch")."""
+    global _output_default
+    if mode not in _OUTPUT_MODES:
+        raise ValueError(f"array output mode must be one of {_OUTPUT_MODES}, got {mode!r}")
+    _output_default = mode
+
+
+def get_array_output():
+    return getattr(_output_local, "mode", None) or _output_default
+
+
+@contextlib.contextmanager
+def array_output(mode):
+    """Thread-local override of the payload policy inside a with-block."""
+    if mode not in _OUTPUT_MODES:
+        raise ValueError(f"array output mode must be one of {_OUTPUT_MODES}, got {mode!r}")
+    prev = getattr(_output_local, "mode", None)
+    _output_local.mode = mode
+    try:
+        yield
+    finally:
+        _output_local.mode = prev
+
+
+def host_output(*inputs):
+    """True when the outputs of a call on ``inputs`` go back as numpy."""
+    mode = get_array_output()
+    if mode != "auto":
+        return mode == "numpy"
+    return not any(isinstance(x, (torch.Tensor, Operator)) or getattr(x, "device_input", False)
+                   for x in inputs if x is not None)
+
+
+def emit(x, host):
+    """``x`` as the caller's payload type (numpy copy when ``host``)."""
+    return to_host(x) if host and isinstance(x, torch.Tensor) else x

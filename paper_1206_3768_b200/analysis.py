@@ -38,7 +38,7 @@ class AngleReport:
 def _standard_vectors(sol, l_factor):
     if sol.form == "standard":
         return to_fblock(sol.vectors)
-    return forward_transform(l_factor, sol.vectors)
+    return to_fblock(forward_transform(to_fblock(l_factor), to_fblock(sol.vectors)))
 
 
 def greedy_match(gram):
@@ -87,7 +87,7 @@ def angle_report(pencils, solutions, fraction=1.0):
     solutions) in the same order as ``solutions``."""
     if not 0 < fraction <= 1:
         raise ValueError("fraction must be in (0, 1]")
-    pencils = list(pencils)
+    pencils = list(getattr(pencils, "pencils", pencils))  # a PencilSequence or pencils
     if len(solutions) != len(pencils):
         raise ValueError(f"need one solution per pencil ({len(pencils)}), got {len(solutions)}")
     report = AngleReport()

@@ -30,7 +30,7 @@ import numpy as np
 import scipy.linalg
 import torch
 
-from ._device import Operator, fblock, ld_of, to_fblock
+from ._device import Operator, emit, fblock, host_output, ld_of, to_fblock, to_host
 from ._lib import ALLREDUCE_CB, FILL_CB, FILTER_CB, GATHER_CB, HP_CB, LoopState, check, ctx, dptr, lib
 from .linalg import qr_orthonormalize_inplace
 from .reduction import EigenSolution
@@ -325,6 +325,7 @@ def chebyshev_filter(h, y, deg, window):
     block, ``y`` is untouched. ``deg`` may also be a sequence of per-column
     degrees (additive): column j is then filtered with degree
     ``deg[j]``."""
+    host = host_output(h, y)
     op = Operator.wrap(h)
     ym = to_fblock(y)
     if ym.shape[0] != op.n:
@@ -334,7 +335,7 @@ def chebyshev_filter(h, y, deg, window):
         if deg < 1:
             raise ValueError("polynomial degree must be >= 1")
         a, b = fblock(n, w), fblock(n, w)
-        return _filter_into(op, ym, a, b, int(deg), window)
+        return emit(_filter_into(op, ym, a, b, int(deg), window), host)
     degs = np.asarray(deg, dtype=np.int64)
     if degs.shape != (w,) or (degs < 1).any():
         raise ValueError("need one polynomial degree >= 1 per column")
@@ -352,10 +353,10 @@ def chebyshev_filter(h, y, deg, window):
                                        ctypes.byref(res)), "chebyshev_filter")
     out = a if res.value == a.data_ptr() else b
     if ident:
-        return out
+        return emit(out, host)
     inv = np.empty(w, dtype=np.int64)
     inv[order] = np.arange(w)
-    return to_fblock(out.index_select(1, torch.from_numpy(inv).to(out.device)))
+    return emit(to_fblock(out.index_select(1, torch.from_numpy(inv).to(out.device))), host)
 
 
 def chebyshev_response(lam, deg, window):
@@ -415,7 +416,8 @@ def _rr_core(op, panel, hp, g, rot_p, rot_hp, ritz_d, res_d, eig_tol=0.0):
 
 def rayleigh_ritz(h, y):
     """Rayleigh-Ritz projection onto the orthonormal block ``y``
-    (chfsi.py:228-239): ascending Ritz values (host) and ``y @ w`` (device)."""
+    (chfsi.py:228-239): ascending Ritz values (host) and ``y @ w``."""
+    host = host_output(h, y)
     op = Operator.wrap(h)
     ym = to_fblock(y)
     n, w = ym.shape
@@ -424,7 +426,7 @@ def rayleigh_ritz(h, y):
     ritz_d = torch.empty(w, dtype=torch.float64, device=ym.device)
     res_d = torch.empty(w, dtype=torch.float64, device=ym.device)
     _rr_core(op, ym, hp, g, rot_p, rot_hp, ritz_d, res_d)
-    return ritz_d.cpu().numpy(), rot_p
+    return ritz_d.cpu().numpy(), emit(rot_p, host)
 
 
 # ------------------------------------------------------------ orthonormal ---
@@ -573,10 +575,13 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     of column groups of the unfused filter. Every rank returns the same full
     solution; ``report.tail_vectors`` holds this rank's rows.
 
-    Returns ``(EigenSolution(form="standard"), SolveReport)``; the solution
-    vectors stay on the device.
+    Returns ``(EigenSolution(form="standard"), SolveReport)``. The solution
+    vectors are numpy when ``h`` (and the guess) came from host memory, as
+    in the reference, and stay on the device for device inputs
+    (`set_array_output`); ``report.tail_vectors`` always stays on the device.
     """
     t0 = time.perf_counter()
+    host = host_output(h, None if guess is None else guess.vectors)
     pre = rng if isinstance(rng, PrefetchedStart) else None
     rng = pre.rng if pre is not None else as_rng(rng)
     op = Operator.wrap(h)
@@ -716,8 +721,9 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     if comm is not None:  # every rank returns the full vectors
         full = fblock(n, nlocked, dev)
         vecs = comm.gather_rows(to_fblock(vecs, copy=True), full)
-    sol = EigenSolution(values=np.asarray(locked_vals)[order], vectors=to_fblock(vecs, copy=True),
-                        form="standard", label=label)
+    vecs = to_host(vecs) if host else to_fblock(vecs, copy=True)
+    sol = EigenSolution(values=np.asarray(locked_vals)[order], vectors=vecs, form="standard",
+                        label=label)
     report.final_residuals = np.asarray(locked_res)[order]
     torch.cuda.current_stream().synchronize()
     report.t_lanczos = t_lz.seconds()

@@ -1,7 +1,11 @@
-"""Sequence driver on the device — drop-in for the solver path of
-`spectral_chain.harness` (reference `harness.py:149-289`).
+"""Sequence drivers on the device — drop-in for `spectral_chain.harness`
+(reference `harness.py:149-336`).
 
-Two protocols over a correlated sequence of pencils (label 1..N):
+`run_experiment(spec)` is the reference's four-stage warm-start experiment
+(dense oracle of problem l-1 -> random-start and warm-start ChFSI cells of
+problem l -> oracle check -> report rows), `emit_report` its CSV/JSON
+writer. `solve_sequence` (additive) is the production driver with two
+protocols over a correlated sequence of pencils (label 1..N):
 
 * ``mode="harness"`` — the reference's parity protocol (harness.py:235-255):
   problem l >= 2 is warm-started from the DENSE eigendecomposition of
@@ -17,22 +21,38 @@ runs to_standard -> chfsi_solve -> back_transform on the device.
 
 from __future__ import annotations
 
+import csv
 import gc
+import json
 import os
+import statistics
 import time
 from concurrent.futures import Future, ThreadPoolExecutor, wait
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
+from pathlib import Path
 
 import numpy as np
 import torch
 
+from ._device import array_output, to_device_matrix
 from .chfsi import ChfsiConfig, ChfsiGuess, PrefetchedStart, chfsi_solve
 from .linalg import hermitian_eig
 from .reduction import EigenPencil, EigenSolution, back_transform, stage_standard, to_standard
 
 __all__ = [
+    "GenerateSource",
+    "LoadSource",
+    "BaselineSource",
+    "ExperimentSpec",
+    "ExperimentRow",
+    "ExperimentReport",
     "OracleMismatchError",
+    "SOLVERS",
+    "REPORT_FIELDS",
     "oracle_solve",
+    "run_experiment",
+    "emit_report",
+    "replace_tracked",
     "ProblemResult",
     "solve_sequence",
     "check_oracle",
@@ -347,3 +367,249 @@ def default_config(cfg):
     """ChfsiConfig for a BASELINE config (sequence.BaselineConfig)."""
     return ChfsiConfig(nev=cfg.nev, nex=cfg.nex, deg=cfg.deg, tol=cfg.tol,
                        adaptive_degree=cfg.adaptive_degree)
+
+
+# ------------------------------------------------ the experiment protocol ---
+# run_experiment(spec) -> ExperimentReport: the reference's four-stage
+# warm-start experiment (harness.py:188-289) with every solve on the device.
+
+# The reference's solver names (harness.py:45); only ChFSI is the hot path
+# this package rebuilds, the LOBPCG baselines stay in the reference.
+SOLVERS = ("chfsi", "lobpcg", "lobpcg-generalized")
+_OUT_OF_SCOPE = ("lobpcg", "lobpcg-generalized")
+
+REPORT_FIELDS = [  # CSV schema (harness.py:52-65); JSON rows carry the same keys
+    "ell", "t_random_s", "t_approx_s", "speedup_time", "matvecs_random", "matvecs_approx",
+    "speedup_matvec", "filtered_random", "filtered_approx", "inner_loops_random",
+    "inner_loops_approx", "median_angle",
+]
+
+
+@dataclass
+class GenerateSource:
+    """Generate with the reference's generator (harness.py:72-78)."""
+
+    n: int
+    schedule: object  # sequence.CorrelationSchedule
+    seed: int = 0
+
+
+@dataclass
+class LoadSource:
+    """A saved sequence directory: npy or the reference's Matrix Market
+    files (harness.py:81-85)."""
+
+    directory: str
+
+
+@dataclass
+class BaselineSource:
+    """Additive: the BASELINE.json generator (`sequence.iter_baseline_sequence`),
+    computed on the device when ``device`` is true."""
+
+    n: int
+    length: int
+    seed: int = 0
+    device: bool = True
+
+
+@dataclass
+class ExperimentSpec:
+    """harness.py:88-107 — same fields, defaults and validation."""
+
+    source: object
+    solver: str
+    nev: int
+    solver_overrides: dict = field(default_factory=dict)
+    tracked_fraction: float = 1.0
+    repetitions: int = 5
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.solver not in SOLVERS:
+            raise ValueError(f"unknown solver {self.solver!r}, expected one of {SOLVERS}")
+        if self.repetitions < 1:
+            raise ValueError("repetitions must be >= 1")
+        if not 0 < self.tracked_fraction <= 1:
+            raise ValueError("tracked_fraction must be in (0, 1]")
+        if self.nev < 1:
+            raise ValueError("nev must be >= 1")
+
+
+@dataclass
+class ExperimentRow:
+    """One compared problem, labels 2..N (harness.py:110-129)."""
+
+    ell: int
+    t_random_s: float
+    t_approx_s: float
+    speedup_time: float
+    matvecs_random: int
+    matvecs_approx: int
+    speedup_matvec: float
+    filtered_random: int
+    filtered_approx: int
+    inner_loops_random: int
+    inner_loops_approx: int
+    median_angle: float
+    max_residual_random: float
+    max_residual_approx: float
+    converged_random: bool
+    converged_approx: bool
+
+
+@dataclass
+class ExperimentReport:
+    """harness.py:132-146."""
+
+    rows: list
+    n: int
+    length: int
+    solver: str
+    nev: int
+    blk: int
+    repetitions: int
+    tracked_fraction: float
+    seed: int
+    warnings: list = field(default_factory=list)
+
+    @property
+    def all_converged(self):
+        return all(r.converged_random and r.converged_approx for r in self.rows)
+
+
+def replace_tracked(sol, count):
+    """The lowest ``count`` pairs of a solution (harness.py:292-295)."""
+    count = min(count, sol.nev)
+    return replace(sol, values=sol.values[:count], vectors=sol.vectors[:, :count])
+
+
+def _source_pencils(source):
+    """(n, length, lazy iterator of device EigenPencils) of a spec source."""
+    from . import pencil_io
+    from .sequence import iter_baseline_sequence, iter_generated_sequence
+
+    def device_pencils(items):
+        for lab, a, b in items:
+            # (memory-mapped files are read-only: np.require copies those)
+            yield EigenPencil(a=to_device_matrix(np.require(a, requirements=["C", "W"]))
+                              if not isinstance(a, torch.Tensor) else a,
+                              b=to_device_matrix(np.require(b, requirements=["C", "W"]))
+                              if not isinstance(b, torch.Tensor) else b, label=lab)
+
+    if isinstance(source, GenerateSource):
+        if source.n < 4:
+            raise ValueError("need dimension >= 4")
+        return (source.n, source.schedule.length,
+                device_pencils(iter_generated_sequence(source.n, source.schedule, source.seed)))
+    if isinstance(source, BaselineSource):
+        dev = torch.cuda.current_device() if source.device else None
+        return (source.n, source.length,
+                device_pencils(iter_baseline_sequence(source.n, source.length, source.seed,
+                                                      device=dev)))
+    if isinstance(source, LoadSource):
+        n, length, _ = pencil_io._manifest(source.directory)
+        return n, length, device_pencils(pencil_io.iter_sequence(source.directory))
+    raise TypeError(f"unknown sequence source {type(source).__name__}")
+
+
+def run_experiment(spec):
+    """The four-stage warm-start experiment over a whole sequence
+    (harness.py:188-289), on the device.
+
+    For every problem l = 2..N: (1) the dense solution of problem l-1 (the
+    previous iteration's oracle: cuSOLVER zheevd of its standard form) gives
+    the warm block — its lowest blk vectors, lambda_1 and lambda_{blk+1};
+    (2) ChFSI from random vectors, rng (seed, l, 0); (3) ChFSI from the warm
+    block, rng (seed, l, 1) — each ``repetitions`` times, the median wall time
+    reported; (4) both converged results are checked against the dense
+    spectrum of problem l (|dlambda| <= 1e-8 * scale, OracleMismatchError)
+    and the tracked vectors of the two dense solutions are matched to give
+    the median deviation angle. Pencils are streamed: only the previous
+    problem's dense block lives across iterations.
+    """
+    if spec.solver in _OUT_OF_SCOPE:
+        raise NotImplementedError(
+            f"solver {spec.solver!r}: this package rebuilds the ChFSI path only; "
+            "the LOBPCG baselines stay in the reference")
+    from .analysis import match_eigenvectors
+
+    with array_output("torch"):  # everything n-sized stays in HBM here
+        n, length, pencils = _source_pencils(spec.source)
+        cfg = ChfsiConfig(nev=spec.nev, **spec.solver_overrides)
+        blk = cfg.resolve(n)[0]
+        report = ExperimentReport(rows=[], n=n, length=length, solver=spec.solver, nev=spec.nev,
+                                  blk=blk, repetitions=spec.repetitions,
+                                  tracked_fraction=spec.tracked_fraction, seed=spec.seed)
+        warnings = []
+        if length < 2:
+            warnings.append("sequence has a single problem; nothing to compare")
+            report.warnings = warnings
+            return report
+        if blk >= n:
+            raise ValueError(
+                f"chfsi warm starts need blk < n for the window eigenvalue (blk={blk}, n={n})")
+        tracked = max(1, int(np.ceil(spec.tracked_fraction * spec.nev)))
+        keep = max(blk + 1, spec.nev)
+
+        def cell(problem, guess, cell_seed, label):
+            times, sol, rep = [], None, None
+            for _ in range(spec.repetitions):
+                sol, rep = chfsi_solve(problem.h, cfg, guess=guess,
+                                       rng=np.random.default_rng(cell_seed), label=label)
+                times.append(rep.wall_time)
+            return sol, rep, statistics.median(times)
+
+        it = iter(pencils)
+        prev_sol, _, prev_vals = oracle_solve(next(it), keep)
+        for pencil in it:
+            sol_now, sp_now, vals_now = oracle_solve(pencil, keep)
+            guess = ChfsiGuess(vectors=prev_sol.vectors[:, :blk], lambda1=float(prev_vals[0]),
+                               lambda_blk_plus_1=float(prev_vals[blk]))
+            lab = pencil.label
+            del pencil
+            sol_r, rep_r, t_r = cell(sp_now, None, (spec.seed, lab, 0), lab)
+            sol_a, rep_a, t_a = cell(sp_now, guess, (spec.seed, lab, 1), lab)
+            del sp_now, guess
+            for rep, sol, start in ((rep_r, sol_r, "random"), (rep_a, sol_a, "approximate")):
+                if rep.converged:
+                    check_oracle(sol.values, vals_now, lab, start)
+                else:
+                    warnings.append(f"problem {lab}: {start} start did not converge")
+            _, theta = match_eigenvectors(replace_tracked(prev_sol, tracked), None,
+                                          replace_tracked(sol_now, tracked), None)
+            report.rows.append(ExperimentRow(
+                ell=lab, t_random_s=t_r, t_approx_s=t_a,
+                speedup_time=t_r / t_a if t_a > 0 else float("inf"),
+                matvecs_random=rep_r.matvecs, matvecs_approx=rep_a.matvecs,
+                speedup_matvec=rep_r.matvecs / rep_a.matvecs if rep_a.matvecs else float("inf"),
+                filtered_random=rep_r.filtered_vectors, filtered_approx=rep_a.filtered_vectors,
+                inner_loops_random=rep_r.inner_loops, inner_loops_approx=rep_a.inner_loops,
+                median_angle=float(np.median(theta)),
+                max_residual_random=float(rep_r.final_residuals.max(initial=0.0)),
+                max_residual_approx=float(rep_a.final_residuals.max(initial=0.0)),
+                converged_random=rep_r.converged, converged_approx=rep_a.converged))
+            prev_sol, prev_vals = sol_now, vals_now
+        report.warnings = warnings
+        return report
+
+
+def _row_record(row):
+    return {k: getattr(row, k) for k in REPORT_FIELDS}
+
+
+def emit_report(report, fmt, path):
+    """Write the rows as CSV (columns exactly REPORT_FIELDS) or as a JSON
+    list of row objects (harness.py:316-336)."""
+    path = Path(path)
+    records = [_row_record(r) for r in report.rows]
+    if fmt == "csv":
+        with open(path, "w", newline="") as fh:
+            w = csv.DictWriter(fh, fieldnames=REPORT_FIELDS)
+            w.writeheader()
+            w.writerows(records)
+    elif fmt == "json":
+        with open(path, "w") as fh:
+            json.dump(records, fh, indent=2)
+    else:
+        raise ValueError(f"unknown report format {fmt!r}")

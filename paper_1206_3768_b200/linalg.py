@@ -3,9 +3,10 @@
 Same names, argument meaning and exceptions as the reference
 (`spectral_chain/linalg.py`), computed in HBM by libchfsi (hand-written
 sm_100a kernels plus cuBLAS/cuSOLVER for the factorizations). Inputs may be
-numpy arrays (uploaded) or CUDA tensors (used in place); outputs are CUDA
-tensors in column-major "F-block" layout (`_device.py`). Inputs are never
-modified.
+numpy arrays (uploaded) or CUDA tensors (used in place); outputs are numpy
+arrays for host inputs (as the reference's) and CUDA tensors in column-major
+"F-block" layout for device inputs (`_device.py`, `set_array_output`).
+Inputs are never modified.
 """
 
 from __future__ import annotations
@@ -16,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import Operator, fblock, ld_of, to_device_matrix, to_fblock
+from ._device import Operator, emit, fblock, host_output, ld_of, to_device_matrix, to_fblock
 from ._lib import check, ctx, dptr, lib
 from .linalg_errors import (
     EigenSolverError,
@@ -54,8 +55,16 @@ def hermitian_defect(m):
 
 
 def hermitian_view(m, tol=None):
-    """Validate that ``m`` is Hermitian; return it as a device complex128
-    tensor (linalg.py:61-85). Raises NotHermitianError."""
+    """Validate that ``m`` is Hermitian (linalg.py:61-85); returns it as a
+    complex128 array of the caller's payload type. Raises NotHermitianError."""
+    host = host_output(m)
+    t = _hermitian_device(m, tol)
+    return np.asarray(m, dtype=np.complex128) if host and not isinstance(m, torch.Tensor) \
+        else emit(t, host)
+
+
+def _hermitian_device(m, tol=None):
+    """hermitian_view's check, returning the device tensor (internal)."""
     t = to_device_matrix(m)
     if t.dim() != 2 or t.shape[0] != t.shape[1]:
         raise NotHermitianError(f"expected a square matrix, got shape {tuple(t.shape)}")
@@ -74,6 +83,7 @@ def gemm(alpha, a, b, beta=0.0, c=None, trans_a="N", trans_b="N"):
     """``alpha * op(a) @ op(b) + beta * c`` on the device (linalg.py:91-113)."""
     if trans_a not in _OPS or trans_b not in _OPS:
         raise ValueError(f"unknown transpose flags ({trans_a!r}, {trans_b!r})")
+    host = host_output(a, b, c)
     am, bm = to_fblock(a), to_fblock(b)
     m, ka = (am.shape[1], am.shape[0]) if trans_a != "N" else (am.shape[0], am.shape[1])
     kb, n = (bm.shape[1], bm.shape[0]) if trans_b != "N" else (bm.shape[0], bm.shape[1])
@@ -94,18 +104,19 @@ def gemm(alpha, a, b, beta=0.0, c=None, trans_a="N", trans_b="N"):
     check(lib().chfsi_gemm_z(ctx(), trans_a.encode(), trans_b.encode(), m, n, ka, al.real, al.imag,
                              dptr(am), ld_of(am), dptr(bm), ld_of(bm), be.real, be.imag, dptr(out),
                              ld_of(out)), "gemm")
-    return out
+    return emit(out, host)
 
 
 def cholesky(b):
     """Lower Cholesky factor with positive diagonal (linalg.py:116-129)."""
-    t = hermitian_view(b)
+    host = host_output(b)
+    t = _hermitian_device(b)
     n = t.shape[0]
     l = to_fblock(t, copy=True)
     info = ctypes.c_int()
     status = lib().chfsi_potrf_z(ctx(), n, dptr(l), ld_of(l), ctypes.byref(info))
     check(status, "cholesky")
-    return l
+    return emit(l, host)
 
 
 def _diag_host(t):
@@ -114,6 +125,7 @@ def _diag_host(t):
 
 def triangular_solve(l, x, conjugate_transpose=False):
     """Solve ``L Z = X`` or ``L^H Z = X`` (linalg.py:132-149); never forms an inverse."""
+    host = host_output(l, x)
     lm = to_fblock(l)
     xm = to_fblock(x, copy=True)
     if lm.shape[0] != lm.shape[1]:
@@ -126,7 +138,7 @@ def triangular_solve(l, x, conjugate_transpose=False):
     check(lib().chfsi_trsm_z(ctx(), b"L", b"C" if conjugate_transpose else b"N", xm.shape[0],
                              xm.shape[1], dptr(lm), ld_of(lm), dptr(xm), ld_of(xm)),
           "triangular_solve")
-    return xm
+    return emit(xm, host)
 
 
 def qr_orthonormalize_inplace(y):
@@ -148,24 +160,26 @@ def qr_orthonormalize(y):
     """Householder QR orthonormalization, positive-real R diagonal
     (linalg.py:152-178). Raises RankDeficientError when a column's
     post-projection norm falls below 1e-13 ||y||_F."""
+    host = host_output(y)
     t = to_fblock(y, copy=True)
     if t.shape[0] < t.shape[1]:
         raise ValueError(f"need rows >= cols, got {tuple(t.shape)}")
     if ld_of(t) != t.shape[0]:
         t = t.contiguous().t().contiguous().t()
-    return qr_orthonormalize_inplace(t)
+    return emit(qr_orthonormalize_inplace(t), host)
 
 
 def hermitian_eig(g, want_vectors=True):
     """Full eigendecomposition of a Hermitian matrix (linalg.py:181-206).
 
     Returns ascending values (host numpy) and, when requested, the
-    eigenvectors as a device F-block.
+    eigenvectors (device F-block, or numpy for a host input).
     """
-    t = hermitian_view(g)
+    host = host_output(g)
+    t = _hermitian_device(g)
     n = t.shape[0]
     a = to_fblock(t, copy=True)
     w = torch.empty(n, dtype=torch.float64, device=a.device)
     check(lib().chfsi_heevd_z(ctx(), n, dptr(a), ld_of(a), dptr(w)), "hermitian_eig")
     vals = w.cpu().numpy()
-    return (vals, a) if want_vectors else (vals, None)
+    return (vals, emit(a, host)) if want_vectors else (vals, None)

@@ -32,11 +32,15 @@ minutes of host LAPACK to the time of its random draws.
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
 __all__ = [
+    "CorrelationSchedule",
+    "PencilSequence",
+    "generate_sequence",
+    "iter_generated_sequence",
     "BaselineConfig",
     "BASELINE_CONFIGS",
     "complex_gaussian",
@@ -196,3 +200,140 @@ def _device_sequence(n, length, seed, device):
 def generate_baseline_sequence(n, length, seed=0):
     """Materialize the whole sequence as a list of ``(label, A, B)``."""
     return list(iter_baseline_sequence(n, length, seed))
+
+
+# ------------------------------------------- the reference's own generator ---
+# `run_experiment(ExperimentSpec(source=GenerateSource(...)))` feeds the
+# reference generator (sequence.py:36-178), so that source is restated here
+# with the same draw order; the arithmetic is numpy on the host like the
+# reference's (it fixes the input bytes — np.linalg.qr's unphased Q is part
+# of B), only the positive-definiteness probe of each B runs on the device
+# (the library's potrf).
+
+_EPS0, _DECAY = 0.5, 0.45  # geometric default, sequence.py:33-34
+
+
+@dataclass
+class CorrelationSchedule:
+    """Perturbation magnitudes between adjacent problems
+    (sequence.py:37-76): ``eps[i]`` takes problem i+1 to i+2 (A update),
+    B is perturbed with eps/10 when ``perturb_b``."""
+
+    length: int
+    eps: list | None = None
+    perturb_b: bool = True
+    b_cond_target: float = 1e6
+
+    def __post_init__(self):
+        if self.length < 1:
+            raise ValueError("a sequence has at least one problem")
+        if self.eps is None:
+            self.eps = [_EPS0 * _DECAY ** i for i in range(self.length - 1)]
+        self.eps = [float(x) for x in self.eps]
+        if len(self.eps) != self.length - 1:
+            raise ValueError(f"need {self.length - 1} perturbation magnitudes, got {len(self.eps)}")
+        if min(self.eps, default=0.0) < 0:
+            raise ValueError("perturbation magnitudes must be non-negative")
+        if self.b_cond_target < 1:
+            raise ValueError("condition target must be >= 1")
+
+    @classmethod
+    def geometric(cls, length, eps0=_EPS0, decay=_DECAY, **kwargs):
+        if eps0 <= 0 or not 0 < decay <= 1:
+            raise ValueError("need eps0 > 0 and 0 < decay <= 1")
+        return cls(length=length, eps=[eps0 * decay ** i for i in range(length - 1)], **kwargs)
+
+
+@dataclass
+class PencilSequence:
+    """Pencils labelled 1..N of one dimension (sequence.py:79-101)."""
+
+    pencils: list
+    provenance: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        if not self.pencils:
+            raise ValueError("empty sequence")
+        n = self.pencils[0].n
+        for pos, p in enumerate(self.pencils):
+            if p.label != pos + 1:
+                raise ValueError(f"labels must run 1..N, found {p.label} at position {pos}")
+            if p.n != n:
+                raise ValueError("all pencils must share one dimension")
+
+    def __len__(self):
+        return len(self.pencils)
+
+    def __iter__(self):
+        return iter(self.pencils)
+
+    @property
+    def n(self):
+        return self.pencils[0].n
+
+
+def _gaussian_hermitian(rng, n):
+    """(G + G^H)/2 of G = (N + iN)/sqrt(2) (sequence.py:117-119)."""
+    g = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(2)
+    return (g + g.conj().T) / 2
+
+
+def _b_is_hpd(b):
+    from .linalg import cholesky
+    from .linalg_errors import NotPositiveDefiniteError
+
+    try:
+        cholesky(b)
+    except NotPositiveDefiniteError:
+        return False
+    return True
+
+
+def iter_generated_sequence(n, schedule, seed=None):
+    """Lazily yield ``(label, A, B)`` host arrays of the reference generator
+    (sequence.py:137-178, same draws in the same order): A1 Gaussian
+    Hermitian, B1 = Q diag(logspace(0, log10 cond, n)) Q^H from the
+    unphased QR of a complex Gaussian (sequence.py:127-134); then
+    A += eps * D / max|D| and B += s * F / max|F| with s = eps/10 halved
+    (up to 5 times) until B stays positive definite."""
+    if n < 4:
+        raise ValueError("need dimension >= 4")
+    rng = seed if isinstance(seed, np.random.Generator) else np.random.default_rng(seed)
+    a = _gaussian_hermitian(rng, n)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    spd = (q * np.logspace(0.0, np.log10(schedule.b_cond_target), n)) @ q.conj().T
+    b = (spd + spd.conj().T) / 2
+    del q, spd
+    yield 1, a, b
+    for i, eps in enumerate(schedule.eps):
+        d = _gaussian_hermitian(rng, n)
+        a = a + eps * (d / np.abs(d).max())
+        if schedule.perturb_b:
+            f = _gaussian_hermitian(rng, n)
+            f = f / np.abs(f).max()
+            scale = eps / 10
+            for attempt in range(6):
+                cand = b + scale * f
+                if _b_is_hpd(cand):
+                    break
+                if attempt == 5:
+                    from .linalg_errors import NotPositiveDefiniteError
+
+                    raise NotPositiveDefiniteError(
+                        f"overlap update {i + 1} breaks positive definiteness after 5 halvings")
+                scale /= 2
+            b = cand
+        yield i + 2, a, b
+
+
+def generate_sequence(n, schedule, seed=None):
+    """The reference generator as a PencilSequence of device EigenPencils
+    (sequence.py:137-178)."""
+    from .reduction import EigenPencil
+
+    pencils = [EigenPencil(a=a, b=b, label=lab)
+               for lab, a, b in iter_generated_sequence(n, schedule, seed)]
+    return PencilSequence(pencils=pencils, provenance={
+        "kind": "generated", "n": n, "length": schedule.length, "eps": list(schedule.eps),
+        "perturb_b": schedule.perturb_b, "b_cond_target": schedule.b_cond_target,
+        "seed": None if isinstance(seed, np.random.Generator) else seed})

@@ -14,6 +14,27 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built libchfsi.so")
     config.addinivalue_line("markers", "slow: long-running parity case")
+    config.addinivalue_line("markers", "host_payloads: run under the default ('auto') array "
+                            "payload policy instead of the device-resident one")
+
+
+@pytest.fixture(autouse=True)
+def _device_payloads(request):
+    """GPU tests exercise the device-resident API: n-sized results stay CUDA
+    tensors even for numpy inputs (payload policy "torch"). Tests marked
+    ``host_payloads`` check the drop-in default instead (numpy in, numpy out)."""
+    if request.node.get_closest_marker("gpu") is None or \
+            request.node.get_closest_marker("host_payloads") is not None:
+        yield
+        return
+    from paper_1206_3768_b200 import _device
+
+    prev = _device._output_default
+    _device.set_array_output("torch")
+    try:
+        yield
+    finally:
+        _device.set_array_output(prev)
 
 
 @pytest.fixture(scope="session")
