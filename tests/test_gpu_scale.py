@@ -1,0 +1,190 @@
+"""Parity at BASELINE scale against the reference (B200 only, slow).
+
+Fixtures: `tests/golden/c{2,3,4,5}_scale.npz`, written by
+`tests/golden/make_golden_scale.py` from the UNMODIFIED reference
+(`chfsi_solve`, `to_standard`, `oracle_solve`, harness cells
+harness.py:235-261) and, for the chained cells, the oracle's chained driver
+(the restatement pinned to the reference by test_oracle_golden):
+
+* C2: all 10 problems chained (the bench workload);
+* C3: all 12 problems — dense oracle, random-start and dense-warm-start
+  cells, and the chained sequence;
+* C4: problems 1-2 (cold, and warm from the dense oracle of problem 1);
+* C5: problem 1 cold at the fixed degree cap 36.
+
+Per cell, `north_star`'s bar: eigenvalues within 1e-9 relative, every
+residual <= tol, loops within +/-1 (matvecs within one loop's worth), and the
+largest principal angle to the reference ChFSI eigenspace <= 1e-6. The
+reference eigenvectors at these sizes are 40 MB - 1 GB per cell and are not
+stored; the angle is bounded through the dense eigenspaces instead:
+
+    sin(gpu, ref) <= sin(gpu, dense_gpu) + d(dense_gpu, dense_cpu) + sin(dense_cpu, ref)
+
+the first term measured here, the last measured by the fixture script on
+the reference's own vectors (`dense_sine`), and the middle one bounded by
+Davis-Kahan: each dense solve lies within ||R||_F / gap of the exact
+eigenspace (gap = lambda_{nev+1} - lambda_nev of the dense spectrum).
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import chfsi_oracle as orc  # noqa: F401  (checker only)
+from tests.conftest import GOLDEN, subspace_sines
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+PROBE = (97, 89)
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_1206_3768_b200 as p
+
+    assert torch.cuda.is_available()
+    return p
+
+
+def _fixture(name):
+    path = os.path.join(GOLDEN, f"{name}_scale.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{name}_scale.npz not generated (tests/golden/make_golden_scale.py)")
+    g = np.load(path)
+    return g, set(str(c) for c in g["done_cells"])
+
+
+def _inputs(pkg, cfg_b, length, device):
+    """The BASELINE sequence; C4/C5 from the device generator (equal to the
+    host generator to rounding, tests/test_gpu_io.py)."""
+    dev = torch.cuda.current_device() if device else None
+    return pkg.iter_baseline_sequence(cfg_b.n, length, seed=0, device=dev)
+
+
+def _check_probe(m, gold, key):
+    probe = gold[key]
+    got = m[:: PROBE[0], :: PROBE[1]]
+    got = got.cpu().numpy() if isinstance(got, torch.Tensor) else got
+    assert np.abs(got - probe).max() <= 1e-12 * np.abs(probe).max(), key
+
+
+def _dense(pkg, h, nev, blk):
+    """Device dense oracle: values, vectors (first blk+1), ||R||_F of nev."""
+    dv, dvec = pkg.hermitian_eig(h)
+    dvec = dvec[:, : blk + 1].clone()  # (drops the n x n eigenvector storage)
+    hv = pkg.gemm(1.0, h, dvec[:, :nev])
+    r = hv - dvec[:, :nev] * torch.from_numpy(dv[:nev]).to(hv.device)
+    return dv, dvec, float(torch.linalg.vector_norm(r))
+
+
+def _check_cell(sol, rep, gold, pre, cfg_b, dvec, dvals, r_gpu, label):
+    nev, blk, deg, tol = cfg_b.nev, cfg_b.nev + cfg_b.nex, cfg_b.deg, cfg_b.tol
+    assert rep.converged == bool(gold[pre + "converged"]), pre
+    loops = int(gold[pre + "inner_loops"])
+    assert abs(rep.inner_loops - loops) <= 1, (pre, rep.inner_loops, loops)
+    if rep.inner_loops == loops:
+        assert abs(rep.matvecs - int(gold[pre + "matvecs"])) <= (deg + 1) * blk, pre
+    assert rep.lanczos_matvecs == int(gold[pre + "lanczos_matvecs"]), pre
+    ref = gold[pre + "values"]
+    assert sol.values.shape == ref.shape, pre
+    assert np.abs(sol.values - ref).max() <= 1e-9 * np.abs(ref).max(), pre
+    assert (rep.final_residuals <= tol).all(), pre
+    # principal angle to the reference eigenspace (module docstring)
+    v = sol.vectors if isinstance(sol.vectors, torch.Tensor) else torch.from_numpy(sol.vectors)
+    s_gpu = float(torch.linalg.svdvals(v.cuda() - dvec[:, :nev] @ (dvec[:, :nev].conj().T
+                                                                  @ v.cuda())).max())
+    gap = float(dvals[nev] - dvals[nev - 1])
+    r_cpu = float(np.linalg.norm(gold[f"{label}/dense_residuals"]))
+    bound = s_gpu + (r_gpu + r_cpu) / gap + float(gold[pre + "dense_sine"])
+    assert bound <= 1e-6, (pre, s_gpu, (r_gpu + r_cpu) / gap, float(gold[pre + "dense_sine"]))
+    return bound
+
+
+def _cfg(pkg, cfg_b, adaptive=False):
+    return pkg.ChfsiConfig(nev=cfg_b.nev, nex=cfg_b.nex, deg=cfg_b.deg, tol=cfg_b.tol,
+                           adaptive_degree=adaptive)
+
+
+def _harness_cells(pkg, name, length, device=False, kinds=("cold", "warm")):
+    """Dense oracle + random/warm cells of the reference harness protocol."""
+    gold, done = _fixture(name)
+    cfg_b = pkg.BASELINE_CONFIGS[name.upper()]
+    cfg = _cfg(pkg, cfg_b)
+    blk = cfg_b.nev + cfg_b.nex
+    prev, checked = None, 0
+    for label, a, b in _inputs(pkg, cfg_b, length, device):
+        if f"{label}/dense" not in done:
+            break
+        _check_probe(a, gold, f"{label}/a_probe")
+        _check_probe(b, gold, f"{label}/b_probe")
+        sp = pkg.to_standard(pkg.EigenPencil(a=a, b=b, label=label))
+        del a, b
+        dv, dvec, r_gpu = _dense(pkg, sp.h, cfg_b.nev, blk)
+        np.testing.assert_allclose(dv[: blk + 1], gold[f"{label}/dense_values"], rtol=0, atol=1e-11)
+        for kind in kinds:
+            if f"{label}/{kind}" not in done or (kind == "warm" and prev is None):
+                continue
+            guess = prev if kind == "warm" else None
+            seed = (0, label, 1 if kind == "warm" else 0)
+            sol, rep = pkg.chfsi_solve(sp.h, cfg, guess=guess, rng=np.random.default_rng(seed))
+            _check_cell(sol, rep, gold, f"{label}/{kind}/", cfg_b, dvec, dv, r_gpu, label)
+            checked += 1
+            del sol
+        prev = pkg.ChfsiGuess(vectors=dvec[:, :blk], lambda1=float(dv[0]),
+                              lambda_blk_plus_1=float(dv[blk]))
+        del sp, dvec
+        torch.cuda.empty_cache()
+    return checked, done
+
+
+def _chained(pkg, name, length, device=False):
+    """The chained (production) driver vs the oracle's chained cells."""
+    gold, done = _fixture(name)
+    cfg_b = pkg.BASELINE_CONFIGS[name.upper()]
+    labels = [l for l in range(1, length + 1) if f"{l}/chained" in done]
+    if not labels:
+        pytest.skip(f"no chained cells in {name}_scale.npz yet")
+    n_chain = labels[-1]
+    assert labels == list(range(1, n_chain + 1))
+    seq = list(_inputs(pkg, cfg_b, n_chain, device))
+    res = pkg.solve_sequence(seq, _cfg(pkg, cfg_b), seed=0, mode="chained", keep_standard=True)
+    blk = cfg_b.nev + cfg_b.nex
+    for (label, a, b), r in zip(seq, res):
+        _check_probe(a, gold, f"{label}/a_probe")
+        sp = pkg.to_standard(pkg.EigenPencil(a=a, b=b, label=label))
+        dv, dvec, r_gpu = _dense(pkg, sp.h, cfg_b.nev, blk)
+        sol = pkg.EigenSolution(values=r.values, vectors=r.standard_vectors)
+        _check_cell(sol, r.report, gold, f"{label}/chained/", cfg_b, dvec, dv, r_gpu, label)
+        assert r.report.lambda_blk_plus_1 == pytest.approx(
+            float(gold[f"{label}/chained/lambda_blk_plus_1"]), rel=1e-9)
+        del sp, dvec
+    return n_chain
+
+
+def test_c2_chained_sequence_matches_oracle(pkg):
+    """The bench workload (C2, 10 problems chained)."""
+    assert _chained(pkg, "c2", 10) == 10
+
+
+def test_c3_harness_all_problems_match_reference(pkg):
+    checked, done = _harness_cells(pkg, "c3", 12)
+    assert checked >= 1
+    if "12/warm" in done:
+        assert checked == 23  # 12 random-start + 11 dense-warm-start cells
+
+
+def test_c3_chained_sequence_matches_oracle(pkg):
+    _chained(pkg, "c3", 12)
+
+
+def test_c4_problems_1_2_match_reference(pkg):
+    checked, _ = _harness_cells(pkg, "c4", 2, device=True)
+    assert checked >= 1
+
+
+def test_c5_problem_1_fixed_degree_matches_reference(pkg):
+    """C5 problem 1, cold, at the fixed degree cap 36 (the reference has no
+    adaptive-degree mode)."""
+    checked, _ = _harness_cells(pkg, "c5", 1, device=True, kinds=("cold",))
+    assert checked == 1
