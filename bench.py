@@ -22,9 +22,13 @@ Reported (one JSON line on rank 0):
 * ``cpu_baseline`` = the numpy oracle port of the reference path on this
   host's cores, on a bounded sample (problems 1-2 of the same sequence).
 
-Multi-GPU (torchrun, N>1): the sequence is not sharded at C1/C2 — every
-rank solves its own replica ("scaling": "weak", no data-path collective);
-value = N x sequence FLOPs / max-over-ranks time.
+Multi-GPU (torchrun, N>1): by default config C3 (n=5000, N=12) row-sharded
+over the ranks — H in 1-D row blocks, the panel all-gathered between filter
+steps ("scaling": "strong"; value = the sequence's FLOPs / max-over-ranks
+time). C1/C2 do not shard: ``--replicas`` (or ``--config C2``) runs one
+replica per rank ("scaling": "weak", no data-path collective). The N=1 line
+carries ``strong_scaling_base``: the single-GPU C3 value the sharded lines
+are measured against (``--no-scale-base`` skips it).
 """
 
 from __future__ import annotations
@@ -53,7 +57,8 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default=None,
+                    help="BASELINE config (default: C2 on one GPU, C3 row-sharded under torchrun)")
     ap.add_argument("--mode", choices=["chained", "harness"], default="chained")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gen", choices=["host", "device"], default="host",
@@ -66,7 +71,17 @@ def parse_args():
                     help="diagnostics: no side-stream reduction of the next problem")
     ap.add_argument("--shard", action="store_true",
                     help="row-shard the filter across the ranks (strong scaling, C3-C5)")
-    return ap.parse_args()
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: one independent replica of the sequence per rank (no sharding)")
+    ap.add_argument("--no-scale-base", action="store_true",
+                    help="N=1: skip the single-GPU C3 strong-scaling base measurement")
+    a = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if a.config is None:
+        a.config = "C3" if world > 1 and not a.replicas else "C2"
+    if world > 1 and not a.replicas and a.config in ("C3", "C4", "C5"):
+        a.shard = True
+    return a
 
 
 # ------------------------------------------------------------------ clocks ---
@@ -243,6 +258,44 @@ def run_reference(args):
 
 # --------------------------------------------------------------- GPU arm ---
 
+def time_sequence(pencils, cfg, steps, warmup, mode="chained"):
+    """Device time (s, median over steps) and filter FLOPs of one sequence
+    through solve_sequence (CUDA events on the caller's stream)."""
+    import torch
+
+    from paper_1206_3768_b200.harness import solve_sequence
+
+    for _ in range(warmup):
+        solve_sequence(pencils, cfg, seed=0, mode=mode)
+    times, flops = [], 0.0
+    for _ in range(steps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res = solve_sequence(pencils, cfg, seed=0, mode=mode)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+        flops = sum(r.report.filter_flops for r in res)
+        del res
+    return statistics.median(times), flops
+
+
+def scale_base(dev, steps=2, warmup=1):
+    """The single-GPU C3 sequence (the config the sharded N>1 lines run):
+    the base a strong-scaling efficiency is computed against."""
+    import paper_1206_3768_b200 as pkg
+    from paper_1206_3768_b200.harness import default_config
+    from paper_1206_3768_b200.sequence import iter_baseline_sequence
+
+    cfg_b = pkg.BASELINE_CONFIGS["C3"]
+    pencils = [pkg.EigenPencil(a=a, b=b, label=lab)
+               for lab, a, b in iter_baseline_sequence(cfg_b.n, cfg_b.length, seed=0, device=dev)]
+    t, flops = time_sequence(pencils, default_config(cfg_b), steps, warmup)
+    return {"config": "C3", "n_gpus": 1, "value": flops / t / 1e9, "unit": "GFLOP/s",
+            "ms_per_step": t * 1e3, "steps": steps, "warmup": warmup,
+            "note": "single-GPU C3 sequence (device generator), the base of the row-sharded N>1 lines"}
+
 def run_ours(args):
     import torch
 
@@ -398,10 +451,17 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sample = seq[: args.cpu_sample]
         f, wall, _ = cpu_sample(sample, cfg_b)
+        # the GPU on exactly the CPU sample's problems (like-for-like ratio)
+        t_s, f_s = time_sequence(dev_pencils[: len(sample)], cfg, steps=5, warmup=1, mode=args.mode)
         cpu = {"value": f / wall / 1e9, "unit": "GFLOP/s", "cores": os.cpu_count(),
                "kind": "port",
                "sample": f"{args.config} problems 1-{len(sample)} chained (1 cold + "
-                         f"{len(sample) - 1} warm), numpy oracle port, {wall:.1f} s"}
+                         f"{len(sample) - 1} warm), numpy oracle port, {wall:.1f} s",
+               "gpu_same_sample": {"value": f_s / t_s / 1e9, "unit": "GFLOP/s",
+                                   "ms": t_s * 1e3, "ratio_vs_cpu": (f_s / t_s) / (f / wall)}}
+    base = None
+    if rank == 0 and world == 1 and not args.no_scale_base and args.config == "C2":
+        base = scale_base(dev)
 
     if rank != 0:
         if dist is not None:
@@ -448,6 +508,11 @@ def run_ours(args):
         "step_ms": step_ms,
         "step_problem_ms": step_detail,
         "filter_kernel_gflops": achieved * 1e3,
+        # K1's executed work over the same time-to-solution: the H*P reuse
+        # skips one K1 product per pass after the first (`value` keeps the
+        # algorithmic deg-per-pass count), and 3M executes 6 of the 8 flops
+        "value_k1_executed_gflops": replicas * f_flops / t_dev / 1e9,
+        "value_fp64_executed_gflops": replicas * f_flops * (2 * product) / 8 / t_dev / 1e9,
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
@@ -461,6 +526,7 @@ def run_ours(args):
                      "executed_frac": achieved * (2 * product) / 8 / peak},
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "strong_scaling_base": base,
         "clocks": clk,
         "per_problem": per_problem,
     }

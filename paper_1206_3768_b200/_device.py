@@ -97,9 +97,11 @@ def to_device_matrix(x):
 
 
 class Operator:
-    """The Hermitian operator H as the kernels read it (pointer, ld, conj)."""
+    """The Hermitian operator H as the kernels read it (pointer, ld, conj).
+    ``row0``: global index of the first row the storage holds (0 for a full
+    H; `distributed.RowOperator` holds one rank's row block)."""
 
-    __slots__ = ("tensor", "n", "ld", "conj")
+    __slots__ = ("tensor", "n", "ld", "conj", "row0", "rows")
 
     def __init__(self, h):
         t = to_device_matrix(h)
@@ -114,6 +116,16 @@ class Operator:
             t = t.contiguous()
             conj, ld = 0, max(n, 1)
         self.tensor, self.n, self.ld, self.conj = t, n, ld, conj
+        self.row0, self.rows = 0, n
+
+    def row_ptr(self, r0, rows):
+        """Device address of rows [r0, r0+rows) as K1 reads them (row-major
+        stride ld; for column-major storage the conj flag makes column r
+        read as row r)."""
+        if r0 < self.row0 or r0 + rows > self.row0 + self.rows:
+            raise ValueError(f"rows [{r0}, {r0 + rows}) are not held by this operator "
+                             f"([{self.row0}, {self.row0 + self.rows}))")
+        return self.tensor.data_ptr() + (r0 - self.row0) * self.ld * 16
 
     @classmethod
     def wrap(cls, h):

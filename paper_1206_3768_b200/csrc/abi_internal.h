@@ -31,6 +31,7 @@ struct chfsi_ctx {
   bool qr_linear2 = true;  // Cholesky-QR2: linearised second pass when |Q1^H Q1 - I| <= 1e-8
   int lanczos_mode = 0;  // 0: cooperative single kernel; 1: one launch per operation
   unsigned step_epoch = 0;
+  unsigned step_tickets = 0;
   cudaEvent_t loop_ev[8] = {};  // chfsi_solve_loop_z phase timers (two sets, alternating passes)
   // second filter stream (two column halves of the filter run concurrently,
   // one CTA per SM each) with its own stream-K scratch
@@ -38,6 +39,7 @@ struct chfsi_ctx {
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   chfsi::StepWorkspace step_ws2{nullptr, nullptr, nullptr, 0};
   unsigned step_epoch2 = 0;
+  unsigned step_tickets2 = 0;
   int filter_chains = 2;  // 1: one launch chain per filter (chfsi_ctx_set_filter_chains)
   void* pinned = nullptr;  // page-locked host staging for small readbacks (grown on demand)
   size_t pinned_bytes = 0;

@@ -244,6 +244,9 @@ cudaError_t cheb_step_rows_launch(const double2* h, long long ldh, bool conj_h, 
   p.partials = ws.partials;
   p.flags = ws.flags;
   p.epoch = ++*ws.epoch;
+  p.ticket = ws.flags + ws.max_grid;  // every CTA of this launch takes one ticket
+  p.ticket_base = *ws.tickets;
+  *ws.tickets += (unsigned)grid;
   void* args[] = {&tmA, &tmB, &p};
   note_launch();
   // Programmatic dependent launch between consecutive steps of one filter

@@ -75,6 +75,8 @@ struct StepParams {
   double* partials;    // [grid][ACC][THREADS]
   unsigned* flags;     // [grid]
   unsigned epoch;
+  unsigned* ticket;    // CTA ticket counter (logical CTA id = ticket - ticket_base)
+  unsigned ticket_base;
   int dbg;             // diagnostics (CHFSI_K1_DEBUG): 2 = whole tiles only, 8 = trace, 16 = reversed
   unsigned long long* trace;  // dbg & 8: per CTA [start, owner wait begin, wait end, end, smid]
   // fused all-gather (multi-GPU row shards): every Ynext element is also
@@ -231,7 +233,21 @@ __global__ void __launch_bounds__(GROUPS* WM* WN * 32, MINB)
     else asm volatile("bar.sync 2, %0;\n" ::"n"(THREADS) : "memory");
   };
   const int G = gridDim.x;
-  const int cta = (p.dbg & 16) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x;  // 16: reversed (diagnostic)
+  // Logical CTA id = dispatch order: thread 0 takes a ticket from a counter
+  // (p.ticket_base = the tickets of all earlier launches on this workspace).
+  // A stream-K owner waits only for LOWER logical ids, i.e. for CTAs that
+  // were dispatched before it and so are resident or done — and every CTA
+  // publishes its partial tile before it could wait on anything. The wait
+  // is therefore deadlock-free whatever order the hardware dispatches
+  // blockIdx in and whatever other grids share the SMs (the two-chain
+  // filter, side-stream reductions); with blockIdx the same proof would
+  // rest on in-order dispatch. Fold order is by logical id: still fixed, so
+  // every launch stays bitwise reproducible. (Under PDL all CTAs of the
+  // previous launch took their tickets before this grid could start.)
+  __shared__ int s_cta;
+  if (threadIdx.x == 0) s_cta = (int)(atomicAdd(p.ticket, 1u) - p.ticket_base);
+  __syncthreads();
+  const int cta = (p.dbg & 16) ? G - 1 - s_cta : s_cta;  // 16: reversed (diagnostic)
   const int kiters = p.kiters;
 
   // ---- this CTA's slice of the linearised iteration space (64-bit once)

@@ -115,9 +115,10 @@ int chfsi_ctx_create(int device, chfsi_ctx** out) {
   ctx->step_ws.max_grid = chfsi::kNumSMs * 4;
   CK_CUDA(cudaMalloc(&ctx->step_ws.partials,
                      chfsi::step_workspace_doubles(ctx->step_ws.max_grid) * sizeof(double)));
-  CK_CUDA(cudaMalloc(&ctx->step_ws.flags, ctx->step_ws.max_grid * sizeof(unsigned)));
-  CK_CUDA(cudaMemset(ctx->step_ws.flags, 0, ctx->step_ws.max_grid * sizeof(unsigned)));
+  CK_CUDA(cudaMalloc(&ctx->step_ws.flags, (ctx->step_ws.max_grid + 1) * sizeof(unsigned)));
+  CK_CUDA(cudaMemset(ctx->step_ws.flags, 0, (ctx->step_ws.max_grid + 1) * sizeof(unsigned)));
   ctx->step_ws.epoch = &ctx->step_epoch;
+  ctx->step_ws.tickets = &ctx->step_tickets;
   *out = ctx;
   return CHFSI_OK;
 }
@@ -408,9 +409,10 @@ int ensure_aux_stream(chfsi_ctx* ctx) {
   ctx->step_ws2.max_grid = ctx->step_ws.max_grid;
   CK_CUDA(cudaMalloc(&ctx->step_ws2.partials,
                      chfsi::step_workspace_doubles(ctx->step_ws2.max_grid) * sizeof(double)));
-  CK_CUDA(cudaMalloc(&ctx->step_ws2.flags, ctx->step_ws2.max_grid * sizeof(unsigned)));
-  CK_CUDA(cudaMemset(ctx->step_ws2.flags, 0, ctx->step_ws2.max_grid * sizeof(unsigned)));
+  CK_CUDA(cudaMalloc(&ctx->step_ws2.flags, (ctx->step_ws2.max_grid + 1) * sizeof(unsigned)));
+  CK_CUDA(cudaMemset(ctx->step_ws2.flags, 0, (ctx->step_ws2.max_grid + 1) * sizeof(unsigned)));
   ctx->step_ws2.epoch = &ctx->step_epoch2;
+  ctx->step_ws2.tickets = &ctx->step_tickets2;
   return CHFSI_OK;
 }
 

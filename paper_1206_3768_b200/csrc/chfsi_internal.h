@@ -20,11 +20,13 @@ struct StepTiling {
   int warps = 0;   // warps per tile group: 0 = the registry's default for (bm, bn, groups)
 };
 
-// Stream-K scratch owned by the context: partial tiles + ready flags.
+// Stream-K scratch owned by the context: partial tiles + ready flags, and
+// the CTA ticket counter at flags[max_grid] (logical CTA ids in dispatch order).
 struct StepWorkspace {
   double* partials;
-  unsigned* flags;
-  unsigned* epoch;  // host-side launch counter (flag generation)
+  unsigned* flags;    // [max_grid + 1]
+  unsigned* epoch;    // host-side launch counter (flag generation)
+  unsigned* tickets;  // host-side mirror of the device ticket counter
   int max_grid;
 };
 

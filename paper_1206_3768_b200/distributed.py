@@ -32,9 +32,11 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+from ._device import Operator
 from ._lib import check, ctx, dptr, filter_coeffs, lib
 
-__all__ = ["RowPartition", "RowShardedFilter", "gpu_row_step"]
+__all__ = ["RowPartition", "RowShardedFilter", "RowComm", "RowOperator", "gpu_row_step",
+           "to_standard_rows", "back_transform_rows"]
 
 BK = 16  # K1 slab: blocked rows per rank are a multiple of it
 
@@ -87,7 +89,7 @@ def gpu_row_step(op, part, ycur_blk, yprev_slab, ynext_slab, w, alpha, c, beta, 
         return
     import ctypes
 
-    h_rows = op.tensor.data_ptr() + part.r0 * op.ld * 16
+    h_rows = op.row_ptr(part.r0, part.rows)
     ycur_rows = ycur_blk[part.rank]
     args = (ctx(), part.n, part.rows, w, ctypes_ptr(h_rows), op.ld, op.conj, dptr(ycur_blk), 0,
             part.kblk, part.world, dptr(ycur_rows), part.kblk,
@@ -330,6 +332,23 @@ class RowComm:
         if self.part.world > 1:
             dist.all_reduce(t, group=self.group)
 
+    def alltoall_blocks(self, send):
+        """send [world][...] -> recv with recv[q] = rank q's send[this rank]."""
+        if self.part.world == 1:
+            return send.clone()
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv.view(-1), send.view(-1), group=self.group)
+        return recv
+
+    def allgather_blocks(self, mine):
+        """[...] on every rank -> [world][...] (rank q's tensor at index q)."""
+        if self.part.world == 1:
+            return mine.unsqueeze(0).clone()
+        out = torch.empty((self.part.world,) + tuple(mine.shape), dtype=mine.dtype,
+                          device=mine.device)
+        dist.all_gather_into_tensor(out.view(-1), mine.contiguous().view(-1), group=self.group)
+        return out
+
     def gather_blocked(self, local, blocked):
         """Local rows (nl x w F-block) -> full rank-blocked buffer on every rank."""
         part = self.part
@@ -419,7 +438,7 @@ def lanczos_rows(comm, op, k, q0):
     alphas, betas = np.zeros(k), np.zeros(k)
     beta_last, steps = ctypes.c_double(), ctypes.c_int()
     pd = ctypes.POINTER(ctypes.c_double)
-    h_rows = ctypes.c_void_p(op.tensor.data_ptr() + part.r0 * op.ld * 16)
+    h_rows = ctypes.c_void_p(op.row_ptr(part.r0, nl) if nl else op.tensor.data_ptr())
     status = lib().chfsi_lanczos_rows_z(ctx(), n, k, h_rows, op.ld, op.conj, part.r0, nl,
                                         dptr(q0d), dptr(basis), dptr(ws), cb_ar, cb_g, None,
                                         alphas.ctypes.data_as(pd), betas.ctypes.data_as(pd),
@@ -428,3 +447,136 @@ def lanczos_rows(comm, op, k, q0):
         raise err[0]
     check(status, "lanczos (row-sharded)")
     return alphas, betas, beta_last.value, steps.value
+
+
+# ----------------------------------------------- row-sharded reduction ---
+
+class RowOperator(Operator):
+    """One rank's row block of the Hermitian operator H = L^-1 A L^-H:
+    rows [row0, row0 + rows) stored as the COLUMN block H[:, row0:row0+rows]
+    (column-major, ld n) — by Hermitian symmetry column r read with the
+    conj flag is row r, so K1 and the row-sharded Lanczos read their rows in
+    place (`Operator.row_ptr`). No rank holds the rest of H."""
+
+    __slots__ = ()
+
+    def __init__(self, block, n, row0):  # noqa: super().__init__ would want a square matrix
+        if block.dim() != 2 or block.shape[0] != n or (block.shape[1] > 1 and block.stride(0) != 1):
+            raise ValueError("row block must be a column-major n x rows tensor")
+        self.tensor, self.n, self.row0, self.rows = block, n, row0, block.shape[1]
+        self.ld = max(int(block.stride(1)), n) if self.rows > 1 else n
+        self.conj = 1
+
+
+class DeviceLinalg:
+    """Local dense kernels of the sharded reduction: cuSOLVER potrf and
+    cuBLAS ZTRSM through libchfsi (tests inject a host restatement)."""
+
+    @staticmethod
+    def potrf(b):
+        """Lower Cholesky factor (column-major device block, upper zeroed) of
+        the Hermitian ``b``; NotPositiveDefiniteError when b is not HPD."""
+        import ctypes
+
+        from ._device import to_fblock
+
+        l = to_fblock(b, copy=True)
+        info = ctypes.c_int()
+        check(lib().chfsi_potrf_z(ctx(), l.shape[0], dptr(l), l.stride(1), ctypes.byref(info)),
+              "cholesky (sharded reduction)")
+        return l
+
+    @staticmethod
+    def trsm(l, x, conj_transpose=False):
+        """x <- L^-1 x (or L^-H x) in place, x a column-major n x k block."""
+        check(lib().chfsi_trsm_z(ctx(), b"L", b"C" if conj_transpose else b"N", x.shape[0],
+                                 x.shape[1], dptr(l), l.stride(1), dptr(x), max(x.stride(1),
+                                                                                 x.shape[0])),
+              "triangular solve (sharded reduction)")
+        return x
+
+
+def _fcols(n, k, like):
+    return torch.empty((k, n), dtype=torch.complex128, device=like.device).t()
+
+
+def _block_transpose(comm, cols):
+    """T = (H[cols_p, :])^H from the column blocks H[:, cols_q] of all ranks:
+    rank q sends the rows cols_p of its block to rank p (one all-to-all of
+    kblk x kblk tiles); T[cols_q, :] = (block_q[cols_p, :])^H."""
+    part = comm.part
+    n, kb, P = part.n, part.kblk, part.world
+    send = torch.zeros((P, kb, kb), dtype=torch.complex128, device=cols.device)
+    for q in range(P):
+        q0, qr = part.block_range(q)
+        if qr and part.rows:  # rows of destination q's column range, this rank's columns
+            send[q, :part.rows, :qr] = cols[q0:q0 + qr, :].t()  # [my col][their row]
+    recv = comm.alltoall_blocks(send)  # recv[q][q's col][my row] = H[my rows, q's cols]^T
+    out = _fcols(n, part.rows, cols)
+    for q in range(P):
+        q0, qr = part.block_range(q)
+        if qr and part.rows:
+            # (H[cols_p, cols_q])^H as a column-major (qr x rows) block: element
+            # [i, j] = conj(H[p0 + j, q0 + i]) = conj(recv[q][i, j])
+            out[q0:q0 + qr, :] = recv[q, :qr, :part.rows].conj()
+    return out
+
+
+def to_standard_rows(a, b, comm, linalg=DeviceLinalg):
+    """Row-sharded reduction to standard form (reference reduction.py:102-113
+    split over the ranks of ``comm``): every rank gets ITS row block of
+    H = L^-1 A L^-H (as a RowOperator) and the Cholesky factor L.
+
+    * L = chol(B) on every rank (n^3/3 complex MACs, replicated: the
+      factor is needed whole by both solves and the back-transform);
+    * Z_p = L^-1 A[:, cols_p] — this rank's column block (TRSM, n^2 kblk);
+    * W_p = (Z[cols_p, :])^H by one all-to-all of kblk x kblk tiles;
+    * H[:, cols_p] = L^-1 W_p (TRSM), since H = L^-1 Z^H;
+    * symmetrised (h + h^H)/2 as the reference does, the transpose part
+      through a second all-to-all.
+    The O(n^3) triangular solves are split P ways; no rank ever holds the
+    rest of H. ``a``/``b``: full Hermitian matrices (numpy or torch, any
+    layout) on every rank."""
+    from ._device import to_device_matrix
+
+    part = comm.part
+    n = part.n
+    dev_b = to_device_matrix(b) if linalg is DeviceLinalg else b
+    l = linalg.potrf(dev_b)
+    a_d = to_device_matrix(a) if linalg is DeviceLinalg else a
+    r0, rows = part.r0, part.rows
+    z = _fcols(n, rows, l)
+    if rows:
+        z.copy_(a_d[:, r0:r0 + rows])
+        linalg.trsm(l, z)
+    w = _block_transpose(comm, z)  # (Z[cols_p, :])^H
+    del z
+    if rows:
+        linalg.trsm(l, w)  # H[:, cols_p]
+    t = _block_transpose(comm, w)  # (H[cols_p, :])^H
+    w.add_(t).mul_(0.5)
+    return RowOperator(w, n, r0), l
+
+
+def back_transform_rows(l, y, comm, linalg=DeviceLinalg):
+    """x = L^-H y (reduction.py:122-134) with the columns of the full
+    standard-form block ``y`` (n x k, the same on every rank) split over
+    the ranks; every rank returns the full x."""
+    part = comm.part
+    n, k = y.shape
+    P = part.world
+    cb = -(-k // P) if k else 0
+    c0, c1 = min(k, part.rank * cb), min(k, (part.rank + 1) * cb)
+    mine = torch.zeros((cb, n), dtype=torch.complex128, device=y.device)  # [col][row]
+    if c1 > c0:
+        blk = _fcols(n, c1 - c0, y)
+        blk.copy_(y[:, c0:c1])
+        linalg.trsm(l, blk, conj_transpose=True)
+        mine[: c1 - c0].copy_(blk.t())
+    every = comm.allgather_blocks(mine)  # [P][cb][n]
+    out = torch.empty((k, n), dtype=torch.complex128, device=y.device)
+    for q in range(P):
+        q0, q1 = min(k, q * cb), min(k, (q + 1) * cb)
+        if q1 > q0:
+            out[q0:q1].copy_(every[q, : q1 - q0])
+    return out.t()

@@ -135,7 +135,36 @@ def side_worker(device):
     return w
 
 
-def _stage(item, side, ready=None):
+class _StagingSlots:
+    """Two preallocated (H, L) buffer pairs that stage_standard writes into
+    in turn (n > _BACK_SIDE_MAX_N). Problem l+2 reuses problem l's pair: its
+    staging is issued after problem l's solve and back-transform finished
+    (the main-stream synchronisation at the end of every problem), so at
+    most two H/L pairs ever exist and no n x n block goes through the
+    caching allocator per problem — at C5 each pair is 12.8 GB, and
+    per-stream allocator pools otherwise left freed pairs unusable by the
+    next staging (OOM with the default bench warm-ups)."""
+
+    def __init__(self, n, device):
+        self.pairs = [(torch.empty((n, n), dtype=torch.complex128, device=device),
+                       torch.empty((n, n), dtype=torch.complex128, device=device))
+                      for _ in range(2)]
+        self.k = 0
+
+    def take(self, side):
+        pair = self.pairs[self.k]
+        self.k ^= 1
+        for t in pair:
+            t.record_stream(side)
+        return pair
+
+
+def _item_n(item):
+    a = item.a if isinstance(item, EigenPencil) else item[1]
+    return int(a.shape[0])
+
+
+def _stage(item, side, ready=None, slot=None):
     """Upload, validate and reduce one pencil on the side stream without any
     host synchronisation (the validation results land in page-locked memory
     and are checked when the problem is about to be solved, raising the
@@ -154,10 +183,11 @@ def _stage(item, side, ready=None):
             if isinstance(t, torch.Tensor) and t.is_cuda:
                 t.record_stream(side)
         if isinstance(item, EigenPencil):  # validated at construction
-            pencil, sp, checks = stage_standard(item.a, item.b, item.label, check_hermitian=False)
+            pencil, sp, checks = stage_standard(item.a, item.b, item.label, check_hermitian=False,
+                                                out=slot)
         else:
             label, a, b = item
-            pencil, sp, checks = stage_standard(a, b, label)
+            pencil, sp, checks = stage_standard(a, b, label, out=slot)
         ev = torch.cuda.Event()
         ev.record(side)
     return pencil, sp, ev, checks
@@ -197,11 +227,24 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
     does not depend on the previous solve), hiding it behind the solver's
     latency-bound phases; the back-transform of problem l runs on the same
     side stream behind problem l+1's solve (``CHFSI_BACK_ON_SIDE=0`` keeps
-    it on the caller's stream). Results are identical either way. ``shard`` is
-    passed to chfsi_solve (row-sharded multi-GPU filter).
+    it on the caller's stream). Results are identical either way.
+
+    ``shard`` (multi-GPU, one process per GPU, every rank calling with the
+    same pencils): True, a process group or a `distributed.RowComm` runs
+    the row-sharded path — per problem the reduction leaves each rank only
+    its row block of H (`distributed.to_standard_rows`), the solve is
+    row-sharded (`chfsi_solve(shard=...)`) and the back-transform splits the
+    eigenvector columns over the ranks; every rank returns the full results
+    (chained mode; the harness protocol needs the dense spectrum of the
+    whole H and is not sharded).
     """
     if mode not in ("chained", "harness"):
         raise ValueError(f"unknown mode {mode!r}")
+    if shard is not None and shard is not False:
+        if mode != "chained":
+            raise NotImplementedError("the row-sharded sequence runs mode='chained' (the harness "
+                                      "protocol needs the dense eigendecomposition of the whole H)")
+        return _solve_sequence_sharded(pencils, cfg, seed, keep_standard, on_problem, shard)
     out = []
     guess = None
     main = torch.cuda.current_stream()
@@ -220,7 +263,14 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
 
     it = iter(pencils)
     first = next(it, None)
-    staged = _stage(first, side, produced()) if first is not None else None
+    slots = None
+    if first is not None and _item_n(first) > _BACK_SIDE_MAX_N:
+        slots = _StagingSlots(_item_n(first), torch.cuda.current_device())
+
+    def slot():
+        return None if slots is None else slots.take(side)
+
+    staged = _stage(first, side, produced(), slot()) if first is not None else None
     prefetch = None
     if staged is not None:
         _reserve_outputs(staged[0], cfg, pencils)
@@ -300,10 +350,12 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
             nxt = next(it, None)
             if nxt is None:
                 staged = None
+            elif slots is not None and _item_n(nxt) != slots.pairs[0][0].shape[0]:
+                raise ValueError("all pencils of a sequence must share one dimension")
             elif side is not main:
-                staged = submit(_stage, nxt, side, produced())
+                staged = submit(_stage, nxt, side, produced(), slot())
             else:
-                staged = _stage(nxt, side)
+                staged = _stage(nxt, side, None, slot())
             t_stage = time.perf_counter() - t1
             t1 = time.perf_counter()
             n = pencil.n
@@ -360,6 +412,59 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
     for res, fut in pending:
         settle(res, fut)  # re-raises a failed back-transform
     main.wait_stream(side)
+    return out
+
+
+def _row_comm(shard, n):
+    """A RowComm (or a stand-in with the same interface) for ``shard``."""
+    if hasattr(shard, "part") and hasattr(shard, "allreduce_"):
+        if shard.part.n != n:
+            raise ValueError(f"communicator is for n={shard.part.n}, the pencils have n={n}")
+        return shard
+    from .distributed import RowComm
+
+    group = shard if not isinstance(shard, (bool, int)) else None
+    chunks = shard if isinstance(shard, int) and not isinstance(shard, bool) else 2
+    return RowComm(n, group=group, chunks=chunks)
+
+
+def _solve_sequence_sharded(pencils, cfg, seed, keep_standard, on_problem, shard):
+    """solve_sequence over row-sharded operators (see its docstring), chained
+    warm starts. No side stream: the reduction's all-to-alls and the solve's
+    collectives stay in one stream order on every rank."""
+    from .distributed import back_transform_rows, to_standard_rows
+
+    out, guess, comm = [], None, None
+    for item in pencils:
+        pencil = _as_pencil(item)
+        n = pencil.n
+        if comm is None:
+            comm = _row_comm(shard, n)
+        elif comm.part.n != n:
+            raise ValueError("all pencils of a sequence must share one dimension")
+        blk = cfg.resolve(n)[0]
+        t0 = time.perf_counter()
+        op, l_factor = to_standard_rows(pencil.a, pencil.b, comm)
+        t1 = time.perf_counter()
+        rng = np.random.default_rng((seed, pencil.label, 0 if guess is None else 1))
+        sol, rep = chfsi_solve(op, cfg, guess=guess, rng=rng, label=pencil.label, shard=comm)
+        t2 = time.perf_counter()
+        x = back_transform_rows(l_factor, sol.vectors, comm)
+        gsol = replace(sol, vectors=x, form="generalized")
+        torch.cuda.current_stream().synchronize()
+        t3 = time.perf_counter()
+        res = ProblemResult(label=pencil.label, values=sol.values, solution=gsol,
+                            standard_vectors=sol.vectors if keep_standard else None, report=rep,
+                            t_reduce=t1 - t0, t_solve=t2 - t1, t_back=t3 - t2)
+        if rep.tail_vectors is not None and rep.tail_vectors.shape[1] == blk and sol.nev:
+            guess = ChfsiGuess(vectors=rep.tail_vectors, lambda1=float(sol.values[0]),
+                               lambda_blk_plus_1=float(rep.lambda_blk_plus_1))
+        else:  # a partial solve leaves no full block: restart cold
+            guess = None
+        out.append(res)
+        if on_problem is not None:
+            on_problem(res)
+        del op, l_factor
     return out
 
 

@@ -11,6 +11,11 @@ all-gather are covered by tests/test_gpu_distributed.py). The result must
 equal the single-GPU solve: this checks the local-row bookkeeping of the
 native loop, the distributed CGS / Cholesky-QR2 / Rayleigh-Ritz with
 all-reduced partial products, locking, the tail and the gathers.
+
+The sequence tests run the production RowComm operators instead (only the
+NCCL calls replaced by the host hub): the row-sharded reduction (each rank
+holds only its row block of H, two all-to-alls), row K1 filter steps on
+the rank-blocked panel, the row Lanczos and the column-split back-transform.
 """
 
 import threading
@@ -149,7 +154,7 @@ def test_row_sharded_sequence_warm_starts_from_local_tails():
     world = 2
 
     def run(r, hub):
-        return pkg.solve_sequence(seq, cfg, seed=0, shard=ThreadComm(cfg_b.n, world, r, hub))
+        return pkg.solve_sequence(seq, cfg, seed=0, shard=_thread_row_comm(cfg_b.n, world, r, hub))
 
     outs = _run_ranks(world, run)
     for res in outs:
@@ -157,3 +162,102 @@ def test_row_sharded_sequence_warm_starts_from_local_tails():
             assert g.report.inner_loops == f.report.inner_loops
             assert np.abs(g.values - f.values).max() <= 1e-11 * np.abs(f.values).max()
             assert g.report.tail_vectors.shape[0] < cfg_b.n  # local rows only
+
+
+def _thread_row_comm(n, world, rank, hub):
+    """distributed.RowComm with host-mediated collectives among threads: the
+    production row-sharded operators (RowOperator, row K1 steps on rank-
+    blocked panels, row Lanczos) with the NCCL calls replaced by `hub`."""
+    from paper_1206_3768_b200.distributed import RowComm, RowPartition, RowShardedFilter
+
+    class ThreadRowComm(RowComm):
+        def __init__(self):
+            self.group, self.chunks, self._filters = None, 1, {}
+            self.part = RowPartition(n, world, rank)
+
+        def _sync(self):
+            torch.cuda.current_stream().synchronize()
+
+        def allreduce_(self, t):
+            self._sync()
+            t.copy_(hub.exchange(rank, t.detach().cpu(), reduce=True).to(t.device))
+
+        def alltoall_blocks(self, send):
+            self._sync()
+            every = hub.exchange(rank, send.detach().cpu())
+            return torch.stack([every[q][rank] for q in range(world)]).to(send.device)
+
+        def allgather_blocks(self, mine):
+            self._sync()
+            return torch.stack(hub.exchange(rank, mine.detach().cpu())).to(mine.device)
+
+        def _allgather_slabs(self, buf, async_op=False):
+            self._sync()
+            slabs = hub.exchange(rank, buf[rank].detach().cpu())
+            for q, sl in enumerate(slabs):
+                if q != rank:
+                    buf[q].copy_(sl.to(buf.device))
+            return None
+
+        def gather_blocked(self, local, blocked):
+            if self.part.rows:
+                blocked[rank, :, : self.part.rows].copy_(local.t())
+            self._allgather_slabs(blocked)
+            return blocked
+
+        def filter(self, op, blk):
+            key = (id(op.tensor), op.tensor.data_ptr(), blk)
+            f = self._filters.get(key)
+            if f is None:
+                f = RowShardedFilter(op, n, allgather=self._allgather_slabs, fused=False)
+                f.part = self.part
+                self._filters[key] = f
+            return f
+
+    return ThreadRowComm()
+
+
+@pytest.mark.parametrize("n,world,adaptive", [(512, 2, False), (333, 3, False), (400, 2, True)])
+def test_row_sharded_sequence_matches_single_gpu(n, world, adaptive):
+    """The sharded sequence driver (solve_sequence(shard=...)): per problem
+    the row-sharded reduction leaves each emulated rank only its row block of
+    H (two all-to-alls), the solve runs the row-sharded loop (row Lanczos,
+    row K1 filter steps on the rank-blocked panel, distributed QR / RR), and
+    the back-transform splits the columns — equal to the single-GPU
+    sequence: same loops and locking, eigenvalues to 1e-11, the standard and
+    generalized eigenspaces to 1e-9, identical bytes on every rank."""
+    import paper_1206_3768_b200 as pkg
+
+    nev, nex = 16, 16
+    cfg = pkg.ChfsiConfig(nev=nev, nex=nex, deg=10, adaptive_degree=adaptive)
+    seq = list(pkg.iter_baseline_sequence(n, 3, seed=1))
+    ref = pkg.solve_sequence(seq, cfg, seed=0, keep_standard=True)
+
+    def run(r, hub):
+        comm = _thread_row_comm(n, world, r, hub)
+        res = pkg.solve_sequence(seq, cfg, seed=0, keep_standard=True, shard=comm)
+        held = [comm.part.r0, comm.part.rows]
+        return res, held
+
+    outs = _run_ranks(world, run)
+    for res, held in outs:
+        for a, b in zip(ref, res):
+            assert b.report.converged
+            assert a.report.inner_loops == b.report.inner_loops
+            assert a.report.locked_per_loop == b.report.locked_per_loop
+            assert np.abs(a.values - b.values).max() <= 1e-11 * np.abs(a.values).max()
+            assert b.report.final_residuals.max() <= cfg.tol
+            assert subspace_sines(a.standard_vectors.cpu().numpy(),
+                                  b.standard_vectors.cpu().numpy()).max() <= 1e-9
+            xa, xb = a.solution.vectors.cpu().numpy(), b.solution.vectors.cpu().numpy()
+            assert b.solution.form == "generalized" and xb.shape == xa.shape
+            # B-orthonormal generalized vectors: compare spans through B
+            qa, _ = np.linalg.qr(xa)
+            qb, _ = np.linalg.qr(xb)
+            assert subspace_sines(qa, qb).max() <= 1e-9
+    covered = sorted(tuple(h) for _, h in outs)
+    assert sum(r for _, r in covered) == n
+    for res, _ in outs[1:]:
+        for a, b in zip(outs[0][0], res):
+            assert np.array_equal(a.values, b.values)
+            assert torch.equal(a.solution.vectors, b.solution.vectors)

@@ -374,6 +374,39 @@ def test_sequence_side_worker_matches_inline_and_serial(pkg, monkeypatch):
 
 
 @pytest.mark.gpu
+def test_sequence_staging_slots_match_allocated_staging(pkg, monkeypatch):
+    """Large-n mode (n > 8192 by default): the driver stages every problem
+    into two preallocated H/L pairs used in turn (problem l+2 reuses l's)
+    instead of allocating; forced here at C1 size, with and without the
+    side stream, the sequence is bitwise the same as with fresh buffers."""
+    from paper_1206_3768_b200 import harness
+
+    cfg_b = pkg.BASELINE_CONFIGS["C1"]
+    cfg = pkg.ChfsiConfig(nev=cfg_b.nev, nex=cfg_b.nex, deg=cfg_b.deg, tol=cfg_b.tol)
+    seq = list(pkg.iter_baseline_sequence(cfg_b.n, 5, seed=0))
+    fresh = pkg.solve_sequence(seq, cfg, seed=0)
+    monkeypatch.setattr(harness, "_BACK_SIDE_MAX_N", 256)
+    taken = []
+    orig = harness._StagingSlots.take
+
+    def take(self, side):
+        pair = orig(self, side)
+        taken.append(pair[0].data_ptr())
+        return pair
+
+    monkeypatch.setattr(harness._StagingSlots, "take", take)
+    for overlap in (True, False):
+        taken.clear()
+        slotted = pkg.solve_sequence(seq, cfg, seed=0, overlap=overlap)
+        assert len(taken) == len(seq) and len(set(taken)) == 2
+        assert taken[0] == taken[2] == taken[4] != taken[1] == taken[3]
+        for a, b in zip(fresh, slotted):
+            assert a.report.locked_per_loop == b.report.locked_per_loop
+            assert np.array_equal(a.values, b.values)
+            assert torch.equal(a.solution.vectors, b.solution.vectors)
+
+
+@pytest.mark.gpu
 def test_sequence_driver_releases_its_operators(pkg):
     """Nothing of a finished sequence call stays on the device once its
     results are dropped (the worker's completed futures must not keep the
