@@ -403,7 +403,11 @@ int filter_range(chfsi_ctx* ctx, cudaStream_t stream, const chfsi::StepWorkspace
 
 int ensure_aux_stream(chfsi_ctx* ctx) {
   if (ctx->aux_stream) return CHFSI_OK;
-  CK_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
+  // the second filter chain runs at the priority of the context's stream
+  // (a high-priority solver stream must not lose half its filter to it)
+  int prio = 0;
+  CK_CUDA(cudaStreamGetPriority(ctx->stream, &prio));
+  CK_CUDA(cudaStreamCreateWithPriority(&ctx->aux_stream, cudaStreamNonBlocking, prio));
   CK_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
   CK_CUDA(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
   ctx->step_ws2.max_grid = ctx->step_ws.max_grid;

@@ -245,6 +245,42 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
             raise NotImplementedError("the row-sharded sequence runs mode='chained' (the harness "
                                       "protocol needs the dense eigendecomposition of the whole H)")
         return _solve_sequence_sharded(pencils, cfg, seed, keep_standard, on_problem, shard)
+    caller = torch.cuda.current_stream()
+    solver = solver_stream() if overlap and _PRIORITY else caller
+    if solver is caller:
+        return _solve_sequence_on(pencils, cfg, seed, mode, keep_standard, on_problem, overlap)
+    # The solver's own work runs on a HIGH-priority stream: the block
+    # scheduler then places its CTAs first whenever SMs free up, so the
+    # side stream's reduction of problem l+1 fills the solver's latency gaps
+    # instead of holding SMs that the solver's short, serial kernels
+    # (potrf, TRSM, the w x w eigensolver) are waiting for.
+    solver.wait_stream(caller)
+    with torch.cuda.stream(solver):
+        out = _solve_sequence_on(pencils, cfg, seed, mode, keep_standard, on_problem, overlap)
+    caller.wait_stream(solver)
+    for r in out:  # results were allocated on the solver stream, used on the caller's
+        for t in (r.solution.vectors if r.solution is not None else None, r.standard_vectors,
+                  r.report.tail_vectors):
+            if isinstance(t, torch.Tensor) and t.is_cuda:
+                t.record_stream(caller)
+    return out
+
+
+_PRIORITY = os.environ.get("CHFSI_STREAM_PRIORITY", "1") != "0"
+_SOLVER_STREAMS = {}
+
+
+def solver_stream(device=None):
+    """One persistent highest-priority stream per device for the solver."""
+    dev = torch.cuda.current_device() if device is None else device
+    st = _SOLVER_STREAMS.get(dev)
+    if st is None:
+        st = _SOLVER_STREAMS[dev] = torch.cuda.Stream(device=dev, priority=-100)
+    return st
+
+
+def _solve_sequence_on(pencils, cfg, seed, mode, keep_standard, on_problem, overlap):
+    """solve_sequence's single-GPU body on the current stream."""
     out = []
     guess = None
     main = torch.cuda.current_stream()
@@ -366,8 +402,7 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
             rng = np.random.default_rng((seed, pencil.label, start))
             if prefetch is not None:  # (always problem 1: guess is None there)
                 rng, prefetch = prefetch, None
-            sol, rep = chfsi_solve(sp.h, cfg, guess=guess, rng=rng, label=pencil.label,
-                                   shard=shard)
+            sol, rep = chfsi_solve(sp.h, cfg, guess=guess, rng=rng, label=pencil.label)
             t2 = time.perf_counter()
             back = None
             # at large n the side-stream back-transform would keep L of problem

@@ -26,6 +26,7 @@ ap.add_argument("--config", default="C2")
 ap.add_argument("--top", type=int, default=40)
 ap.add_argument("--problems", type=int, default=None)
 ap.add_argument("--json", default=None)
+ap.add_argument("--by-stream", action="store_true", help="one row per (kernel, stream)")
 a = ap.parse_args()
 
 cfg_b = pkg.BASELINE_CONFIGS[a.config]
@@ -48,7 +49,7 @@ for e in kern:
     name = e.name
     st = getattr(e, "device_resource_id", None)
     ivl = (e.time_range.start, e.time_range.end)
-    rec = by[name[:110]]
+    rec = by[(name[:100] + f"  @s{st}") if a.by_stream else name[:110]]
     rec[0] += 1
     rec[1] += ivl[1] - ivl[0]
     rec[2].add(st)
