@@ -149,6 +149,14 @@ CHFSI_API int chfsi_step_tiling(int n, int w, int* bm, int* bn, int* split);
  * or CHFSI_EINVAL; product = 0 only queries. */
 CHFSI_API int chfsi_set_complex_product(int product);
 
+/* K-slab depth of the 3M K1 kernels in 128-byte halves (process-wide):
+ * 2 = 16 complex per TMA stage, 4 = 32 complex (default unless
+ * CHFSI_K1_NH=2; half the stage barriers per MMA, same shared memory with half the
+ * stages; tiles without a deep variant keep 16). Same arithmetic and
+ * summation order either way. Returns the previous setting, or CHFSI_EINVAL;
+ * halves = 0 only queries. No reference counterpart (tuning knob). */
+CHFSI_API int chfsi_set_k1_slab(int halves);
+
 /* ---------------------------------------------------------------- K2 ---
  * k-step Lanczos with full reorthogonalization (chfsi.py:125-162): q0 is
  * the raw start vector (normalised on device), basis an n x k column-major

@@ -560,7 +560,7 @@ def _safe_window(scale_ref, a, b):
 
 # ----------------------------------------------------------------- solver ---
 
-def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
+def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None, _hooks=None, _sync=True):
     """Compute the ``cfg.nev`` lowest eigenpairs of the Hermitian ``h``
     (chfsi.py:274-384). ``h`` may be a numpy array (uploaded once) or a CUDA
     tensor in either row- or column-major layout (used in place).
@@ -685,6 +685,8 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
         st.hp_fn = callbacks.hp_cb
         st.gather = callbacks.gather_cb
     hw["lanczos_start"] = time.perf_counter() - t0 - hw["setup"]
+    if _hooks is not None:  # (sequence driver: hand queued side-stream work to its worker)
+        _hooks()
     t_loop = time.perf_counter()
     status = lib().chfsi_solve_loop_z(ctx(), ctypes.byref(st))
     hw["loop"] = time.perf_counter() - t_loop
@@ -725,7 +727,8 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None):
     sol = EigenSolution(values=np.asarray(locked_vals)[order], vectors=vecs, form="standard",
                         label=label)
     report.final_residuals = np.asarray(locked_res)[order]
-    torch.cuda.current_stream().synchronize()
+    if _sync:
+        torch.cuda.current_stream().synchronize()
     report.t_lanczos = t_lz.seconds()
     report.t_filter = st.t_filter
     report.t_ortho = st.t_ortho

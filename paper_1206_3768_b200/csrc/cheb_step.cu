@@ -6,6 +6,7 @@ namespace chfsi {
 
 namespace k1 {
 const Variant* variant_3m(int bm, int bn, int groups, int warps, bool conj);  // cheb_step_3m.cu
+const Variant* variant_3m_deep(int bm, int bn, int groups, int warps, bool conj);
 }  // namespace k1
 
 namespace {
@@ -99,8 +100,24 @@ int g_product = [] {
   return (e && atoi(e) == 4) ? 4 : 3;
 }();
 
-const Variant* variant(int bm, int bn, int groups, int warps, bool conj, int product) {
+// k-slab depth preference of the 3M kernels: 2 (16 complex) or 4 (32
+// complex) 128-byte halves; CHFSI_K1_NH or chfsi_set_k1_slab(). Deep-slab
+// variants exist for the default 3M tiles; others keep 16-deep slabs.
+// Measured (profiles/r02n_k1_slab_depth.txt, TFLOP/s at 8 flops/CMAC, 16 vs
+// 32 deep): 2048x160 34.6 -> 35.9, 2048x100 27.8 -> 29.6, 2048x40 22.9 ->
+// 24.6, 5000x600 39.0 -> 39.6, 12000x1400 41.5 -> 42.1; C2 sequence
+// 306-311 -> 299 ms. Default 4 (CHFSI_K1_NH=2 restores 16-deep slabs).
+int g_nh = [] {
+  const char* e = getenv("CHFSI_K1_NH");
+  return (e && atoi(e) == 2) ? 2 : 4;
+}();
+
+const Variant* variant(int bm, int bn, int groups, int warps, bool conj, int product,
+                       bool allow_deep = true) {
   if (product == 0) product = g_product;
+  if (product == 3 && g_nh == 4 && allow_deep) {
+    if (const Variant* v = variant_3m_deep(bm, bn, groups, warps, conj)) return v;
+  }
   if (product == 3) {
     if (const Variant* v = variant_3m(bm, bn, groups, warps, conj)) return v;
   }
@@ -179,9 +196,11 @@ cudaError_t cheb_step_rows_launch(const double2* h, long long ldh, bool conj_h, 
   const int m = shard.rows;
   if (n <= 0 || w <= 0 || m <= 0) return cudaSuccess;
   if (tiling.bm == 0) tiling = choose_step_tiling(n, w);
+  // a rank-blocked operand needs whole slabs per rank block
+  const bool deep_ok = shard.kblk <= 0 || shard.kblk % 32 == 0;
   const Variant* vp =
       variant(tiling.bm, tiling.bn, tiling.groups ? tiling.groups : 1, tiling.warps, conj_h,
-              tiling.product);
+              tiling.product, deep_ok);
   if (vp == nullptr) return cudaErrorInvalidValue;
   const Variant& v = *vp;
   int grid = v.resident * kNumSMs;
@@ -192,7 +211,8 @@ cudaError_t cheb_step_rows_launch(const double2* h, long long ldh, bool conj_h, 
   // column-major (ld ldc) or rank-blocked (kblk rows per block, nblk blocks).
   alignas(64) CUtensorMap tmA, tmB;
   const bool blocked = shard.kblk > 0;
-  if (blocked && (shard.kblk % BK != 0 || (long long)shard.kblk * shard.nblk < n))
+  const int slab = 8 * v.nh;  // complex elements per k-slab
+  if (blocked && (shard.kblk % slab != 0 || (long long)shard.kblk * shard.nblk < n))
     return cudaErrorInvalidValue;
   if (!encode_map(&tmA, h, n, m, ldh, v.bm)) return cudaErrorInvalidValue;
   if (blocked ? !encode_map_blocked(&tmB, ycur, shard.kblk, w, shard.nblk, v.bn)
@@ -203,7 +223,7 @@ cudaError_t cheb_step_rows_launch(const double2* h, long long ldh, bool conj_h, 
   p.ycur = shard.ycur_rows ? shard.ycur_rows : ycur;
   p.ldc = shard.ycur_rows ? shard.ldcr : ldc;
   p.m = m;
-  p.kblk_slabs = blocked ? shard.kblk / BK : 0;
+  p.kblk_slabs = blocked ? shard.kblk / slab : 0;
   p.yprev = yprev ? yprev : ynext;
   p.ldp = yprev ? ldp : ldn;
   p.ynext = ynext;
@@ -215,7 +235,7 @@ cudaError_t cheb_step_rows_launch(const double2* h, long long ldh, bool conj_h, 
   p.tiles_n = (w + v.bn - 1) / v.bn;
   const int tiles_m = (m + v.bm - 1) / v.bm;
   const long long tiles = (long long)tiles_m * p.tiles_n;
-  p.kiters = blocked ? shard.nblk * (shard.kblk / BK) : (n + BK - 1) / BK;
+  p.kiters = blocked ? shard.nblk * (shard.kblk / slab) : (n + slab - 1) / slab;
   static const int dbg = [] {
     const char* e = getenv("CHFSI_K1_DEBUG");
     return e ? atoi(e) : 0;
@@ -279,5 +299,12 @@ int set_complex_product(int product) {
 }
 
 int complex_product() { return g_product; }
+
+int set_k1_slab(int nh) {
+  if (nh != 2 && nh != 4) return -1;
+  const int old = g_nh;
+  g_nh = nh;
+  return old;
+}
 
 }  // namespace chfsi

@@ -197,7 +197,11 @@ __device__ __forceinline__ void epilogue_store(const StepParams& p, int row, int
 // Ci = T3 - T1 -+ T2 (+ for conj(H)), so partial tiles, the fold and the
 // epilogue are the same as for the 4M product. Work per complex MAC: 6 real
 // flops executed (the 8-flop algorithmic count stays the metric).
-template <int BM, int BN, int WM, int WN, int STAGES, int MINB, bool CONJ, int GROUPS, bool GAUSS>
+//
+// NH: 128-byte halves per k-slab (2: 16 complex, 4: 32 complex) — a deeper
+// slab halves the per-slab barrier / proxy-fence / refill overhead per DMMA.
+template <int BM, int BN, int WM, int WN, int STAGES, int MINB, bool CONJ, int GROUPS, bool GAUSS,
+          int NH = 2>
 __global__ void __launch_bounds__(GROUPS* WM* WN * 32, MINB)
     cheb_step_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const StepParams p) {
@@ -209,7 +213,8 @@ __global__ void __launch_bounds__(GROUPS* WM* WN * 32, MINB)
   constexpr int ACC = MI * NI * 4;
   constexpr int A_BYTES = BM * HALF;  // one half-slab of A
   constexpr int B_BYTES = BN * HALF;
-  constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
+  constexpr int STAGE_BYTES = NH * (A_BYTES + B_BYTES);
+  static_assert(NH == 2 || NH == 4, "k-slab of 2 or 4 halves");
   static_assert(THREADS <= kMaxThreads && ACC * THREADS <= kSlotDoubles, "workspace bound");
   static_assert(MI >= 1 && NI >= 1, "warp tile too small");
   static_assert(A_BYTES % 1024 == 0 && B_BYTES % 1024 == 0, "128B swizzle needs 1024B-aligned boxes");
@@ -312,17 +317,19 @@ __global__ void __launch_bounds__(GROUPS* WM* WN * 32, MINB)
   // one elected thread: arm the stage's barrier and issue its four TMA boxes
   auto issue = [&](const Cursor& c, int stage) {
     const unsigned dst = smem0 + stage * STAGE_BYTES, bar = full0 + 8 * stage;
-    const int x = c.kk * (2 * BK);  // in doubles
+    const int x = c.kk * (NH * BK);  // in doubles
     mbar_expect_tx(bar, STAGE_BYTES);
-    tma_load_2d(dst, &tmA, bar, x, c.m0);
-    tma_load_2d(dst + A_BYTES, &tmA, bar, x + BK, c.m0);
+#pragma unroll
+    for (int hh = 0; hh < NH; ++hh) tma_load_2d(dst + hh * A_BYTES, &tmA, bar, x + hh * BK, c.m0);
     if (p.kblk_slabs > 0) {  // rank-blocked Y: block q holds rows [q*kblk, (q+1)*kblk)
-      const int q = c.kk / p.kblk_slabs, xl = (c.kk - q * p.kblk_slabs) * (2 * BK);
-      tma_load_3d(dst + 2 * A_BYTES, &tmB, bar, xl, c.n0, q);
-      tma_load_3d(dst + 2 * A_BYTES + B_BYTES, &tmB, bar, xl + BK, c.n0, q);
+      const int q = c.kk / p.kblk_slabs, xl = (c.kk - q * p.kblk_slabs) * (NH * BK);
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh)
+        tma_load_3d(dst + NH * A_BYTES + hh * B_BYTES, &tmB, bar, xl + hh * BK, c.n0, q);
     } else {
-      tma_load_2d(dst + 2 * A_BYTES, &tmB, bar, x, c.n0);
-      tma_load_2d(dst + 2 * A_BYTES + B_BYTES, &tmB, bar, x + BK, c.n0);
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh)
+        tma_load_2d(dst + NH * A_BYTES + hh * B_BYTES, &tmB, bar, x + hh * BK, c.n0);
     }
   };
 
@@ -390,7 +397,7 @@ __global__ void __launch_bounds__(GROUPS* WM* WN * 32, MINB)
   const int lo = (t ^ (g >> 1)) << 4;
   const int off_even = ((g & 1) << 6) | lo, off_odd = (((g & 1) ^ 1) << 6) | lo;
   const unsigned char* a_base = smem + (wm * TM + sg) * HALF;
-  const unsigned char* b_base = smem + 2 * A_BYTES + (wn * TN + sg) * HALF;
+  const unsigned char* b_base = smem + NH * A_BYTES + (wn * TN + sg) * HALF;
   // two groups: hand-over buffer for group 1's partial tile
   double* cbuf = reinterpret_cast<double*>(bars + 2 * STAGES);
 
@@ -407,7 +414,7 @@ __global__ void __launch_bounds__(GROUPS* WM* WN * 32, MINB)
       const unsigned char* sa = a_base + stage * STAGE_BYTES;
       const unsigned char* sbm = b_base + stage * STAGE_BYTES;
 #pragma unroll
-      for (int k4 = 0; k4 < BK / 4; ++k4) {
+      for (int k4 = 0; k4 < NH * 2; ++k4) {
         const int off = (k4 & 1) ? off_odd : off_even;
         const unsigned char* ah = sa + (k4 >> 1) * A_BYTES + off;
         const unsigned char* bh = sbm + (k4 >> 1) * B_BYTES + off;
@@ -585,20 +592,23 @@ __global__ void __launch_bounds__(GROUPS* WM* WN * 32, MINB)
 struct Variant {
   const void* fn;
   int bm, bn, groups, threads, smem;
+  int nh;        // 128-byte halves per k-slab: the slab is 8*nh complex deep
   int resident;  // CTAs per SM actually achievable
 };
 
-template <int BM, int BN, int WM, int WN, int STAGES, int MINB, bool CONJ, int GROUPS, bool GAUSS>
+template <int BM, int BN, int WM, int WN, int STAGES, int MINB, bool CONJ, int GROUPS, bool GAUSS,
+          int NH = 2>
 Variant make_variant() {
   Variant v{};
-  auto fn = cheb_step_kernel<BM, BN, WM, WN, STAGES, MINB, CONJ, GROUPS, GAUSS>;
+  auto fn = cheb_step_kernel<BM, BN, WM, WN, STAGES, MINB, CONJ, GROUPS, GAUSS, NH>;
+  v.nh = NH;
   v.fn = reinterpret_cast<const void*>(fn);
   v.bm = BM;
   v.bn = BN;
   v.groups = GROUPS;
   v.threads = GROUPS * WM * WN * 32;
   constexpr int ACC = (BM / WM / 8) * (BN / WN / 8) * 4;
-  v.smem = STAGES * 2 * (BM + BN) * HALF + 2 * STAGES * 8 + 1024 +
+  v.smem = STAGES * NH * (BM + BN) * HALF + 2 * STAGES * 8 + 1024 +
            (GROUPS == 2 ? ACC * WM * WN * 32 * 8 : 0);  // + group hand-over buffer
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem);
   int occ = 0;

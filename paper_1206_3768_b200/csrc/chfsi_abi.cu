@@ -529,6 +529,16 @@ int chfsi_set_complex_product(int product) {
   return chfsi::set_complex_product(product);
 }
 
+int chfsi_set_k1_slab(int halves) {
+  CK_ARG(halves == 0 || halves == 2 || halves == 4, "k-slab depth must be 2 or 4 halves");
+  if (halves == 0) {  // query
+    const int cur = chfsi::set_k1_slab(2);
+    chfsi::set_k1_slab(cur);
+    return cur;
+  }
+  return chfsi::set_k1_slab(halves);
+}
+
 // ------------------------------------------------------------------- K2 ---
 
 int chfsi_lanczos_z(chfsi_ctx* ctx, int n, int k, const void* H, long long ldh, int conj_h,

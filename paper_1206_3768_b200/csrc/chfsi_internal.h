@@ -34,6 +34,8 @@ StepTiling choose_step_tiling(int n, int w);
 // process-wide K1 complex-product default (3 or 4); returns the previous one, -1 if invalid
 int set_complex_product(int product);
 int complex_product();
+// K1 3M k-slab depth in 128-byte halves (2 or 4); returns the previous, -1 if invalid
+int set_k1_slab(int nh);
 size_t step_workspace_doubles(int max_grid);
 // CHFSI_K1_DEBUG & 8 diagnostics: copy the last K1 launch's per-CTA trace
 // ([start, wait begin, wait end, end] globaltimer ns, smid) to host.

@@ -38,7 +38,7 @@ from ._lib import check, ctx, dptr, filter_coeffs, lib
 __all__ = ["RowPartition", "RowShardedFilter", "RowComm", "RowOperator", "gpu_row_step",
            "to_standard_rows", "back_transform_rows"]
 
-BK = 16  # K1 slab: blocked rows per rank are a multiple of it
+BK = 32  # K1's deepest k-slab (32 complex): blocked rows per rank are a multiple of it
 
 
 class RowPartition:

@@ -90,3 +90,25 @@ print("solver phases (ms): " + ", ".join(f"{k} {v:.1f}" for k, v in phase.items(
 if a.json:
     json.dump({"kernels": [[n, c, u] for n, (c, u, _) in rows], "phases": dict(phase)},
               open(a.json, "w"), indent=1)
+
+# main-stream idle gaps attributed to (previous -> next) activity
+main_st = max(streams, key=lambda s: len(streams[s]))
+mk = sorted((e.time_range.start, e.time_range.end, e.name) for e in kern
+            if getattr(e, "device_resource_id", None) == main_st)
+gaps = collections.defaultdict(lambda: [0, 0.0])
+cur_e, prev = mk[0][1], mk[0][2]
+hist = collections.Counter()
+for s_, e_, name in mk[1:]:
+    g = s_ - cur_e
+    if g > 0:
+        key = (prev[:55], name[:55])
+        gaps[key][0] += 1
+        gaps[key][1] += g
+        hist[min(int(g // 10) * 10, 200)] += 1
+    cur_e = max(cur_e, e_)
+    prev = name
+tot_gap = sum(v[1] for v in gaps.values())
+print(f"\nmain stream {main_st}: {tot_gap / 1e3:.2f} ms idle in {sum(v[0] for v in gaps.values())} gaps; "
+      f"gap histogram (us bucket: count) {sorted(hist.items())}")
+for (p, n), (c, t) in sorted(gaps.items(), key=lambda kv: -kv[1][1])[: a.top]:
+    print(f"{t / 1e3:8.3f} ms {c:6d}x {t / c:7.1f} us  {p}  ->  {n}")
