@@ -135,6 +135,8 @@ def _harness_cells(pkg, name, length, device=False, kinds=("cold", "warm")):
                               lambda_blk_plus_1=float(dv[blk]))
         del sp, dvec
         torch.cuda.empty_cache()
+    if checked == 0:
+        pytest.skip(f"{name}_scale.npz holds no solved cells yet (generation in progress)")
     return checked, done
 
 
