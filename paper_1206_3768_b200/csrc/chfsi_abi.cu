@@ -894,6 +894,35 @@ int heev_near_diag(chfsi_ctx* ctx, int n, double2* a, long long lda, double* w, 
     return e ? atof(e) : 0.5;  // measured: 0.1 -> 0.5 turns 5 of the cold C2 start's 10 zheevd calls into fast ones
   }();
   constexpr int kSlots = 4 * (kMaxSteps + 1) + kMaxSteps;  // build stats + NS defects
+  // Panel widths: the whole iteration as one cooperative kernel (nd_persist.cu;
+  // CHFSI_ND_PERSIST=0 keeps the multi-kernel version below) — one host
+  // round trip per call instead of one per step, no per-step launches.
+  static const bool persist = [] {
+    const char* e = getenv("CHFSI_ND_PERSIST");
+    return !(e && atoi(e) == 0);
+  }();
+  if (persist && n <= chfsi::kNdPersistMaxN) {
+    const size_t pneed = chfsi::nd_persist_ws_bytes(n);
+    if (pneed > ctx->eig_ws_bytes) {
+      CK_CUDA(cudaStreamSynchronize(s));
+      if (ctx->eig_ws) CK_CUDA(cudaFree(ctx->eig_ws));
+      ctx->eig_ws = nullptr;
+      ctx->eig_ws_bytes = 0;
+      CK_CUDA(cudaMalloc(&ctx->eig_ws, pneed));
+      ctx->eig_ws_bytes = pneed;
+    }
+    CK(chfsi::ensure_pinned(ctx, 4 * sizeof(double)));
+    double* st_dev = ctx->scalars + 12;  // 4 doubles of the context's scalar scratch
+    CK_CUDA(chfsi::nd_persist_launch(a, lda, n, w, tol, bail, ctx->eig_ws, st_dev, s));
+    double* hs = static_cast<double*>(ctx->pinned);
+    CK_CUDA(cudaMemcpyAsync(hs, st_dev, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK_CUDA(cudaStreamSynchronize(s));
+    static const bool dbgp = getenv("CHFSI_RR_DEBUG") != nullptr;
+    if (dbgp)
+      fprintf(stderr, "ndp n=%d done=%g steps=%g rmax=%.3e emax=%.3e\n", n, hs[0], hs[1], hs[2], hs[3]);
+    *done = hs[0] == 1.0;
+    return CHFSI_OK;
+  }
   const size_t need = 5 * mat + kSlots * sizeof(double) + (size_t)n * sizeof(int) + 1024;
   if (need > ctx->eig_ws_bytes) {
     CK_CUDA(cudaStreamSynchronize(s));

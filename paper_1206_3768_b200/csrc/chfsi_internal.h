@@ -145,6 +145,11 @@ cudaError_t add_diag_shift_launch(double2* a, long long lda, int n, const double
 // acc[i] = (first ? 1 : acc[i]) * Re(R[i,i])
 cudaError_t diag_accumulate_launch(const double2* r, long long ldr, int n, double* acc, bool first,
                                    cudaStream_t s);
+// near-diagonal Hermitian eigensolver as one cooperative kernel (nd_persist.cu)
+constexpr int kNdPersistMaxN = 256;
+size_t nd_persist_ws_bytes(int n);
+cudaError_t nd_persist_launch(const double2* a, long long lda, int n, double* w, double tol,
+                              double bail, void* ws, double* status_dev, cudaStream_t s);
 // near-diagonal Hermitian eigensolver pieces (nd_eig.cu)
 cudaError_t nd_build_step_launch(const double2* g, long long ldg, int n, double2* x, long long ldx,
                                  double* stats, cudaStream_t s);

@@ -392,10 +392,13 @@ def test_hermitian_eig(pkg, n):
     assert np.abs(g @ v - v * vals).max() <= 1e-11 * max(1, n)
 
 
-@pytest.mark.parametrize("n,off", [(48, 1e-4), (160, 1e-6), (301, 1e-5), (160, 0.3)])
+@pytest.mark.parametrize("n,off", [(48, 1e-4), (160, 1e-6), (301, 1e-5), (160, 0.3), (37, 1e-5),
+                                   (123, 1e-4), (256, 1e-6), (2, 1e-6), (9, 1e-3)])
 def test_near_diagonal_eigensolver(pkg, n, off):
     """chfsi_heev_rr_z: near-diagonal G (the RR regime after the first loops)
-    goes through the Jacobi/ZGEMM path; a far-from-diagonal G must fall back
+    goes through the Jacobi/DMMA path (one cooperative kernel for n <= 256,
+    ragged n included; the multi-kernel ZGEMM version above); a
+    far-from-diagonal G must fall back
     to zheevd. Either way: ascending values and an orthonormal eigenbasis
     matching numpy to rounding."""
     from paper_1206_3768_b200._device import to_fblock, ld_of

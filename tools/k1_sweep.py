@@ -76,10 +76,12 @@ for n, w in shapes:
             _lib.check(_lib.lib().chfsi_ctx_set_tiling(_lib.ctx(), 0, 0, 0))
         else:
             # "64x32d": two 8-warp groups per CTA; "128x32w8": 8 warps per group
-            vv, _, wp = v.partition("w")
+            # "...g148": grid override (CTAs per launch)
+            v0, _, gr = v.partition("g")
+            vv, _, wp = v0.partition("w")
             dual = vv.endswith("d")
             bm, bn = (int(t) for t in vv.rstrip("d").split("x"))
-            _lib.check(_lib.lib().chfsi_ctx_set_tiling(_lib.ctx(), bm, bn, 0))
+            _lib.check(_lib.lib().chfsi_ctx_set_tiling(_lib.ctx(), bm, bn, int(gr) if gr else 0))
             if dual:
                 _lib.check(_lib.lib().chfsi_ctx_set_step_groups(_lib.ctx(), 2))
             _lib.check(_lib.lib().chfsi_ctx_set_step_warps(_lib.ctx(), int(wp) if wp else 0))
