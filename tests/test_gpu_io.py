@@ -35,3 +35,25 @@ def test_device_generator_feeds_the_solver():
     seq = list(pkg.iter_baseline_sequence(cfg_b.n, 2, seed=0, device="cuda:0"))
     res = pkg.solve_sequence(seq, pkg.ChfsiConfig(nev=cfg_b.nev, nex=cfg_b.nex, deg=cfg_b.deg))
     assert all(r.report.converged for r in res)
+
+
+def test_lazy_device_generator_feeds_the_driver_directly():
+    """The sequence driver stages problem l+1 on its side stream while it
+    solves problem l; a LAZY device generator queues the work that writes
+    A_{l+1}, B_{l+1} on the solver's stream inside next(). The staging must
+    wait for it (the driver records an event after each next() and the side
+    stream waits on it): fed the generator itself, the results are bitwise
+    those of the materialised list."""
+    import paper_1206_3768_b200 as pkg
+    import torch
+
+    cfg_b = pkg.BASELINE_CONFIGS["C1"]
+    cfg = pkg.ChfsiConfig(nev=cfg_b.nev, nex=cfg_b.nex, deg=cfg_b.deg)
+    listed = pkg.solve_sequence(list(pkg.iter_baseline_sequence(cfg_b.n, 4, seed=0, device="cuda:0")),
+                                cfg)
+    lazy = pkg.solve_sequence(pkg.iter_baseline_sequence(cfg_b.n, 4, seed=0, device="cuda:0"), cfg)
+    assert len(lazy) == len(listed) == 4
+    for a, b in zip(listed, lazy):
+        assert a.report.locked_per_loop == b.report.locked_per_loop
+        assert np.array_equal(a.values, b.values)
+        assert torch.equal(a.solution.vectors, b.solution.vectors)
