@@ -357,6 +357,10 @@ typedef struct chfsi_loop {
    * and filter_flops stay the algorithmic deg-per-pass counts) */
   long long filter_k1_launches;
   double filter_k1_flops;
+  /* out: passes whose speculative Cholesky-QR2 (acceptance test judged at
+   * the pass's readback, no host round trip inside the QR) was rejected and
+   * redone on the full QR path, together with their Rayleigh-Ritz */
+  long long qr_redone;
 } chfsi_loop;
 
 CHFSI_API int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* loop);

@@ -130,6 +130,7 @@ class LoopState(ctypes.Structure):
         ("filter_flops", _d),
         ("t_filter", _d), ("t_ortho", _d), ("t_rr", _d),
         ("reuse_hp", _i), ("filter_k1_launches", _ll), ("filter_k1_flops", _d),
+        ("qr_redone", _ll),
     ]
 
 

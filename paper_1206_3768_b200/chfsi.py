@@ -156,6 +156,7 @@ class SolveReport:
     filter_k1_flops: float = 0.0
     filter_k1_launches: int = 0
     rr_fast_eigs: int = 0
+    qr_redone: int = 0  # passes whose speculative Cholesky-QR2 was redone on the full path
     filter_degree_sum: int = 0  # sum of per-column degrees (= deg * filtered_vectors unless adaptive)
     tail_vectors: object = None
     lambda_blk_plus_1: float = float("nan")
@@ -704,6 +705,7 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None, _hooks=Non
     report.filter_k1_flops = float(st.filter_k1_flops)
     report.filter_degree_sum = int(st.filter_degree_sum)
     report.rr_fast_eigs = int(st.rr_fast_eigs)
+    report.qr_redone = int(st.qr_redone)
     report.converged = bool(st.converged)
     report.locked_per_loop = [int(x) for x in locked_per_loop[: st.inner_loops]]
     locked_vals = host_f[0, :nlocked].tolist()

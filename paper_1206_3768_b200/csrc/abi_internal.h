@@ -43,12 +43,27 @@ struct chfsi_ctx {
   int filter_chains = 2;  // 1: one launch chain per filter (chfsi_ctx_set_filter_chains)
   void* pinned = nullptr;  // page-locked host staging for small readbacks (grown on demand)
   size_t pinned_bytes = 0;
+  // deferred Cholesky-QR acceptance test (native loop): the checks' inputs
+  // land here and are judged after the pass's own synchronisation
+  void* qr_pinned = nullptr;
+  size_t qr_pinned_bytes = 0;
+  bool qr_pending = false;
+  int qr_pending_n = 0;
 };
 
 namespace chfsi {
 // Page-locked host buffer of at least `bytes` owned by the context (for the
 // small device->host readbacks that drive host decisions).
 int ensure_pinned(chfsi_ctx* ctx, size_t bytes);
+// Cholesky-QR2 with its acceptance test deferred: the panel is backed up,
+// orthonormalised (CholQR2, linearised second pass) and the test's inputs
+// queued to page-locked memory WITHOUT a host synchronisation; after the
+// caller's next stream synchronisation `qr_deferred_verdict` judges them
+// exactly as chfsi_qr_orthonormalize_z would. On rejection
+// `qr_deferred_restore` puts the panel back as it was before the QR.
+int qr_orthonormalize_deferred(chfsi_ctx* ctx, int m, int n, void* Y, long long ldy);
+int qr_deferred_verdict(chfsi_ctx* ctx, bool* accept);
+int qr_deferred_restore(chfsi_ctx* ctx, int m, int n, void* Y);
 // chfsi_filter_z with an optional known first product hy0 = H y0 (ld ldhy0):
 // the first recurrence step is then elementwise (the native loop passes the
 // previous Rayleigh-Ritz's rotated H P)

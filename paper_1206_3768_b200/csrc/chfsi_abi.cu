@@ -150,6 +150,7 @@ int chfsi_ctx_destroy(chfsi_ctx* ctx) {
   for (cudaEvent_t e : ctx->loop_ev)
     if (e) cudaEventDestroy(e);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->qr_pinned) cudaFreeHost(ctx->qr_pinned);
   delete ctx;
   return CHFSI_OK;
 }
@@ -694,7 +695,7 @@ int qr_householder(chfsi_ctx* ctx, int m, int n, double2* y, const double2* back
 int qr_cholqr(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdiag_acc,
               double* rlast, const double* fro, int passes, bool shifted, bool* fallback,
               double* last_dev, bool linear2 = false, bool* linear_reject = nullptr,
-              double2* tmp = nullptr) {
+              double2* tmp = nullptr, bool defer = false) {
   cudaStream_t s = ctx->stream;
   *fallback = false;
   *last_dev = 0.0;
@@ -756,8 +757,17 @@ int qr_cholqr(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdia
                         CUBLAS_DIAG_NON_UNIT, m, n, &one, reinterpret_cast<const cuDoubleComplex*>(g),
                         n, reinterpret_cast<cuDoubleComplex*>(y), m));
   }
-  CK(chfsi::ensure_pinned(ctx, (size_t)(2 * n + 2) * sizeof(double) + 4 * sizeof(int)));
-  double* hd = static_cast<double*>(ctx->pinned);
+  const size_t hbytes = (size_t)(2 * n + 2) * sizeof(double) + 4 * sizeof(int);
+  if (defer && hbytes > ctx->qr_pinned_bytes) {
+    CK_CUDA(cudaStreamSynchronize(s));
+    if (ctx->qr_pinned) CK_CUDA(cudaFreeHost(ctx->qr_pinned));
+    ctx->qr_pinned = nullptr;
+    ctx->qr_pinned_bytes = 0;
+    CK_CUDA(cudaMallocHost(&ctx->qr_pinned, std::max<size_t>(hbytes, 4096)));
+    ctx->qr_pinned_bytes = std::max<size_t>(hbytes, 4096);
+  }
+  if (!defer) CK(chfsi::ensure_pinned(ctx, hbytes));
+  double* hd = static_cast<double*>(defer ? ctx->qr_pinned : ctx->pinned);
   double* hl = hd + n + 1;
   double* heps = hl + n;
   int* info = reinterpret_cast<int*>(heps + 1);
@@ -766,6 +776,13 @@ int qr_cholqr(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdia
   CK_CUDA(cudaMemcpyAsync(hd + n, fro, sizeof(double), cudaMemcpyDeviceToHost, s));
   CK_CUDA(cudaMemcpyAsync(hl, rlast, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s));
   CK_CUDA(cudaMemcpyAsync(info, ctx->dinfo, passes * sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (defer) {  // judged later by qr_deferred_verdict (same checks as below)
+    ctx->qr_pending = true;
+    ctx->qr_pending_n = n;
+    *fallback = false;
+    *last_dev = 0.0;
+    return CHFSI_OK;
+  }
   CK_CUDA(cudaStreamSynchronize(s));
   const double hfro = hd[n];
   bool bad = !std::isfinite(hfro);
@@ -846,6 +863,63 @@ int chfsi_qr_orthonormalize_z(chfsi_ctx* ctx, int m, int n, void* Y, long long l
   }
   return qr_householder(ctx, m, n, y, backup, tau, rdiag, fro, dead, ndead);
 }
+
+}  // extern "C"
+
+namespace chfsi {
+
+int qr_orthonormalize_deferred(chfsi_ctx* ctx, int m, int n, void* Y, long long ldy) {
+  CK_ARG(ctx && Y && m >= n && n >= 1 && ldy == m, "bad deferred QR arguments");
+  CK_ARG(ctx->qr_mode == 0 && ctx->qr_linear2, "the deferred QR is the default Cholesky-QR2 only");
+  cudaStream_t s = ctx->stream;
+  double2* y = static_cast<double2*>(Y);
+  const size_t blk = (size_t)m * n * sizeof(double2);
+  CK(ensure_scratch(ctx, 2 * blk + 2 * (size_t)n * sizeof(double2) + (size_t)n * n * sizeof(double2) +
+                             2 * (size_t)n * sizeof(double)));
+  double2* backup = static_cast<double2*>(ctx->scratch);
+  double2* g = backup + (size_t)m * n + 2 * (size_t)n;
+  double* racc = reinterpret_cast<double*>(g + (size_t)n * n);
+  double2* tmp = reinterpret_cast<double2*>(racc + 2 * (size_t)n);
+  double* fro = ctx->scalars + 1;
+  CK_CUDA(cudaMemcpyAsync(backup, y, blk, cudaMemcpyDeviceToDevice, s));
+  CK_CUDA(chfsi::norm2_launch(y, (long long)m * n, ctx->partial, fro, nullptr, s));
+  bool fallback = false, lin_reject = false;
+  double dev = 0.0;
+  return qr_cholqr(ctx, m, n, y, g, racc, racc + n, fro, 2, false, &fallback, &dev, true,
+                   &lin_reject, tmp, /*defer=*/true);
+}
+
+int qr_deferred_verdict(chfsi_ctx* ctx, bool* accept) {
+  CK_ARG(ctx && accept && ctx->qr_pending, "no deferred QR pending");
+  ctx->qr_pending = false;
+  const int n = ctx->qr_pending_n;
+  const double* hd = static_cast<const double*>(ctx->qr_pinned);
+  const double* hl = hd + n + 1;
+  const double heps = hl[n];
+  const int* info = reinterpret_cast<const int*>(hl + n + 1);
+  const double hfro = hd[n];
+  // the checks of qr_cholqr + chfsi_qr_orthonormalize_z's acceptance (linearised CholQR2)
+  bool ok = std::isfinite(hfro) && info[0] == 0;
+  const double safe = 1e-11 * hfro;
+  double dev = 0.0;
+  for (int j = 0; ok && j < n; ++j) {
+    if (!(hd[j] >= safe)) ok = false;  // also NaN
+    dev = std::max(dev, std::fabs(hl[j] - 1.0));
+  }
+  ok = ok && std::isfinite(dev) && dev <= 1e-6 && heps <= 1e-8;
+  *accept = ok;
+  return CHFSI_OK;
+}
+
+int qr_deferred_restore(chfsi_ctx* ctx, int m, int n, void* Y) {
+  CK_CUDA(cudaMemcpyAsync(Y, ctx->scratch, (size_t)m * n * sizeof(double2), cudaMemcpyDeviceToDevice,
+                          ctx->stream));
+  return CHFSI_OK;
+}
+
+}  // namespace chfsi
+
+extern "C" {
 
 int chfsi_ctx_set_lanczos_mode(chfsi_ctx* ctx, int mode) {
   CK_ARG(ctx, "ctx is NULL");

@@ -75,15 +75,35 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
   return cudaEventElapsedTime(&ms, a, b) == cudaSuccess ? ms : 0.f;
 }
 
+// CHFSI_QR_DEFER=0: the Cholesky-QR acceptance test synchronises inside
+// the QR (one host round trip per pass more) instead of at the pass's end
+bool qr_defer_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CHFSI_QR_DEFER");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 // Two CGS passes against the locked block, then QR; rank-deficient columns
 // are replaced through the fill callback and the whole panel is redone,
 // at most `retries` times (chfsi.py:242-261).
-int orthonormalize(chfsi_ctx* ctx, chfsi_loop* L, void* work, int width) {
+//   mode 1 (speculative): CGS + Cholesky-QR2 with the acceptance test
+//          deferred to the pass's own synchronisation (no host round trip);
+//   mode 2: after a rejected speculation — the pre-QR panel (already
+//          projected) is restored and the full QR path runs.
+int orthonormalize(chfsi_ctx* ctx, chfsi_loop* L, void* work, int width, int mode = 0) {
   const int n = L->n;
   constexpr int retries = 3;
+  if (mode == 1) {
+    if (L->nlocked)
+      CK(chfsi_cgs_project_z(ctx, n, L->nlocked, width, L->locked, n, work, n, L->coef));
+    return chfsi::qr_orthonormalize_deferred(ctx, n, width, work, n);
+  }
+  if (mode == 2) CK(chfsi::qr_deferred_restore(ctx, n, width, work));
   std::vector<int> dead(width);
   for (int attempt = 0;; ++attempt) {
-    if (L->nlocked)
+    if (L->nlocked && !(mode == 2 && attempt == 0))
       CK(chfsi_cgs_project_z(ctx, n, L->nlocked, width, L->locked, n, work, n, L->coef));
     int ndead = 0;
     const int rc = chfsi_qr_orthonormalize_z(ctx, n, width, work, n, dead.data(), &ndead);
@@ -335,8 +355,11 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
     L->filter_k1_flops += 8.0 * (double)n * (double)n * (double)dsum;
     const bool q_in_other = result == other;
 
-    // ---- orthonormalize (chfsi.py:335-336)
-    CK(dist ? orthonormalize_dist(ctx, L, result, width) : orthonormalize(ctx, L, result, width));
+    // ---- orthonormalize (chfsi.py:335-336); single-GPU: Cholesky-QR2 with
+    // its acceptance test judged after this pass's readback (speculative)
+    const bool spec = !dist && qr_defer_enabled() && ctx->qr_mode == 0 && ctx->qr_linear2;
+    CK(dist ? orthonormalize_dist(ctx, L, result, width)
+            : orthonormalize(ctx, L, result, width, spec ? 1 : 0));
     CK_CUDA(cudaEventRecord(ev[2], s));
 
     // ---- Rayleigh-Ritz into the buffer the filter left free (chfsi.py:337-350)
@@ -358,6 +381,24 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
     CK_CUDA(cudaMemcpyAsync(host + width, L->res_d, (size_t)width * sizeof(double),
                             cudaMemcpyDeviceToHost, s));
     CK_CUDA(cudaStreamSynchronize(s));
+    if (spec) {  // the speculative QR's acceptance test (its inputs are on the host now)
+      bool accept = false;
+      CK(chfsi::qr_deferred_verdict(ctx, &accept));
+      if (!accept) {  // rare: redo the pass's QR and Rayleigh-Ritz on the full path
+        CK(orthonormalize(ctx, L, result, width, 2));
+        L->rr_fast_eigs -= used_fast;
+        used_fast = 0;
+        CK(rayleigh_ritz(ctx, L, result, rot_p, width, eig_tol, &used_fast));
+        L->rr_fast_eigs += used_fast;
+        host = static_cast<double*>(ctx->pinned);
+        CK_CUDA(cudaMemcpyAsync(host, L->ritz_d, (size_t)width * sizeof(double),
+                                cudaMemcpyDeviceToHost, s));
+        CK_CUDA(cudaMemcpyAsync(host + width, L->res_d, (size_t)width * sizeof(double),
+                                cudaMemcpyDeviceToHost, s));
+        CK_CUDA(cudaStreamSynchronize(s));
+        L->qr_redone += 1;
+      }
+    }
     pending = ev;
     if (dist)  // summed squares of the local row norms
       for (int j = 0; j < width; ++j) host[width + j] = std::sqrt(host[width + j]);

@@ -246,7 +246,10 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
                                       "protocol needs the dense eigendecomposition of the whole H)")
         return _solve_sequence_sharded(pencils, cfg, seed, keep_standard, on_problem, shard)
     caller = torch.cuda.current_stream()
-    solver = solver_stream() if overlap and _PRIORITY else caller
+    # (also without the side stream: the solver's library handles then keep
+    # one history across driver modes — cuBLAS's algorithm choices depend on
+    # it, and results would differ in the last bit between modes)
+    solver = solver_stream() if _PRIORITY else caller
     if solver is caller:
         return _solve_sequence_on(pencils, cfg, seed, mode, keep_standard, on_problem, overlap)
     # The solver's own work runs on a HIGH-priority stream: the block

@@ -367,10 +367,11 @@ def test_sequence_side_worker_matches_inline_and_serial(pkg, monkeypatch):
     for k, (a, b, c) in enumerate(zip(threaded, inline, serial)):
         assert a.solution.form == "generalized"
         assert torch.equal(seen[k], a.solution.vectors)
-        for other in (b, c):
-            assert a.report.locked_per_loop == other.report.locked_per_loop
-            assert np.array_equal(a.values, other.values)
-            assert torch.equal(a.solution.vectors, other.solution.vectors)
+        for name, other in (("inline", b), ("serial", c)):
+            assert a.report.locked_per_loop == other.report.locked_per_loop, (k, name)
+            assert np.array_equal(a.values, other.values), (
+                k, name, float(np.abs(a.values - other.values).max()))
+            assert torch.equal(a.solution.vectors, other.solution.vectors), (k, name)
 
 
 @pytest.mark.gpu
