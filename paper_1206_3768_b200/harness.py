@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import csv
 import gc
+import itertools
 import json
 import os
 import statistics
@@ -246,12 +247,23 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
                                       "protocol needs the dense eigendecomposition of the whole H)")
         return _solve_sequence_sharded(pencils, cfg, seed, keep_standard, on_problem, shard)
     caller = torch.cuda.current_stream()
+    it = iter(pencils)
+    first = next(it, None)
+    if first is None:
+        return []
+    # (a list keeps its length for the output reservation; other iterables
+    # go on lazily behind the peeked first item)
+    seq = pencils if isinstance(pencils, (list, tuple)) else itertools.chain([first], it)
     # (also without the side stream: the solver's library handles then keep
     # one history across driver modes — cuBLAS's algorithm choices depend on
-    # it, and results would differ in the last bit between modes)
-    solver = solver_stream() if _PRIORITY else caller
+    # it, and results would differ in the last bit between modes). Large n:
+    # the staged reduction of problem l+1 (~0.5 s at n = 12000) needs real SM
+    # time beside the solve, so the solver stream keeps the side stream's
+    # priority there (C4: a high-priority solver starved it, +2 s of waits).
+    high = _item_n(first) <= _BACK_SIDE_MAX_N
+    solver = solver_stream(high=high) if _PRIORITY else caller
     if solver is caller:
-        return _solve_sequence_on(pencils, cfg, seed, mode, keep_standard, on_problem, overlap)
+        return _solve_sequence_on(seq, cfg, seed, mode, keep_standard, on_problem, overlap)
     # The solver's own work runs on a HIGH-priority stream: the block
     # scheduler then places its CTAs first whenever SMs free up, so the
     # side stream's reduction of problem l+1 fills the solver's latency gaps
@@ -259,7 +271,7 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
     # (potrf, TRSM, the w x w eigensolver) are waiting for.
     solver.wait_stream(caller)
     with torch.cuda.stream(solver):
-        out = _solve_sequence_on(pencils, cfg, seed, mode, keep_standard, on_problem, overlap)
+        out = _solve_sequence_on(seq, cfg, seed, mode, keep_standard, on_problem, overlap)
     caller.wait_stream(solver)
     for r in out:  # results were allocated on the solver stream, used on the caller's
         for t in (r.solution.vectors if r.solution is not None else None, r.standard_vectors,
@@ -273,12 +285,14 @@ _PRIORITY = os.environ.get("CHFSI_STREAM_PRIORITY", "1") != "0"
 _SOLVER_STREAMS = {}
 
 
-def solver_stream(device=None):
-    """One persistent highest-priority stream per device for the solver."""
+def solver_stream(device=None, high=True):
+    """One persistent solver stream per device and priority class: highest
+    priority (small n) or the default priority of the side stream (large n)."""
     dev = torch.cuda.current_device() if device is None else device
-    st = _SOLVER_STREAMS.get(dev)
+    st = _SOLVER_STREAMS.get((dev, high))
     if st is None:
-        st = _SOLVER_STREAMS[dev] = torch.cuda.Stream(device=dev, priority=-100)
+        st = _SOLVER_STREAMS[(dev, high)] = torch.cuda.Stream(device=dev,
+                                                              priority=-100 if high else 0)
     return st
 
 
