@@ -370,8 +370,25 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
     // zheevd runs instead (measured: 4 zheevd calls less per warm C2 problem).
     const double eig_tol = L->rr_fast_tol > 0.0 ? L->rr_fast_tol : 0.0;
     int used_fast = 0;
-    CK(dist ? rayleigh_ritz_dist(ctx, L, result, rot_p, width, eig_tol, &used_fast)
-            : rayleigh_ritz(ctx, L, result, rot_p, width, eig_tol, &used_fast));
+    bool spec_redo = false;  // the speculative QR must be judged (and redone) now
+    if (dist) {
+      CK(rayleigh_ritz_dist(ctx, L, result, rot_p, width, eig_tol, &used_fast));
+    } else {
+      const int rc = rayleigh_ritz(ctx, L, result, rot_p, width, eig_tol, &used_fast);
+      if (rc != CHFSI_OK) {
+        // A failed Cholesky inside the speculative QR leaves non-finite
+        // panels; the eigensolver then fails before the pass's readback.
+        // Judge the QR first: a rejection redoes the pass below; an
+        // accepted QR means the failure is genuine.
+        if (!spec) return rc;
+        CK_CUDA(cudaStreamSynchronize(s));
+        bool accept = true;
+        CK(chfsi::qr_deferred_verdict(ctx, &accept));
+        if (accept) return rc;
+        spec_redo = true;
+        used_fast = 0;
+      }
+    }
     CK_CUDA(cudaEventRecord(ev[3], s));
     L->rr_fast_eigs += used_fast;
     L->residual_check_matvecs += width;
@@ -383,7 +400,7 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
     CK_CUDA(cudaStreamSynchronize(s));
     if (spec) {  // the speculative QR's acceptance test (its inputs are on the host now)
       bool accept = false;
-      CK(chfsi::qr_deferred_verdict(ctx, &accept));
+      if (!spec_redo) CK(chfsi::qr_deferred_verdict(ctx, &accept));
       if (!accept) {  // rare: redo the pass's QR and Rayleigh-Ritz on the full path
         CK(orthonormalize(ctx, L, result, width, 2));
         L->rr_fast_eigs -= used_fast;

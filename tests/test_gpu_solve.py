@@ -10,6 +10,8 @@ Parity bar (`north_star`, per problem):
   (in practice the counts are identical).
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -143,6 +145,47 @@ def test_rank_repair_path(pkg):
     assert rep.converged and orep.converged
     assert abs(rep.inner_loops - orep.inner_loops) <= 1
     assert np.abs(sol.values - ov).max() <= 1e-9
+    # the rank-deficient first panel fails the speculative Cholesky-QR2 (its
+    # acceptance test is judged at the pass's readback): that pass's QR and
+    # Rayleigh-Ritz were redone on the full path (Householder + rank repair)
+    assert rep.qr_redone >= 1
+
+
+def test_speculative_qr_matches_synchronous_qr(pkg, monkeypatch):
+    """CHFSI_QR_DEFER=0 (acceptance test inside the QR) and the default
+    speculative path give bitwise the same solve, with and without a
+    rejected speculation (the rank-deficient warm start)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, torch, paper_1206_3768_b200 as pkg\n"
+        "from tests.golden.recipes import random_hermitian\n"
+        "pkg.set_array_output('torch')\n"
+        "rng = np.random.default_rng(21); n, nev, blk = 120, 6, 14\n"
+        "h = random_hermitian(rng, n); w, v = np.linalg.eigh(h)\n"
+        "vec = v[:, :blk].copy(); vec[:, 5] = vec[:, 2]\n"
+        "g = pkg.ChfsiGuess(vec, float(w[0]), float(w[blk]))\n"
+        "h2 = random_hermitian(np.random.default_rng(5), 300)\n"
+        "out = []\n"
+        "for hh, guess, cfg in ((h, g, pkg.ChfsiConfig(nev=nev, blk=blk)),\n"
+        "                        (h2, None, pkg.ChfsiConfig(nev=20, blk=36))):\n"
+        "    sol, rep = pkg.chfsi_solve(hh, cfg, guess=guess, rng=np.random.default_rng(3))\n"
+        "    out.append((sol.values.tobytes().hex(), sol.vectors.cpu().numpy().tobytes().hex()[:4096],\n"
+        "                rep.qr_redone, rep.locked_per_loop))\n"
+        "print(repr(out))\n")
+    runs = []
+    for defer in ("1", "0"):
+        env = dict(os.environ, CHFSI_QR_DEFER=defer)
+        res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                             cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                             timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        runs.append(eval(res.stdout.strip().splitlines()[-1]))
+    spec, sync = runs
+    assert spec[0][2] >= 1 and sync[0][2] == 0  # the speculation was rejected once
+    for a, b in zip(spec, sync):
+        assert a[0] == b[0] and a[1] == b[1] and a[3] == b[3]
 
 
 def test_c1_harness_protocol_matches_reference(pkg, c1_golden):
