@@ -134,10 +134,14 @@ StepTiling choose_step_tiling(int n, int w) {
     // 128x32 with 8 warps (1 CTA/SM): 2048x160 34.7, 4096x160 37.7,
     // 5000x600 39.0, 12000x1400 41.6; 64x16 with 4 warps when it pads
     // >10 % fewer columns (2048x100: 28.0 vs 26.5).
+    // (round 2, 32-deep slabs, profiles/r03e_k1_narrow_tiles.txt, n = 2048:
+    // 64x16 wins whenever it pads fewer columns — w = 144: 34.3 vs 32.8,
+    // w = 80: 31.7 vs 27.8 — and at w <= 64 — w = 64: 30.5 vs 29.6; 64x32 at
+    // equal padding above that — w = 96/128/160: 33.3/35.1/36.4 vs 32.4/33.6/34.0)
     const int p16 = ((w + 15) / 16) * 16, p32 = ((w + 31) / 32) * 32;
     StepTiling t{64, 32, 0};
     t.warps = 4;
-    if (w <= 16 || p16 * 10 < p32 * 9) t.bn = 16;
+    if (w <= 64 || p16 < p32) t.bn = 16;
     else if (n >= 8000 || w >= 400) {
       t.bm = 128;
       t.warps = 8;
