@@ -561,7 +561,8 @@ def _safe_window(scale_ref, a, b):
 
 # ----------------------------------------------------------------- solver ---
 
-def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None, _hooks=None, _sync=True):
+def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None, _hooks=None, _sync=True,
+                _out=None):
     """Compute the ``cfg.nev`` lowest eigenpairs of the Hermitian ``h``
     (chfsi.py:274-384). ``h`` may be a numpy array (uploaded once) or a CUDA
     tensor in either row- or column-major layout (used in place).
@@ -662,7 +663,8 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None, _hooks=Non
     st.g, st.coef = g_buf.data_ptr(), coef.data_ptr()
     st.ritz_d, st.res_d, st.perm_d = ritz_d.data_ptr(), res_d.data_ptr(), perm_d.data_ptr()
     st.adaptive, st.deg_min = int(cfg.adaptive_degree), int(cfg.min_degree)
-    tail = fblock(rows, blk, dev)
+    # (_out: the sequence driver's preallocated (tail, vectors) blocks)
+    tail = _out[0] if _out is not None else fblock(rows, blk, dev)
     st.tail = tail.data_ptr()
     st.win_a, st.win_b, st.win_scale_ref = window.a, window.b, window.scale_ref
     st.pb, st.off, st.width = 0, 0, blk
@@ -725,7 +727,16 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None, _hooks=Non
     if comm is not None:  # every rank returns the full vectors
         full = fblock(n, nlocked, dev)
         vecs = comm.gather_rows(to_fblock(vecs, copy=True), full)
-    vecs = to_host(vecs) if host else to_fblock(vecs, copy=True)
+    if host:
+        vecs = to_host(vecs)
+    elif _out is not None and not nlocked:
+        vecs = _out[1][:, :0]
+    elif _out is not None:
+        dst = _out[1][:, :nlocked]
+        dst.copy_(vecs)
+        vecs = dst
+    else:
+        vecs = to_fblock(vecs, copy=True)
     sol = EigenSolution(values=np.asarray(locked_vals)[order], vectors=vecs, form="standard",
                         label=label)
     report.final_residuals = np.asarray(locked_res)[order]

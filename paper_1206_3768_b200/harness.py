@@ -160,6 +160,13 @@ class _StagingSlots:
         return pair
 
 
+# the staging pairs of small sequences, reused by later calls on the same
+# stream: problem l+2's staging is ordered after problem l's solve (the event
+# it waits on) and back-transform (same side stream), and a later call's
+# first staging after everything of the previous call
+_SLOT_CACHE = {}
+
+
 def _item_n(item):
     a = item.a if isinstance(item, EigenPencil) else item[1]
     return int(a.shape[0])
@@ -194,25 +201,69 @@ def _stage(item, side, ready=None, slot=None):
     return pencil, sp, ev, checks
 
 
-def _reserve_outputs(pencil, cfg, pencils):
-    """Grow torch's caching allocator once, up front, by what the sequence's
-    results will hold (per problem: tail block, standard and generalized
-    solution vectors). Each steady-state cudaMalloc otherwise happens at an
-    arbitrary point of the solve loop and was measured to stall the host for
-    15-100 ms on B200 boxes; carving the outputs out of one cached segment
-    removes them. Skipped when the length is unknown or the reservation
-    would exceed 10 % of the free device memory."""
+class _OutputArena:
+    """One device block per sequence call holding every problem's outputs —
+    the chained tail (n x blk) and the eigenvector block (n x nev) — carved
+    as column-major views. One allocation of the same size per call reuses
+    the same cached segment of torch's allocator (the previous call's results
+    released it), where per-problem allocations and the round-1 "reserve and
+    free" trick made the allocator cudaMalloc new segments at arbitrary
+    points (measured: +25-90 ms in ~1 of 5 C2 sequences, in the reservation
+    or inside a solve). The views keep the block alive as long as any result
+    is alive."""
+
+    def __init__(self, count, n, blk, nev, device):
+        self.per = n * (blk + nev)
+        self.buf = torch.empty(count * self.per, dtype=torch.complex128, device=device)
+        self.k = 0
+        self.count = count
+
+    def take(self, n, blk, nev):
+        if self.k >= self.count or n * (blk + nev) != self.per:
+            return None
+        base = self.buf[self.k * self.per:(self.k + 1) * self.per]
+        self.k += 1
+        tail = base[: n * blk].view(blk, n).t()
+        vecs = base[n * blk:].view(nev, n).t()
+        return tail, vecs
+
+
+def _output_arena(pencil, cfg, pencils):
+    """The per-call output arena (None when the sequence length is unknown
+    or the outputs would take more than 5 % of the device memory)."""
     try:
         length = len(pencils)
     except TypeError:
-        return
+        return None
     n = pencil.n
     blk = cfg.resolve(n)[0]
-    need = length * (n * blk + 2 * n * cfg.nev) * 16 * 5 // 4  # + rounding slack
-    free, _ = torch.cuda.mem_get_info()
-    if need > free // 10:
-        return
-    torch.empty(need, dtype=torch.uint8, device=torch.cuda.current_device())
+    dev = torch.cuda.current_device()
+    total = _TOTAL_MEM.get(dev)
+    if total is None:
+        total = _TOTAL_MEM[dev] = torch.cuda.get_device_properties(dev).total_memory
+    if length * n * (blk + cfg.nev) * 16 > total // 20:
+        return None
+    # The previous call's arena of this shape is reused when none of its
+    # results is alive any more (the storage is referenced by the cached
+    # tensor alone): no allocation at all in a steady sequence of calls.
+    key = (dev, torch.cuda.current_stream().cuda_stream, length, n, blk, cfg.nev)
+    cached = _ARENAS.get(key)
+    if cached is not None and _storage_users(cached.buf) <= 1:
+        cached.k = 0
+        return cached
+    arena = _ARENAS[key] = _OutputArena(length, n, blk, cfg.nev, dev)
+    if len(_ARENAS) > 4:  # a few shapes at most
+        _ARENAS.pop(next(iter(_ARENAS)))
+    return arena
+
+
+def _storage_users(t):
+    """Tensors (the base and its views) sharing ``t``'s storage."""
+    return torch._C._storage_Use_Count(t.untyped_storage()._cdata) - 1
+
+
+_ARENAS = {}
+_TOTAL_MEM = {}
 
 
 def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on_problem=None,
@@ -282,6 +333,15 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
 
 
 _PRIORITY = os.environ.get("CHFSI_STREAM_PRIORITY", "1") != "0"
+# CHFSI_DRIVER_TRACE=1: (event, perf_counter) marks of the driver's host
+# timeline appended to DRIVER_TRACE (diagnostics: tools/diag/step_outliers.py)
+_TRACE_ON = os.environ.get("CHFSI_DRIVER_TRACE") == "1"
+DRIVER_TRACE = []
+
+
+def _mark(what):
+    if _TRACE_ON:
+        DRIVER_TRACE.append((what, time.perf_counter()))
 _SOLVER_STREAMS = {}
 
 
@@ -298,6 +358,7 @@ def solver_stream(device=None, high=True):
 
 def _solve_sequence_on(pencils, cfg, seed, mode, keep_standard, on_problem, overlap):
     """solve_sequence's single-GPU body on the current stream."""
+    _mark("enter")
     out = []
     guess = None
     main = torch.cuda.current_stream()
@@ -317,16 +378,28 @@ def _solve_sequence_on(pencils, cfg, seed, mode, keep_standard, on_problem, over
     it = iter(pencils)
     first = next(it, None)
     slots = None
-    if first is not None and _item_n(first) > _BACK_SIDE_MAX_N:
-        slots = _StagingSlots(_item_n(first), torch.cuda.current_device())
+    if first is not None:
+        n0 = _item_n(first)
+        if n0 > _BACK_SIDE_MAX_N:  # per call: 12.8 GB per pair at C5
+            slots = _StagingSlots(n0, torch.cuda.current_device())
+        else:  # kept across calls: no per-problem 2 n^2 allocations at all
+            key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream, n0)
+            slots = _SLOT_CACHE.get(key)
+            if slots is None:
+                if len(_SLOT_CACHE) >= 2:
+                    _SLOT_CACHE.pop(next(iter(_SLOT_CACHE)))
+                slots = _SLOT_CACHE[key] = _StagingSlots(n0, torch.cuda.current_device())
 
     def slot():
         return None if slots is None else slots.take(side)
 
     staged = _stage(first, side, produced(), slot()) if first is not None else None
+    _mark("first stage issued")
     prefetch = None
+    arena = None
     if staged is not None:
-        _reserve_outputs(staged[0], cfg, pencils)
+        arena = _output_arena(staged[0], cfg, pencils)
+        _mark("output arena")
         # problem 1 is a cold start: its draws (q0, then the n x blk block)
         # run on a host thread from here on, behind its upload and reduction
         p0 = staged[0]
@@ -414,8 +487,10 @@ def _solve_sequence_on(pencils, cfg, seed, mode, keep_standard, on_problem, over
         res.solution, done = fut.result()
         return done
 
+    _mark("first staged")
     try:
         while staged is not None:
+            _mark("problem top")
             t0 = time.perf_counter()
             if not isinstance(staged, tuple):  # issued by the worker during the last solve
                 fut, staged = staged, staged.result()
@@ -449,8 +524,11 @@ def _solve_sequence_on(pencils, cfg, seed, mode, keep_standard, on_problem, over
             rng = np.random.default_rng((seed, pencil.label, start))
             if prefetch is not None:  # (always problem 1: guess is None there)
                 rng, prefetch = prefetch, None
+            _mark("solve start")
+            out_bufs = arena.take(n, blk, cfg.nev) if arena is not None else None
             sol, rep = chfsi_solve(sp.h, cfg, guess=guess, rng=rng, label=pencil.label,
-                                   _hooks=flush if deferred else None, _sync=False)
+                                   _hooks=flush if deferred else None, _sync=False, _out=out_bufs)
+            _mark("solve end")
             t2 = time.perf_counter()
             back = None
             # at large n the side-stream back-transform would keep L of problem
@@ -491,13 +569,16 @@ def _solve_sequence_on(pencils, cfg, seed, mode, keep_standard, on_problem, over
                 on_problem(res)
             del sp
     finally:
+        _mark("loop end")
         flush()
         wait(issued)  # nothing the worker issues outlives this call
+        _mark("worker idle")
         if gc_on:
             gc.enable()
     for res, fut in pending:
         settle(res, fut)  # re-raises a failed back-transform
     main.wait_stream(side)
+    _mark("exit")
     return out
 
 
