@@ -469,3 +469,39 @@ def test_sequence_driver_releases_its_operators(pkg):
         torch.cuda.synchronize()
         used.append(torch.cuda.memory_allocated(dev))
     assert len(set(used[1:])) == 1, used
+
+
+@pytest.mark.gpu
+def test_sequence_outputs_reuse_cached_blocks_without_gc(pkg):
+    """Steady sequences of calls allocate nothing from the device: dropping
+    the last reference to a call's results frees its output block for the
+    next call at once (no cyclic GC pass needed), and a caller that still
+    holds the previous results alternates between cached blocks."""
+    import gc
+
+    cfg_b = pkg.BASELINE_CONFIGS["C1"]
+    cfg = pkg.ChfsiConfig(nev=cfg_b.nev, nex=cfg_b.nex, deg=cfg_b.deg, tol=cfg_b.tol)
+    dev = torch.device("cuda", 0)
+    seq = [pkg.EigenPencil(a=torch.from_numpy(a).to(dev), b=torch.from_numpy(b).to(dev), label=lab)
+           for lab, a, b in pkg.iter_baseline_sequence(cfg_b.n, 6, seed=0)]
+    for _ in range(3):  # warm: workspaces, staging slots, output blocks
+        pkg.solve_sequence(seq, cfg, seed=0)
+    gc.collect()
+    gc.disable()
+    try:
+        res = pkg.solve_sequence(seq, cfg, seed=0)
+        blocks = set()
+        allocs = torch.cuda.memory_stats(dev)["num_device_alloc"]
+        for _ in range(4):  # results dropped before the next call
+            res = None
+            res = pkg.solve_sequence(seq, cfg, seed=0)
+            blocks.add(res[0].solution.vectors.untyped_storage().data_ptr())
+        assert len(blocks) == 1, blocks
+        for _ in range(4):  # previous results still held during the next call
+            res = pkg.solve_sequence(seq, cfg, seed=0)
+            blocks.add(res[0].solution.vectors.untyped_storage().data_ptr())
+        assert len(blocks) <= 3, blocks
+        torch.cuda.synchronize()
+        assert torch.cuda.memory_stats(dev)["num_device_alloc"] == allocs
+    finally:
+        gc.enable()
