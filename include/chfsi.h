@@ -157,6 +157,15 @@ CHFSI_API int chfsi_set_complex_product(int product);
  * halves = 0 only queries. No reference counterpart (tuning knob). */
 CHFSI_API int chfsi_set_k1_slab(int halves);
 
+/* Panel kernels of the Cholesky-QR2 orthonormalisation (process-wide; default
+ * on unless CHFSI_PANEL_KERNELS=0): for panel widths <= 192 the triangular
+ * solve Y L^-H and the linearised second pass run as one hand-written
+ * row-parallel kernel each instead of cuBLAS ZTRSM / ZGEMM chains. on = 1 / 0
+ * sets, -1 queries; returns the previous setting. Same algebra, results
+ * agree to rounding. No reference counterpart (tuning knob; the reference's
+ * QR is numpy's Householder, linalg.py:152-178). */
+CHFSI_API int chfsi_set_panel_kernels(int on);
+
 /* ---------------------------------------------------------------- K2 ---
  * k-step Lanczos with full reorthogonalization (chfsi.py:125-162): q0 is
  * the raw start vector (normalised on device), basis an n x k column-major

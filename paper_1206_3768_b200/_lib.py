@@ -75,6 +75,7 @@ _SIGNATURES = {
     "chfsi_step_tiling": [_i, _i, _pi, _pi, _pi],
     "chfsi_set_complex_product": [_i],
     "chfsi_set_k1_slab": [_i],
+    "chfsi_set_panel_kernels": [_i],
     "chfsi_debug_k1_trace": [ctypes.POINTER(ctypes.c_ulonglong), _i],
     "chfsi_lanczos_z": [_vp, _i, _i, _vp, _ll, _i, _vp, _vp, _pd, _pd, _pd, _pi],
     "chfsi_gemm_z": [_vp, _c, _c, _i, _i, _i, _d, _d, _vp, _ll, _vp, _ll, _d, _d, _vp, _ll],

@@ -49,6 +49,7 @@ struct chfsi_ctx {
   size_t qr_pinned_bytes = 0;
   bool qr_pending = false;
   int qr_pending_n = 0;
+  double2* panel_linv = nullptr;  // inverted diagonal blocks of the Cholesky-QR factor (panel_kernels.cu)
 };
 
 namespace chfsi {

@@ -19,7 +19,7 @@ PKG = os.path.dirname(CSRC)
 ROOT = os.path.dirname(PKG)
 BUILD = os.path.join(CSRC, "build")
 LIB = os.path.join(PKG, "libchfsi.so")
-SOURCES = ["cheb_step.cu", "cheb_step_3m.cu", "lanczos.cu", "nd_eig.cu", "nd_persist.cu", "aux_kernels.cu",
+SOURCES = ["cheb_step.cu", "cheb_step_3m.cu", "lanczos.cu", "nd_eig.cu", "nd_persist.cu", "aux_kernels.cu", "panel_kernels.cu",
            "chfsi_abi.cu", "chfsi_loop.cu"]
 HEADERS = ["common.cuh", "cheb_step_kernel.cuh", "chfsi_internal.h", "abi_internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -24,6 +24,11 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 namespace chfsi {
 static thread_local std::string g_last_error;
+// Cholesky-QR2 panel kernels (panel_kernels.cu) on/off: CHFSI_PANEL_KERNELS, chfsi_set_panel_kernels()
+static std::atomic<bool> g_panel_kernels{[] {
+  const char* e = getenv("CHFSI_PANEL_KERNELS");
+  return !(e && atoi(e) == 0);
+}()};
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
@@ -137,6 +142,7 @@ int chfsi_ctx_destroy(chfsi_ctx* ctx) {
   cudaFree(ctx->scalars);
   cudaFree(ctx->dinfo);
   cudaFree(ctx->lstate);
+  cudaFree(ctx->panel_linv);
   cudaFree(ctx->step_ws.partials);
   cudaFree(ctx->step_ws.flags);
   if (ctx->aux_stream) {
@@ -530,6 +536,12 @@ int chfsi_set_complex_product(int product) {
   return chfsi::set_complex_product(product);
 }
 
+int chfsi_set_panel_kernels(int on) {
+  CK_ARG(on == -1 || on == 0 || on == 1, "panel kernels: 1 on, 0 off, -1 query");
+  if (on == -1) return chfsi::g_panel_kernels.load(std::memory_order_relaxed) ? 1 : 0;
+  return chfsi::g_panel_kernels.exchange(on != 0) ? 1 : 0;
+}
+
 int chfsi_set_k1_slab(int halves) {
   CK_ARG(halves == 0 || halves == 2 || halves == 4, "k-slab depth must be 2 or 4 halves");
   if (halves == 0) {  // query
@@ -701,7 +713,12 @@ int qr_cholqr(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdia
   *last_dev = 0.0;
   if (linear_reject) *linear_reject = false;
   linear2 = linear2 && passes == 2 && !shifted && tmp != nullptr;
-  double* eps_dev = ctx->scalars + 8;
+  // The acceptance test's inputs are contiguous on the device in the order
+  // the host reads them — [rdiag_acc n | fro | rlast n | eps | info] (the
+  // callers lay the scratch out so) — and come back in ONE copy per call.
+  CK_ARG(rlast == rdiag_acc + n + 1 && fro == rdiag_acc + n, "qr_cholqr scratch layout");
+  double* eps_dev = rlast + n;
+  int* info_dev = reinterpret_cast<int*>(rlast + n + 1);
   // The factor is taken LOWER (G = L L^H, L = R^H) and Y <- Y L^-H: cuSOLVER's
   // lower potrf is ~1.8x faster than its upper one at the panel sizes (w=160:
   // 74 vs 135 us, tools/microbench/qr_bench.cu); the TRSM costs the same.
@@ -717,6 +734,14 @@ int qr_cholqr(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdia
   // 2048 x 160: 25 vs 76 us), and the linearised pass's Q1 M by out-of-place
   // ZTRMM from w >= 400 (5000 x 600: 0.28 vs 0.43 ms; 2048 x 160: ZGEMM 23 vs 26 us).
   const bool herk = n >= 1000, trmm = n >= 400;
+  // Panel widths of the ChFSI loop (n <= kPanelMaxW): the triangular solve
+  // and the linearised pass run as one row-parallel kernel each
+  // (panel_kernels.cu) instead of cuBLAS's latency-bound ZTRSM chain and
+  // near-identity update + ZGEMM + copy-back (2048 x 160 in the C2 loop:
+  // ~47 + ~45 us -> ~2 x 10 us). CHFSI_PANEL_KERNELS=0 restores the
+  // library calls.
+  const bool panel = chfsi::g_panel_kernels.load(std::memory_order_relaxed) && n <= chfsi::kPanelMaxW;
+  if (panel && !ctx->panel_linv) CK_CUDA(cudaMalloc(&ctx->panel_linv, chfsi::panel_linv_bytes()));
   for (int pass = 0; pass < passes; ++pass) {
     const bool lin = linear2 && pass == 1;
     if (herk) {  // lower triangle for potrf, upper for the near-identity kernel
@@ -731,6 +756,10 @@ int qr_cholqr(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdia
                           reinterpret_cast<cuDoubleComplex*>(g), n));
     }
     if (shifted && pass == 0) CK_CUDA(chfsi::add_diag_shift_launch(g, n, n, fro, shift_coef, s));
+    if (linear2 && pass == 1 && panel) {
+      CK_CUDA(chfsi::panel_apply_near_identity_launch(y, m, m, n, g, n, rdiag_acc, rlast, eps_dev, s));
+      continue;
+    }
     if (linear2 && pass == 1) {
       CK_CUDA(chfsi::near_identity_update_launch(g, n, n, rdiag_acc, rlast, eps_dev, s));
       // Q = Q1 M out of place (ZGEMM + copy back: 2048 x 160 27 us vs 47 us
@@ -750,7 +779,14 @@ int qr_cholqr(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdia
     }
     CK_SOLVER(cusolverDnZpotrf(ctx->solver, CUBLAS_FILL_MODE_LOWER, n,
                                reinterpret_cast<cuDoubleComplex*>(g), n,
-                               static_cast<cuDoubleComplex*>(ctx->ws), lwork, ctx->dinfo + pass));
+                               static_cast<cuDoubleComplex*>(ctx->ws), lwork, info_dev + pass));
+    if (panel) {
+      CK_CUDA(chfsi::panel_post_potrf_launch(g, n, n, rdiag_acc, pass == 0,
+                                             pass == passes - 1 ? rlast : nullptr, ctx->panel_linv,
+                                             linear2 ? eps_dev : nullptr, s));
+      CK_CUDA(chfsi::panel_trsm_lh_launch(y, m, m, n, g, n, ctx->panel_linv, s));
+      continue;
+    }
     CK_CUDA(chfsi::diag_accumulate_launch(g, n, n, rdiag_acc, pass == 0, s));
     if (pass == passes - 1) CK_CUDA(chfsi::diag_accumulate_launch(g, n, n, rlast, true, s));
     CK_BLAS(cublasZtrsm(ctx->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C,
@@ -771,11 +807,7 @@ int qr_cholqr(chfsi_ctx* ctx, int m, int n, double2* y, double2* g, double* rdia
   double* hl = hd + n + 1;
   double* heps = hl + n;
   int* info = reinterpret_cast<int*>(heps + 1);
-  if (linear2) CK_CUDA(cudaMemcpyAsync(heps, eps_dev, sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK_CUDA(cudaMemcpyAsync(hd, rdiag_acc, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK_CUDA(cudaMemcpyAsync(hd + n, fro, sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK_CUDA(cudaMemcpyAsync(hl, rlast, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK_CUDA(cudaMemcpyAsync(info, ctx->dinfo, passes * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK_CUDA(cudaMemcpyAsync(hd, rdiag_acc, hbytes, cudaMemcpyDeviceToHost, s));
   if (defer) {  // judged later by qr_deferred_verdict (same checks as below)
     ctx->qr_pending = true;
     ctx->qr_pending_n = n;
@@ -826,14 +858,16 @@ int chfsi_qr_orthonormalize_z(chfsi_ctx* ctx, int m, int n, void* Y, long long l
   // last pass's diagonal (n)
   const size_t blk = (size_t)m * n * sizeof(double2);
   CK(ensure_scratch(ctx, 2 * blk + 2 * (size_t)n * sizeof(double2) + (size_t)n * n * sizeof(double2) +
-                             2 * (size_t)n * sizeof(double)));
+                             (2 * (size_t)n + 4) * sizeof(double)));
   double2* backup = static_cast<double2*>(ctx->scratch);
   double2* tau = backup + (size_t)m * n;
   double2* rdiag = tau + n;
   double2* g = rdiag + n;
+  // [racc n | fro | rlast n | eps | info]: the acceptance test's inputs (qr_cholqr)
   double* racc = reinterpret_cast<double*>(g + (size_t)n * n);
-  double2* tmp = reinterpret_cast<double2*>(racc + 2 * (size_t)n);  // m x n (linearised pass 2)
-  double* fro = ctx->scalars + 1;
+  double* fro = racc + n;
+  double* rlast = racc + n + 1;
+  double2* tmp = reinterpret_cast<double2*>(racc + 2 * (size_t)n + 4);  // m x n (linearised pass 2)
   CK_CUDA(cudaMemcpyAsync(backup, y, blk, cudaMemcpyDeviceToDevice, s));
   CK_CUDA(chfsi::norm2_launch(y, (long long)m * n, ctx->partial, fro, nullptr, s));
   if (ctx->qr_mode != 1) {  // 0: Cholesky-QR first, 1: Householder only
@@ -847,17 +881,17 @@ int chfsi_qr_orthonormalize_z(chfsi_ctx* ctx, int m, int n, void* Y, long long l
     // Cholesky-QR3 runs from the backup, and Householder after that.
     if (ctx->qr_mode == 0) {
       bool lin_reject = false;
-      CK(qr_cholqr(ctx, m, n, y, g, racc, racc + n, fro, 2, false, &fallback, &dev,
+      CK(qr_cholqr(ctx, m, n, y, g, racc, rlast, fro, 2, false, &fallback, &dev,
                    ctx->qr_linear2, &lin_reject, tmp));
       if (!fallback && dev <= 1e-6) return CHFSI_OK;
       CK_CUDA(cudaMemcpyAsync(y, backup, blk, cudaMemcpyDeviceToDevice, s));
       if (lin_reject) {  // the first pass was fine but left |Q1^H Q1 - I| > 1e-8: exact pass 2
-        CK(qr_cholqr(ctx, m, n, y, g, racc, racc + n, fro, 2, false, &fallback, &dev));
+        CK(qr_cholqr(ctx, m, n, y, g, racc, rlast, fro, 2, false, &fallback, &dev));
         if (!fallback && dev <= 1e-6) return CHFSI_OK;
         CK_CUDA(cudaMemcpyAsync(y, backup, blk, cudaMemcpyDeviceToDevice, s));
       }
     }
-    CK(qr_cholqr(ctx, m, n, y, g, racc, racc + n, fro, 3, true, &fallback, &dev));
+    CK(qr_cholqr(ctx, m, n, y, g, racc, rlast, fro, 3, true, &fallback, &dev));
     if (!fallback) return CHFSI_OK;
     CK_CUDA(cudaMemcpyAsync(y, backup, blk, cudaMemcpyDeviceToDevice, s));
   }
@@ -875,17 +909,18 @@ int qr_orthonormalize_deferred(chfsi_ctx* ctx, int m, int n, void* Y, long long 
   double2* y = static_cast<double2*>(Y);
   const size_t blk = (size_t)m * n * sizeof(double2);
   CK(ensure_scratch(ctx, 2 * blk + 2 * (size_t)n * sizeof(double2) + (size_t)n * n * sizeof(double2) +
-                             2 * (size_t)n * sizeof(double)));
+                             (2 * (size_t)n + 4) * sizeof(double)));
   double2* backup = static_cast<double2*>(ctx->scratch);
   double2* g = backup + (size_t)m * n + 2 * (size_t)n;
-  double* racc = reinterpret_cast<double*>(g + (size_t)n * n);
-  double2* tmp = reinterpret_cast<double2*>(racc + 2 * (size_t)n);
-  double* fro = ctx->scalars + 1;
+  double* racc = reinterpret_cast<double*>(g + (size_t)n * n);  // [racc n | fro | rlast n | eps | info]
+  double* fro = racc + n;
+  double* rlast = racc + n + 1;
+  double2* tmp = reinterpret_cast<double2*>(racc + 2 * (size_t)n + 4);
   CK_CUDA(cudaMemcpyAsync(backup, y, blk, cudaMemcpyDeviceToDevice, s));
   CK_CUDA(chfsi::norm2_launch(y, (long long)m * n, ctx->partial, fro, nullptr, s));
   bool fallback = false, lin_reject = false;
   double dev = 0.0;
-  return qr_cholqr(ctx, m, n, y, g, racc, racc + n, fro, 2, false, &fallback, &dev, true,
+  return qr_cholqr(ctx, m, n, y, g, racc, rlast, fro, 2, false, &fallback, &dev, true,
                    &lin_reject, tmp, /*defer=*/true);
 }
 

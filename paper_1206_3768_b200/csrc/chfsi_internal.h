@@ -169,6 +169,22 @@ cudaError_t cheb_first_step_launch(const double2* hy, long long ldhy, const doub
 // acc[i] *= 1 + E_ii/2, last[i] = 1 + E_ii/2 (the R2 diagonal to O(|E|^2)).
 cudaError_t near_identity_update_launch(double2* g, long long ldg, int n, double* acc, double* last,
                                         double* out, cudaStream_t s);
+// ---- Cholesky-QR2 panel kernels (panel_kernels.cu), widths <= kPanelMaxW ----
+constexpr int kPanelMaxW = 192;
+size_t panel_linv_bytes();
+// after potrf (lower L in g): acc[i] = (first ? 1 : acc[i]) * L_ii, last[i] = L_ii
+// (when given), the inverted 16x16 diagonal blocks of L into linv, *eps = 0
+cudaError_t panel_post_potrf_launch(const double2* g, long long ldg, int n, double* acc, bool first,
+                                    double* last, double2* linv, double* eps, cudaStream_t s);
+// Y <- Y L^-H (m x n, ld; L lower n x n), one kernel, rows in shared memory
+cudaError_t panel_trsm_lh_launch(double2* y, long long ld, int m, int n, const double2* l, long long ldl,
+                                 const double2* linv, cudaStream_t s);
+// linearised second pass in one kernel: Y <- Y (I - tri(G2 - I)) from the
+// Gram matrix G2 (upper triangle read), *eps = max(*eps, max|E_ij|),
+// acc[i] *= 1 + E_ii/2, last[i] = 1 + E_ii/2
+cudaError_t panel_apply_near_identity_launch(double2* y, long long ld, int m, int n, const double2* g2,
+                                             long long ldg, double* acc, double* last, double* eps,
+                                             cudaStream_t s);
 // Y[:, j] = X[:, j]
 cudaError_t copy_cols_launch(const double2* x, long long ldx, double2* y, long long ldy, int m,
                              int n, cudaStream_t s);
