@@ -26,7 +26,7 @@ namespace chfsi {
 
 namespace {
 
-constexpr int PK_THREADS = 256;
+constexpr int PK_THREADS = 512;
 
 __device__ __forceinline__ void cmac(double2& acc, const double2 a, const double2 b) {  // acc += a b
   acc.x = fma(a.x, b.x, acc.x);
@@ -90,22 +90,38 @@ __global__ void __launch_bounds__(32) panel_post_potrf_kernel(const double2* g, 
   if (b == 0 && lane == 0 && eps) *eps = 0.0;
 }
 
-// shared memory: the CTA's rows [np][16], two factor-block buffers [np][17]
-// (cp.async double buffering), the k-parity hand-over and T tiles, two
-// inverted-diagonal-block buffers
+// shared memory (complex elements): the CTA's rows [np][XS], two factor-block
+// buffers [np][FS] (cp.async double buffering), the off-diagonal partial
+// tiles [4 k-quarters][4 blocks][32 lanes][2], T [16][XS], two
+// inverted-diagonal-block buffers [16][FS]. Row strides of 18 elements
+// (288 B) keep the 16-byte DMMA fragment loads bank-conflict free.
+constexpr int XS = 18, FS = 18;
 __host__ __device__ constexpr size_t panel_smem_bytes(int np) {
-  return ((size_t)np * 16 + 2 * (size_t)np * 17 + 4 * 256) * sizeof(double2);
+  return ((size_t)np * XS + 2 * (size_t)np * FS + 1024 + 16 * XS + 2 * 16 * FS) * sizeof(double2);
+}
+
+// complex 8x8x4 block on DMMA: (cr, ci) += a b (CONJ_B: a conj(b)), four real products
+template <bool CONJ_B>
+__device__ __forceinline__ void zmma884(double (&cr)[2], double (&ci)[2], const double2 a, const double2 b) {
+  dmma884(cr, a.x, b.x);
+  dmma884(cr, CONJ_B ? a.y : -a.y, b.y);
+  dmma884(ci, a.y, b.x);
+  dmma884(ci, CONJ_B ? -a.x : a.x, b.y);
 }
 
 // MODE 0: Y <- Y L^-H (L lower in g, inverted diagonal blocks in linv).
 // MODE 1: Y <- Y M, M = I - tri(E), E = G2 - I (G2 upper in g); statistics:
 //         *eps = max(*eps, max |Re/Im E_ij|, i <= j) (NaN propagates),
 //         acc[j] *= 1 + E_jj / 2, last[j] = 1 + E_jj / 2.
-// 256 threads: r = tid & 15 (row), cg = (tid >> 4) & 7 (columns cg, cg + 8 of
-// the current 16-column block), kh = tid >> 7 (even / odd k of the
-// off-diagonal products; the halves are added in fixed order). The factor
-// block of step b + 1 streams into the other buffer (cp.async) while step b
-// computes.
+// 16 warps. Per 16-column block b the 16 x 16 output tile is four 8x8 DMMA
+// blocks (blk = row half + 2 column half); warp w accumulates block w & 3
+// over the k4 steps congruent to w >> 2 mod 4 of the off-diagonal product
+// (fragments straight from shared memory: two 16-byte loads per four
+// DMMA.8x8x4 — the FFMA-style version of this kernel was bound by
+// shared-memory wavefronts at 29 % of the FP64 pipe); the four k-quarters
+// are added in fixed order, and warps 0-3 finish the block (diagonal
+// product, also on DMMA). The factor block of step b + 1 streams into the
+// other buffer (cp.async) while step b computes.
 template <int MODE>
 __global__ void __launch_bounds__(PK_THREADS) panel_right_kernel(double2* y, long long ld, int m, int n,
                                                                  const double2* g, long long ldg,
@@ -113,123 +129,129 @@ __global__ void __launch_bounds__(PK_THREADS) panel_right_kernel(double2* y, lon
                                                                  double* last, double* eps) {
   extern __shared__ double2 psm[];
   const int t16 = (n + 15) >> 4, np = t16 * 16;
-  double2* Xs = psm;                        // [np][16]: column c, row r at c * 16 + r
-  double2* Fbuf = Xs + (size_t)np * 16;     // 2 x [np][17]: factor block, k * 17 + c
-  double2* Ps = Fbuf + 2 * (size_t)np * 17; // [16][16]: odd-k partial sums, c * 16 + r
-  double2* Ts = Ps + 256;                   // [16][16]: c * 16 + r
-  double2* Lbuf = Ts + 256;                 // 2 x [16][16]: k * 16 + c = (L_bb^-1)[c][k]
-  const int tid = threadIdx.x, r = tid & 15, cg = (tid >> 4) & 7, kh = tid >> 7;
+  double2* Xs = psm;                        // [np][XS]: column c, row r at c * XS + r
+  double2* Fbuf = Xs + (size_t)np * XS;     // 2 x [np][FS]: factor block, k * FS + c
+  double2* Ps = Fbuf + 2 * (size_t)np * FS; // [4][4][32][2]: partial C fragments
+  double2* Ts = Ps + 1024;                  // [16][XS]: T, column kk, row r at kk * XS + r
+  double2* Lbuf = Ts + 16 * XS;             // 2 x [16][FS]: k * FS + c = (L_bb^-1)[c][k]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, gq = lane >> 2, t = lane & 3;
+  const int blk = w & 3, kq = w >> 2, rb = blk & 1, cb = blk >> 1;
   const int r0 = blockIdx.x * 16;
   const double2 zero = make_double2(0.0, 0.0);
   // factor block b into buffer `buf` (asynchronous; zero fill outside the matrix)
   auto stage = [&](int b, int buf) {
-    double2* Fs = Fbuf + (size_t)buf * np * 17;
+    double2* Fs = Fbuf + (size_t)buf * np * FS;
     const int b16 = b * 16;
     if (MODE == 0) {  // Fs[k][c] = L[b16 + c][k], k < b16 (c contiguous in memory)
       for (int idx = tid; idx < b16 * 16; idx += PK_THREADS) {
         const int k = idx >> 4, c = idx & 15;
         const bool ok = b16 + c < n;
-        cp_async16(&Fs[k * 17 + c], &g[(long long)k * ldg + (ok ? b16 + c : 0)], ok);
+        cp_async16(&Fs[k * FS + c], &g[(long long)k * ldg + (ok ? b16 + c : 0)], ok);
       }
-      double2* Li = Lbuf + buf * 256;
-      cp_async16(&Li[tid], &linv[(long long)b * 256 + tid], true);
+      double2* Li = Lbuf + buf * 16 * FS;
+      if (tid < 256) cp_async16(&Li[(tid >> 4) * FS + (tid & 15)], &linv[(long long)b * 256 + tid], true);
     } else {  // Fs[k][c] = G2[k][b16 + c], k < b16 + 16 (k contiguous in memory)
       const int klen = b16 + 16;
       for (int idx = tid; idx < klen * 16; idx += PK_THREADS) {
         const int c = idx / klen, k = idx - c * klen, j = b16 + c;
         const bool ok = j < n && k < n;
-        cp_async16(&Fs[k * 17 + c], &g[(long long)(ok ? j : 0) * ldg + (ok ? k : 0)], ok);
+        cp_async16(&Fs[k * FS + c], &g[(long long)(ok ? j : 0) * ldg + (ok ? k : 0)], ok);
       }
     }
   };
   for (int idx = tid; idx < np * 16; idx += PK_THREADS) {
     const int c = idx >> 4, rr = idx & 15;
     const bool ok = c < n && r0 + rr < m;
-    cp_async16(&Xs[idx], &y[ok ? (long long)c * ld + r0 + rr : 0], ok);
+    cp_async16(&Xs[c * XS + rr], &y[ok ? (long long)c * ld + r0 + rr : 0], ok);
   }
   const int first = MODE == 0 ? 0 : t16 - 1, step = MODE == 0 ? 1 : -1;
   stage(first, 0);
   cp_async_commit();
   for (int it = 0; it < t16; ++it) {
     const int b = first + it * step, b16 = b * 16, buf = it & 1;
-    const double2* Fs = Fbuf + (size_t)buf * np * 17;
+    const double2* Fs = Fbuf + (size_t)buf * np * FS;
     if (it + 1 < t16) stage(b + step, buf ^ 1);  // (that buffer's readers finished in step it - 1)
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();  // this step's factor block (and Xs) landed; the previous step's Xs columns are written
-    // off-diagonal products over k < b16, even / odd k by thread half:
+    // off-diagonal product over k < b16:
     //   MODE 0: sum_k X[r][k] conj(L[b16 + c][k]);  MODE 1: sum_k X[r][k] G2[k][b16 + c]
-    // (b16 / 2 k values per thread, a multiple of 8: four independent
-    // accumulator pairs, the twelve operand loads of a group issued ahead
-    // of its sixteen complex MACs)
-    double2 s0, s1;
     {
-      double2 p0[4] = {zero, zero, zero, zero}, p1[4] = {zero, zero, zero, zero};
-      for (int k = kh; k < b16; k += 8) {
-        double2 x[4], f0[4], f1[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          x[u] = Xs[(k + 2 * u) * 16 + r];
-          f0[u] = Fs[(k + 2 * u) * 17 + cg];
-          f1[u] = Fs[(k + 2 * u) * 17 + cg + 8];
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (MODE == 0) {
-            cmac_conj(p0[u], x[u], f0[u]);
-            cmac_conj(p1[u], x[u], f1[u]);
-          } else {
-            cmac(p0[u], x[u], f0[u]);
-            cmac(p1[u], x[u], f1[u]);
-          }
-        }
+      double cr0[2] = {0.0, 0.0}, ci0[2] = {0.0, 0.0}, cr1[2] = {0.0, 0.0}, ci1[2] = {0.0, 0.0};
+      const double2* xa = Xs + t * XS + rb * 8 + gq;
+      const double2* fb = Fs + t * FS + cb * 8 + gq;
+      const int nk4 = b16 >> 2;
+      int k4 = kq;
+      for (; k4 + 4 < nk4; k4 += 8) {  // two steps per trip on independent accumulators
+        const double2 a0 = xa[4 * k4 * XS], f0 = fb[4 * k4 * FS];
+        const double2 a1 = xa[4 * (k4 + 4) * XS], f1 = fb[4 * (k4 + 4) * FS];
+        zmma884<MODE == 0>(cr0, ci0, a0, f0);
+        zmma884<MODE == 0>(cr1, ci1, a1, f1);
       }
-      s0 = make_double2((p0[0].x + p0[1].x) + (p0[2].x + p0[3].x), (p0[0].y + p0[1].y) + (p0[2].y + p0[3].y));
-      s1 = make_double2((p1[0].x + p1[1].x) + (p1[2].x + p1[3].x), (p1[0].y + p1[1].y) + (p1[2].y + p1[3].y));
-    }
-    if (kh) {
-      Ps[cg * 16 + r] = s0;
-      Ps[(cg + 8) * 16 + r] = s1;
+      if (k4 < nk4) zmma884<MODE == 0>(cr0, ci0, xa[4 * k4 * XS], fb[4 * k4 * FS]);
+      double2* pp = Ps + ((kq * 4 + blk) * 32 + lane) * 2;
+      pp[0] = make_double2(cr0[0] + cr1[0], ci0[0] + ci1[0]);
+      pp[1] = make_double2(cr0[1] + cr1[1], ci0[1] + ci1[1]);
     }
     __syncthreads();
     if (MODE == 0) {
-      if (!kh) {  // T = Y_b - (even + odd)
-        const double2 p0 = Ps[cg * 16 + r], p1 = Ps[(cg + 8) * 16 + r];
-        const double2 a0 = Xs[(b16 + cg) * 16 + r], a1 = Xs[(b16 + cg + 8) * 16 + r];
-        Ts[cg * 16 + r] = make_double2(a0.x - (s0.x + p0.x), a0.y - (s0.y + p0.y));
-        Ts[(cg + 8) * 16 + r] = make_double2(a1.x - (s1.x + p1.x), a1.y - (s1.y + p1.y));
+      if (tid < 256) {  // T = Y_b - (k-quarters 0..3 in fixed order), element (r, c) per thread
+        const int r = tid & 15, c = tid >> 4;
+        const double2* pp = Ps + (((r >> 3) + 2 * (c >> 3)) * 32 + (r & 7) * 4 + ((c & 7) >> 1)) * 2 + (c & 1);
+        const double2 p0 = pp[0], p1 = pp[256], p2 = pp[512], p3 = pp[768];
+        const double2 yv = Xs[(b16 + c) * XS + r];
+        Ts[c * XS + r] = make_double2(yv.x - ((p0.x + p1.x) + (p2.x + p3.x)), yv.y - ((p0.y + p1.y) + (p2.y + p3.y)));
       }
       __syncthreads();
-      // X_b = T L_bb^-H: X_b[r][c] = sum_{k <= c} T[r][k] conj((L_bb^-1)[c][k]);
-      // thread half kh takes column cg + 8 kh
-      const double2* Li = Lbuf + buf * 256;
-      const int c = cg + 8 * kh;
-      double2 o = zero;
-      for (int kk = 0; kk <= c; ++kk) cmac_conj(o, Ts[kk * 16 + r], Li[kk * 16 + c]);
-      Xs[(b16 + c) * 16 + r] = o;
+      if (w < 4) {  // X_b = T L_bb^-H: X_b[r][c] = sum_k T[r][k] conj((L_bb^-1)[c][k]) (zero for k > c)
+        const double2* Li = Lbuf + buf * 16 * FS;
+        double cr[4][2] = {}, ci[4][2] = {};  // one accumulator pair per k4 step: no DMMA chain
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4)
+          zmma884<true>(cr[k4], ci[k4], Ts[(4 * k4 + t) * XS + rb * 8 + gq], Li[(4 * k4 + t) * FS + cb * 8 + gq]);
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          Xs[(b16 + cb * 8 + 2 * t + e) * XS + rb * 8 + gq] =
+              make_double2((cr[0][e] + cr[1][e]) + (cr[2][e] + cr[3][e]), (ci[0][e] + ci[1][e]) + (ci[2][e] + ci[3][e]));
+      }
     } else {
-      // out[r][c] = -(even + odd) - sum_{k' < c} X[r][b16 + k'] G2[b16 + k'][j] + X[r][j] (1 - E_jj / 2);
-      // thread half kh takes column cg + 8 kh (reads the block's own input columns)
-      const int c = cg + 8 * kh;
-      if (!kh) {  // even-k sums through Ts (the odd ones are in Ps)
-        Ts[cg * 16 + r] = s0;
-        Ts[(cg + 8) * 16 + r] = s1;
+      // out[r][c] = X[r][j] (1 - E_jj / 2) - sum - sum_{k' < c} X[r][b16 + k'] G2[b16 + k'][j]
+      // (the block's own input columns are read before any of them is overwritten)
+      double2 o[2] = {zero, zero};
+      if (w < 4) {
+        double cr4[4][2] = {}, ci4[4][2] = {};  // one accumulator pair per k4 step: no DMMA chain
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+          const int kk = 4 * k4 + t, cc = cb * 8 + gq;
+          const double2 f = Fs[(b16 + kk) * FS + cc];
+          zmma884<false>(cr4[k4], ci4[k4], Xs[(b16 + kk) * XS + rb * 8 + gq], kk < cc ? f : zero);
+        }
+        const double cr[2] = {(cr4[0][0] + cr4[1][0]) + (cr4[2][0] + cr4[3][0]),
+                              (cr4[0][1] + cr4[1][1]) + (cr4[2][1] + cr4[3][1])};
+        const double ci[2] = {(ci4[0][0] + ci4[1][0]) + (ci4[2][0] + ci4[3][0]),
+                              (ci4[0][1] + ci4[1][1]) + (ci4[2][1] + ci4[3][1])};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = rb * 8 + gq, c = cb * 8 + 2 * t + e;
+          const double2* pp = Ps + (blk * 32 + lane) * 2 + e;
+          const double2 p0 = pp[0], p1 = pp[256], p2 = pp[512], p3 = pp[768];
+          const double2 xj = Xs[(b16 + c) * XS + r];
+          const double mjj = 1.0 - 0.5 * (Fs[(b16 + c) * FS + c].x - 1.0);
+          o[e] = make_double2(xj.x * mjj - (((p0.x + p1.x) + (p2.x + p3.x)) + cr[e]),
+                              xj.y * mjj - (((p0.y + p1.y) + (p2.y + p3.y)) + ci[e]));
+        }
       }
       __syncthreads();
-      const double2 ev = Ts[c * 16 + r], od = Ps[c * 16 + r];
-      double2 d = zero;
-      for (int kk = 0; kk < c; ++kk) cmac(d, Xs[(b16 + kk) * 16 + r], Fs[(b16 + kk) * 17 + c]);
-      const double2 xj = Xs[(b16 + c) * 16 + r];
-      const double mjj = 1.0 - 0.5 * (Fs[(b16 + c) * 17 + c].x - 1.0);
-      const double2 o = make_double2(xj.x * mjj - ((ev.x + od.x) + d.x), xj.y * mjj - ((ev.y + od.y) + d.y));
-      __syncthreads();  // every thread has read the block's own input columns
-      Xs[(b16 + c) * 16 + r] = o;
+      if (w < 4) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) Xs[(b16 + cb * 8 + 2 * t + e) * XS + rb * 8 + gq] = o[e];
+      }
     }
     __syncthreads();  // this step's buffers are free for the prefetch after next; its Xs columns are final
   }
   for (int idx = tid; idx < np * 16; idx += PK_THREADS) {
     const int c = idx >> 4, rr = idx & 15;
-    if (c < n && r0 + rr < m) y[(long long)c * ld + r0 + rr] = Xs[idx];
+    if (c < n && r0 + rr < m) y[(long long)c * ld + r0 + rr] = Xs[c * XS + rr];
   }
   if (MODE == 1) {
     // statistics of E = G2 - I, column j by CTA j % grid (max is exact: order-free)
@@ -244,15 +266,15 @@ __global__ void __launch_bounds__(PK_THREADS) panel_right_kernel(double2* y, lon
         emax = (a > emax || a != a) ? a : emax;
       }
       for (int o = 16; o > 0; o >>= 1) {
-        const double t = __shfl_down_sync(0xffffffffu, emax, o);
-        emax = (t > emax || t != t) ? t : emax;
+        const double tt = __shfl_down_sync(0xffffffffu, emax, o);
+        emax = (tt > emax || tt != tt) ? tt : emax;
       }
       __syncthreads();
       if ((tid & 31) == 0) red[tid >> 5] = emax;
       __syncthreads();
       if (tid == 0) {
         double mx = 0.0;
-        for (int w = 0; w < PK_THREADS / 32; ++w) mx = (red[w] > mx || red[w] != red[w]) ? red[w] : mx;
+        for (int q = 0; q < PK_THREADS / 32; ++q) mx = (red[q] > mx || red[q] != red[q]) ? red[q] : mx;
         // non-negative doubles and NaNs order like their bit patterns
         atomicMax(reinterpret_cast<unsigned long long*>(eps),
                   (unsigned long long)__double_as_longlong(fabs(mx)));
