@@ -541,11 +541,13 @@ def _workspace(dev, n, blk, nev):
     if ws is None:
         if len(_WORKSPACES) >= 4:  # bound the cache: drop the oldest shape
             _WORKSPACES.pop(next(iter(_WORKSPACES)))
+        # (Ritz values | residuals) as the halves of one buffer: the native
+        # loop then reads both back in one copy per pass
+        rr = torch.empty(2 * blk, dtype=torch.float64, device=dev)
         ws = _WORKSPACES[key] = (
             [fblock(n, blk, dev), fblock(n, blk, dev)], fblock(n, blk, dev), fblock(n, blk, dev),
             fblock(n, max(nev, 1), dev), fblock(blk, blk, dev), fblock(max(nev, 1), blk, dev),
-            torch.empty(blk, dtype=torch.float64, device=dev),
-            torch.empty(blk, dtype=torch.float64, device=dev),
+            rr[:blk], rr[blk:],
             torch.empty(blk, dtype=torch.int32, device=dev))
     return ws
 

@@ -49,6 +49,7 @@ struct chfsi_ctx {
   size_t qr_pinned_bytes = 0;
   bool qr_pending = false;
   int qr_pending_n = 0;
+  unsigned* red_counter = nullptr;  // ticket word of the single-launch reductions (zero between launches)
   double2* panel_linv = nullptr;  // inverted diagonal blocks of the Cholesky-QR factor (panel_kernels.cu)
 };
 

@@ -131,6 +131,41 @@ __global__ void reduce_final_kernel(const double* __restrict__ partial, int np, 
 
 __global__ void sqrt_scalar_kernel(double* x) { *x = sqrt(*x); }
 
+// dst = src and *out = ||src||_2 in ONE launch (the Cholesky-QR's backup copy
+// and Frobenius norm): every block copies its grid-stride slice and leaves
+// its partial sum of squares; the block that takes the last ticket adds the
+// partials in block order (fixed: bitwise reproducible) and re-arms the counter.
+__global__ void __launch_bounds__(kRedThreads) copy_norm2_kernel(const double2* __restrict__ src,
+                                                                 double2* __restrict__ dst, long long n,
+                                                                 double* __restrict__ partial,
+                                                                 unsigned* counter, double* out) {
+  __shared__ double sh[32];
+  __shared__ bool last;
+  double acc = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double2 a = src[i];
+    dst[i] = a;
+    acc = fma(a.x, a.x, fma(a.y, a.y, acc));
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = acc;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double tot = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) tot += __ldcg(partial + i);
+  tot = block_sum(tot, sh);
+  if (threadIdx.x == 0) {
+    *out = sqrt(tot);
+    *counter = 0u;
+  }
+}
+
 // out[j] = V[:,j]^H r, one block per column
 __global__ void colsdot_kernel(const double2* __restrict__ v, long long ldv, int n,
                                const double2* __restrict__ r, double2* __restrict__ out,
@@ -506,6 +541,13 @@ cudaError_t norm2_launch(const double2* x, long long n, double* partial, double*
   reduce_partial_kernel<1><<<kRedBlocks, kRedThreads, 0, s>>>(x, nullptr, n, partial, done);
   note_launch();
   reduce_final_kernel<1><<<1, 1024, 0, s>>>(partial, kRedBlocks, out, done);
+  return cudaGetLastError();
+}
+
+cudaError_t copy_norm2_launch(const double2* src, double2* dst, long long n, double* partial,
+                              unsigned* counter, double* out, cudaStream_t s) {
+  note_launch();
+  copy_norm2_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(src, dst, n, partial, counter, out);
   return cudaGetLastError();
 }
 

@@ -116,6 +116,8 @@ int chfsi_ctx_create(int device, chfsi_ctx** out) {
   CK_CUDA(cudaMalloc(&ctx->scalars, 16 * sizeof(double)));
   CK_CUDA(cudaMalloc(&ctx->dinfo, 4 * sizeof(int)));
   CK_CUDA(cudaMalloc(&ctx->lstate, sizeof(LanczosState)));
+  CK_CUDA(cudaMalloc(&ctx->red_counter, sizeof(unsigned)));
+  CK_CUDA(cudaMemset(ctx->red_counter, 0, sizeof(unsigned)));
   // K1 stream-K scratch: partial tiles and ready flags for every resident CTA
   ctx->step_ws.max_grid = chfsi::kNumSMs * 4;
   CK_CUDA(cudaMalloc(&ctx->step_ws.partials,
@@ -143,6 +145,7 @@ int chfsi_ctx_destroy(chfsi_ctx* ctx) {
   cudaFree(ctx->dinfo);
   cudaFree(ctx->lstate);
   cudaFree(ctx->panel_linv);
+  cudaFree(ctx->red_counter);
   cudaFree(ctx->step_ws.partials);
   cudaFree(ctx->step_ws.flags);
   if (ctx->aux_stream) {
@@ -868,8 +871,7 @@ int chfsi_qr_orthonormalize_z(chfsi_ctx* ctx, int m, int n, void* Y, long long l
   double* fro = racc + n;
   double* rlast = racc + n + 1;
   double2* tmp = reinterpret_cast<double2*>(racc + 2 * (size_t)n + 4);  // m x n (linearised pass 2)
-  CK_CUDA(cudaMemcpyAsync(backup, y, blk, cudaMemcpyDeviceToDevice, s));
-  CK_CUDA(chfsi::norm2_launch(y, (long long)m * n, ctx->partial, fro, nullptr, s));
+  CK_CUDA(chfsi::copy_norm2_launch(y, backup, (long long)m * n, ctx->partial, ctx->red_counter, fro, s));
   if (ctx->qr_mode != 1) {  // 0: Cholesky-QR first, 1: Householder only
     bool fallback = false;
     double dev = 0.0;
@@ -916,8 +918,7 @@ int qr_orthonormalize_deferred(chfsi_ctx* ctx, int m, int n, void* Y, long long 
   double* fro = racc + n;
   double* rlast = racc + n + 1;
   double2* tmp = reinterpret_cast<double2*>(racc + 2 * (size_t)n + 4);
-  CK_CUDA(cudaMemcpyAsync(backup, y, blk, cudaMemcpyDeviceToDevice, s));
-  CK_CUDA(chfsi::norm2_launch(y, (long long)m * n, ctx->partial, fro, nullptr, s));
+  CK_CUDA(chfsi::copy_norm2_launch(y, backup, (long long)m * n, ctx->partial, ctx->red_counter, fro, s));
   bool fallback = false, lin_reject = false;
   double dev = 0.0;
   return qr_cholqr(ctx, m, n, y, g, racc, rlast, fro, 2, false, &fallback, &dev, true,

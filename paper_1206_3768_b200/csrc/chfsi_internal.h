@@ -88,6 +88,9 @@ cudaError_t dot_re_launch(const double2* x, const double2* y, int n, double* par
                           const int* done, cudaStream_t s);
 cudaError_t norm2_launch(const double2* x, long long n, double* partial, double* out,
                          const int* done, cudaStream_t s);
+// dst = src and *out = ||src||_2 in one launch (counter: a zeroed device word the kernel re-arms)
+cudaError_t copy_norm2_launch(const double2* src, double2* dst, long long n, double* partial,
+                              unsigned* counter, double* out, cudaStream_t s);
 // out[j] = x_j^H r for columns j < ncols of col-major V (ld).
 cudaError_t colsdot_launch(const double2* v, long long ldv, int n, int ncols, const double2* r,
                            double2* out, const int* done, cudaStream_t s);

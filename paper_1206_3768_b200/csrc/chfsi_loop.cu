@@ -298,6 +298,20 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
          "adaptive degree needs degs, perm_d and 1 <= deg_min <= deg");
   // pinned staging: [ritz | res] readback, then the adaptive column order
   CK(chfsi::ensure_pinned(ctx, 2 * (size_t)L->blk * sizeof(double) + (size_t)L->blk * sizeof(int)));
+  // (ritz | res) readback: ONE copy when the two device arrays are the halves
+  // of one 2 blk buffer (res_d == ritz_d + blk; the Python workspace), else two
+  const bool packed = static_cast<double*>(L->res_d) == static_cast<double*>(L->ritz_d) + L->blk;
+  auto readback = [&](double* host, int width) -> int {
+    if (packed) {
+      CK_CUDA(cudaMemcpyAsync(host, L->ritz_d, (size_t)(L->blk + width) * sizeof(double),
+                              cudaMemcpyDeviceToHost, s));
+      return CHFSI_OK;
+    }
+    CK_CUDA(cudaMemcpyAsync(host, L->ritz_d, (size_t)width * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK_CUDA(cudaMemcpyAsync(host + width, L->res_d, (size_t)width * sizeof(double),
+                            cudaMemcpyDeviceToHost, s));
+    return CHFSI_OK;
+  };
   bool have_degs = false;
   std::vector<int> dtmp, order;
   // H * (next panel) from the previous pass's Rayleigh-Ritz: hp_rot columns
@@ -394,9 +408,7 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
     L->residual_check_matvecs += width;
     L->matvecs += width;
     double* host = static_cast<double*>(ctx->pinned);  // (re-read: RR may have grown it)
-    CK_CUDA(cudaMemcpyAsync(host, L->ritz_d, (size_t)width * sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK_CUDA(cudaMemcpyAsync(host + width, L->res_d, (size_t)width * sizeof(double),
-                            cudaMemcpyDeviceToHost, s));
+    CK(readback(host, width));
     CK_CUDA(cudaStreamSynchronize(s));
     if (spec) {  // the speculative QR's acceptance test (its inputs are on the host now)
       bool accept = false;
@@ -408,19 +420,17 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
         CK(rayleigh_ritz(ctx, L, result, rot_p, width, eig_tol, &used_fast));
         L->rr_fast_eigs += used_fast;
         host = static_cast<double*>(ctx->pinned);
-        CK_CUDA(cudaMemcpyAsync(host, L->ritz_d, (size_t)width * sizeof(double),
-                                cudaMemcpyDeviceToHost, s));
-        CK_CUDA(cudaMemcpyAsync(host + width, L->res_d, (size_t)width * sizeof(double),
-                                cudaMemcpyDeviceToHost, s));
+        CK(readback(host, width));
         CK_CUDA(cudaStreamSynchronize(s));
         L->qr_redone += 1;
       }
     }
     pending = ev;
+    double* hres = host + (packed ? L->blk : width);
     if (dist)  // summed squares of the local row norms
-      for (int j = 0; j < width; ++j) host[width + j] = std::sqrt(host[width + j]);
+      for (int j = 0; j < width; ++j) hres[j] = std::sqrt(hres[j]);
     const double* ritz = host;
-    const double* res = host + width;
+    const double* res = hres;
     for (int j = 0; j < width; ++j) {
       L->ritz[j] = ritz[j];
       L->res[j] = res[j];
