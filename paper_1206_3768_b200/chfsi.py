@@ -563,8 +563,35 @@ def _safe_window(scale_ref, a, b):
 
 # ----------------------------------------------------------------- solver ---
 
+@dataclass
+class WarmLanczos:
+    """A warm start's Lanczos bound estimate computed ahead of the solve
+    (`warm_lanczos`): the generator (already past the q0 draw, so later
+    draws continue the reference's stream) and the estimate."""
+    rng: np.random.Generator
+    ritz: np.ndarray
+    beta_last: float
+    steps: int
+
+
+def warm_lanczos(h, seed):
+    """The spectral-bound estimate of a warm start (chfsi.py:301-305 as called
+    from chfsi.py:309-316: ten Lanczos steps from a fresh q0) on torch's
+    current stream, ahead of the solve. Returns None on any failure (the
+    solve then computes it itself, after the pencil's validation)."""
+    try:
+        rng = np.random.default_rng(seed)
+        op = Operator.wrap(h)
+        ritz, beta_last, steps = _lanczos_estimates(op, min(10, op.n), rng)
+        if not (np.isfinite(ritz).all() and np.isfinite(beta_last)):
+            return None
+        return WarmLanczos(rng=rng, ritz=ritz, beta_last=float(beta_last), steps=int(steps))
+    except Exception:  # noqa: BLE001  (e.g. a pencil that fails validation: reported by the solve path)
+        return None
+
+
 def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None, _hooks=None, _sync=True,
-                _out=None):
+                _out=None, _warm=None):
     """Compute the ``cfg.nev`` lowest eigenpairs of the Hermitian ``h``
     (chfsi.py:274-384). ``h`` may be a numpy array (uploaded once) or a CUDA
     tensor in either row- or column-major layout (used in place).
@@ -620,7 +647,10 @@ def chfsi_solve(h, cfg, guess=None, rng=None, label=1, *, shard=None, _hooks=Non
         shape = tuple(gv.shape)
         if shape not in ((n, blk), (rows, blk)):
             raise ValueError(f"guess block must be {n}x{blk}, got {shape}")
-        ritz, beta_last, steps = _lanczos_estimates(op, min(10, n), rng, comm=comm)
+        if _warm is not None and comm is None:  # estimated ahead (sequence driver), same rng stream
+            ritz, beta_last, steps = _warm.ritz, _warm.beta_last, _warm.steps
+        else:
+            ritz, beta_last, steps = _lanczos_estimates(op, min(10, n), rng, comm=comm)
         b_up = float(ritz[-1] + beta_last)
         window = _safe_window(guess.lambda1, guess.lambda_blk_plus_1, b_up)
         gv = to_fblock(gv)

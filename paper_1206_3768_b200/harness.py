@@ -36,7 +36,7 @@ import numpy as np
 import torch
 
 from ._device import array_output, to_device_matrix
-from .chfsi import ChfsiConfig, ChfsiGuess, PrefetchedStart, chfsi_solve
+from .chfsi import ChfsiConfig, ChfsiGuess, PrefetchedStart, WarmLanczos, chfsi_solve, warm_lanczos
 from .linalg import hermitian_eig
 from .reduction import EigenPencil, EigenSolution, back_transform, stage_standard, to_standard
 
@@ -146,15 +146,15 @@ class _StagingSlots:
     per-stream allocator pools otherwise left freed pairs unusable by the
     next staging (OOM with the default bench warm-ups)."""
 
-    def __init__(self, n, device):
+    def __init__(self, n, device, count=2):
         self.pairs = [(torch.empty((n, n), dtype=torch.complex128, device=device),
                        torch.empty((n, n), dtype=torch.complex128, device=device))
-                      for _ in range(2)]
+                      for _ in range(count)]
         self.k = 0
 
     def take(self, side):
         pair = self.pairs[self.k]
-        self.k ^= 1
+        self.k = (self.k + 1) % len(self.pairs)
         for t in pair:
             t.record_stream(side)
         return pair
@@ -172,7 +172,7 @@ def _item_n(item):
     return int(a.shape[0])
 
 
-def _stage(item, side, ready=None, slot=None):
+def _stage(item, side, ready=None, slot=None, warm_seed=None):
     """Upload, validate and reduce one pencil on the side stream without any
     host synchronisation (the validation results land in page-locked memory
     and are checked when the problem is about to be solved, raising the
@@ -182,7 +182,14 @@ def _stage(item, side, ready=None, slot=None):
     ``ready`` is an event recorded on the caller's stream right after the
     item was produced: a lazy device generator queues the work that writes
     A and B on that stream inside ``next()``, so the side stream must wait
-    for it before reading them."""
+    for it before reading them.
+
+    ``warm_seed`` (worker thread only: it blocks until the side stream gets
+    there): also run the problem's warm-start Lanczos bound estimate on the
+    side stream right behind its reduction — it needs only H, not the
+    previous solve — so the solve starts its filter at once instead of
+    spending ~0.6 ms of host round trips (q0 upload, 10 Lanczos steps, the
+    tridiagonal eigenvalues on the host) with the main stream idle."""
     with torch.cuda.stream(side):
         if ready is not None:
             side.wait_event(ready)
@@ -198,7 +205,8 @@ def _stage(item, side, ready=None, slot=None):
             pencil, sp, checks = stage_standard(a, b, label, out=slot)
         ev = torch.cuda.Event()
         ev.record(side)
-    return pencil, sp, ev, checks
+        warm = warm_lanczos(sp.h, warm_seed) if warm_seed is not None else None
+    return pencil, sp, ev, checks, warm
 
 
 class _OutputArena:
@@ -342,6 +350,10 @@ def solve_sequence(pencils, cfg, seed=0, mode="chained", keep_standard=False, on
 
 
 _PRIORITY = os.environ.get("CHFSI_STREAM_PRIORITY", "1") != "0"
+# CHFSI_WARM_AHEAD=0: the warm-start Lanczos estimate inside the solve (A/B)
+_WARM_AHEAD = os.environ.get("CHFSI_WARM_AHEAD", "1") != "0"
+# CHFSI_STAGE_DEPTH=1: stage only problem l+1 during solve l (two H/L pairs; A/B)
+_STAGE_DEPTH = int(os.environ.get("CHFSI_STAGE_DEPTH", "2"))
 # CHFSI_DRIVER_TRACE=1: (event, perf_counter) marks of the driver's host
 # timeline appended to DRIVER_TRACE (diagnostics: tools/diag/step_outliers.py)
 _TRACE_ON = os.environ.get("CHFSI_DRIVER_TRACE") == "1"
@@ -387,17 +399,34 @@ def _solve_sequence_on(pencils, cfg, seed, mode, keep_standard, on_problem, over
     it = iter(pencils)
     first = next(it, None)
     slots = None
+    # Side-stream work (staging of problems l+1.., back-transform of problem
+    # l) is ISSUED by one worker thread: its host-side launch cost (~1 ms per
+    # problem) then overlaps the solve instead of leaving the main stream
+    # idle between problems (the native loop runs without the GIL). The
+    # worker's FIFO keeps the side stream's order: stage(l+2), back(l), ...
+    # (large n: seconds per problem make the worker's ~1 ms moot, and issuing
+    # inline keeps the allocator's frees ordered as at C5's memory limit)
+    threaded = (side is not main and os.environ.get("CHFSI_SIDE_WORKER", "1") != "0"
+                and (first is None or _item_n(first) <= _BACK_SIDE_MAX_N))
+    # Staging depth: with the worker, problems l+1 AND l+2 are staged while l
+    # is solved (three H/L pairs in rotation). The side stream only gets the
+    # SM time the high-priority solver leaves, so a reduction handed over at
+    # the start of solve l finishes near its end — the short late solves of a
+    # sequence then waited 0.7-1.2 ms each for their operator, and anything
+    # queued behind the reduction (the warm-start Lanczos estimate) landed on
+    # the critical path. One problem further ahead, both are long done.
+    depth = 2 if threaded and _STAGE_DEPTH >= 2 else 1
     if first is not None:
         n0 = _item_n(first)
         if n0 > _BACK_SIDE_MAX_N:  # per call: 12.8 GB per pair at C5
             slots = _StagingSlots(n0, torch.cuda.current_device())
         else:  # kept across calls: no per-problem 2 n^2 allocations at all
-            key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream, n0)
+            key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream, n0, depth + 1)
             slots = _SLOT_CACHE.get(key)
             if slots is None:
                 if len(_SLOT_CACHE) >= 2:
                     _SLOT_CACHE.pop(next(iter(_SLOT_CACHE)))
-                slots = _SLOT_CACHE[key] = _StagingSlots(n0, torch.cuda.current_device())
+                slots = _SLOT_CACHE[key] = _StagingSlots(n0, torch.cuda.current_device(), depth + 1)
 
     def slot():
         return None if slots is None else slots.take(side)
@@ -414,16 +443,7 @@ def _solve_sequence_on(pencils, cfg, seed, mode, keep_standard, on_problem, over
         p0 = staged[0]
         prefetch = PrefetchedStart(np.random.default_rng((seed, p0.label, 0)), p0.n,
                                    cfg.resolve(p0.n)[0])
-    # Side-stream work (staging of problem l+1, back-transform of problem l)
-    # is ISSUED by one worker thread: its host-side launch cost (~1 ms per
-    # problem) then overlaps the solve instead of leaving the main stream
-    # idle between problems (the native loop runs without the GIL). The
-    # worker's FIFO keeps the side stream's order: stage(l+1), back(l), ...
     dev = torch.cuda.current_device()
-    # (large n: seconds per problem make the worker's ~1 ms moot, and issuing
-    # inline keeps the allocator's frees ordered as at C5's memory limit)
-    threaded = (side is not main and os.environ.get("CHFSI_SIDE_WORKER", "1") != "0"
-                and (staged is None or staged[0].n <= _BACK_SIDE_MAX_N))
     worker = side_worker(dev) if threaded else None
     issued = []
     # Side-stream jobs are collected here and handed to the worker only once
@@ -497,32 +517,40 @@ def _solve_sequence_on(pencils, cfg, seed, mode, keep_standard, on_problem, over
         return done
 
     _mark("first staged")
+    queue = [staged] if staged is not None else []  # staged problems, in order (at most `depth` ahead)
+    exhausted = False
     try:
-        while staged is not None:
+        while queue:
             _mark("problem top")
             t0 = time.perf_counter()
-            if not isinstance(staged, tuple):  # issued by the worker during the last solve
+            staged = queue.pop(0)
+            if not isinstance(staged, tuple):  # issued by the worker during an earlier solve
                 fut, staged = staged, staged.result()
                 fut = getattr(fut, "fut", fut)
                 if fut in issued:  # a done future holds its result: drop it, or every
                     issued.remove(fut)  # problem's H and L would live until the call ends
-            pencil, sp, ev, checks = staged
-            ev.synchronize()  # long done for l >= 2: staged while l-1 was solved
+            pencil, sp, ev, checks, warm = staged
+            ev.synchronize()  # long done for l >= 2: staged while an earlier problem was solved
             checks.raise_if_invalid()
             main.wait_event(ev)
             if side is not main:
                 for t in (sp.h, sp.cholesky_factor, pencil.a, pencil.b):
                     t.record_stream(main)
             t1 = time.perf_counter()
-            nxt = next(it, None)
-            if nxt is None:
-                staged = None
-            elif slots is not None and _item_n(nxt) != slots.pairs[0][0].shape[0]:
-                raise ValueError("all pencils of a sequence must share one dimension")
-            elif side is not main:
-                staged = later(_stage, nxt, side, produced(), slot())
-            else:
-                staged = _stage(nxt, side, None, slot())
+            while len(queue) < depth and not exhausted:
+                nxt = next(it, None)
+                if nxt is None:
+                    exhausted = True
+                elif slots is not None and _item_n(nxt) != slots.pairs[0][0].shape[0]:
+                    raise ValueError("all pencils of a sequence must share one dimension")
+                elif side is not main:
+                    # (with the worker thread the problem's warm-start Lanczos
+                    # estimate runs ahead too; its seed is the warm start's)
+                    nlab = nxt.label if isinstance(nxt, EigenPencil) else nxt[0]
+                    wseed = (seed, nlab, 1) if worker is not None and _WARM_AHEAD else None
+                    queue.append(later(_stage, nxt, side, produced(), slot(), wseed))
+                else:
+                    queue.append(_stage(nxt, side, None, slot()))
             t_stage = time.perf_counter() - t1
             t1 = time.perf_counter()
             n = pencil.n
@@ -533,10 +561,15 @@ def _solve_sequence_on(pencils, cfg, seed, mode, keep_standard, on_problem, over
             rng = np.random.default_rng((seed, pencil.label, start))
             if prefetch is not None:  # (always problem 1: guess is None there)
                 rng, prefetch = prefetch, None
+            if guess is None or warm is None:
+                warm = None  # (cold restart: the estimate drawn for a warm start is not used)
+            else:
+                rng = warm.rng  # the same generator, already past the q0 draw
             _mark("solve start")
             out_bufs = arena.take(n, blk, cfg.nev) if arena is not None else None
             sol, rep = chfsi_solve(sp.h, cfg, guess=guess, rng=rng, label=pencil.label,
-                                   _hooks=flush if deferred else None, _sync=False, _out=out_bufs)
+                                   _hooks=flush if deferred else None, _sync=False, _out=out_bufs,
+                                   _warm=warm)
             _mark("solve end")
             t2 = time.perf_counter()
             back = None

@@ -505,3 +505,40 @@ def test_sequence_outputs_reuse_cached_blocks_without_gc(pkg):
         assert torch.cuda.memory_stats(dev)["num_device_alloc"] == allocs
     finally:
         gc.enable()
+
+
+@pytest.mark.gpu
+def test_sequence_stages_two_problems_ahead(pkg, monkeypatch):
+    """Default driver (worker thread): three H/L pairs in rotation, problems
+    l+1 and l+2 staged during solve l, the warm-start Lanczos estimate run
+    ahead on the side stream — bitwise the same results as staging depth 1
+    with the estimate inside the solve, and as the serial driver."""
+    from paper_1206_3768_b200 import harness
+
+    cfg_b = pkg.BASELINE_CONFIGS["C1"]
+    cfg = pkg.ChfsiConfig(nev=cfg_b.nev, nex=cfg_b.nex, deg=cfg_b.deg, tol=cfg_b.tol)
+    seq = list(pkg.iter_baseline_sequence(cfg_b.n, 6, seed=0))
+    taken = []
+    orig = harness._StagingSlots.take
+
+    def take(self, side):
+        pair = orig(self, side)
+        taken.append(pair[0].data_ptr())
+        return pair
+
+    monkeypatch.setattr(harness._StagingSlots, "take", take)
+    ahead = pkg.solve_sequence(seq, cfg, seed=0)
+    assert len(taken) == 6 and len(set(taken)) == 3
+    assert taken[0] == taken[3] and taken[1] == taken[4] and taken[2] == taken[5]
+    monkeypatch.setattr(harness, "_STAGE_DEPTH", 1)
+    monkeypatch.setattr(harness, "_WARM_AHEAD", False)
+    taken.clear()
+    plain = pkg.solve_sequence(seq, cfg, seed=0)
+    assert len(set(taken)) == 2
+    serial = pkg.solve_sequence(seq, cfg, seed=0, overlap=False)
+    for a, b, c in zip(ahead, plain, serial):
+        assert a.report.locked_per_loop == b.report.locked_per_loop == c.report.locked_per_loop
+        assert a.report.lanczos_matvecs == b.report.lanczos_matvecs == c.report.lanczos_matvecs
+        assert np.array_equal(a.values, b.values) and np.array_equal(a.values, c.values)
+        assert torch.equal(a.solution.vectors, b.solution.vectors)
+        assert torch.equal(a.solution.vectors, c.solution.vectors)
