@@ -634,26 +634,11 @@ int chfsi_gemm_z(chfsi_ctx* ctx, char transa, char transb, int m, int n, int k, 
   CK_ARG(valid_op(transa) && valid_op(transb), "unknown transpose flag");
   CK_ARG(m >= 0 && n >= 0 && k >= 0, "negative size");
   if (m == 0 || n == 0) return CHFSI_OK;
-  // Gram-type products C = A^H B of the loop (tall contraction, small output:
-  // the CGS coefficients, the Cholesky-QR Grams, the projected matrix) on K1
-  // itself: A's columns are the rows of "H" read conjugated through TMA, the
-  // contraction is split over every SM by the stream-K schedule and folded in
-  // fixed order (deterministic) — one launch instead of cuBLAS's Ampere-era
-  // z884gemm + splitKreduce pair. CHFSI_GRAM_K1=1 enables (experimental).
-  static const bool gram_k1 = [] {
-    const char* e = getenv("CHFSI_GRAM_K1");
-    return e && atoi(e) == 1;
-  }();
-  if (gram_k1 && transa == 'C' && transb == 'N' && alpha_re == 1.0 && alpha_im == 0.0 && beta_re == 0.0 &&
-      beta_im == 0.0 && k >= 1024 && m <= 256 && n <= 256 && A != C && B != C) {
-    const chfsi::RowShard shard{m, 0, 0, nullptr, 0};
-    chfsi::StepTiling tiling = chfsi::choose_step_tiling(k, n);
-    CK_CUDA(chfsi::cheb_step_rows_launch(static_cast<const double2*>(A), lda, /*conj=*/true,
-                                         static_cast<const double2*>(B), ldb, nullptr, 0,
-                                         static_cast<double2*>(C), ldc, k, n, 1.0, 0.0, 0.0, shard, tiling,
-                                         ctx->step_ws, ctx->stream));
-    return CHFSI_OK;
-  }
+  // (Measured and rejected, round 2: Gram-type products C = A^H B of the loop
+  // — CGS coefficients, Cholesky-QR Grams, the projected matrix — on K1's
+  // stream-K schedule, A's columns read conjugated through TMA. Correct and
+  // deterministic, but the ~20-way fixed-order fold per output tile costs
+  // more than cuBLAS's z884gemm + splitKreduce pair: C2 ortho 31 -> 39 ms.)
   const cuDoubleComplex al = make_cuDoubleComplex(alpha_re, alpha_im);
   const cuDoubleComplex be = make_cuDoubleComplex(beta_re, beta_im);
   CK_BLAS(cublasZgemm(ctx->blas, op_of(transa), op_of(transb), m, n, k, &al,
