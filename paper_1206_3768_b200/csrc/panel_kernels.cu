@@ -15,6 +15,13 @@
 //               second pass's Gram matrix G2 (linearised second pass), plus
 //               the pass's statistics (max|E|, R2 diagonal)
 //
+// (Measured and rejected: the w x w Cholesky itself as ONE hand-written CTA —
+// left-looking 16-column blocks, DMMA updates from staged L rows,
+// right-looking block-column factorisation in shared memory, fused with
+// post_potrf's work. Correct against every QR test, but one SM's worth of
+// FP64 plus ~10 serial block steps took 174 us at w = 160 against cuSOLVER
+// potrf's 71 us (level at w <= 48); C2 ortho 31 -> 35 ms. potrf stays.)
+//
 // Each CTA owns 16 rows of Y, keeps them in shared memory for the whole
 // operation (Y is read and written once), and streams the w x w factor
 // through shared memory one 16-column block at a time (L2-resident: 410 KB at
