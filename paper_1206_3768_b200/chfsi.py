@@ -447,10 +447,11 @@ class _LoopCallbacks:
         self.full = None                      # scratch of the gather fallback
         self.error = None
         self.fill_cb = FILL_CB(self._fill)
-        self.filter_cb = FILTER_CB(self._filter)
-        self.allreduce_cb = ALLREDUCE_CB(self._allreduce)
-        self.hp_cb = HP_CB(self._hp)
-        self.gather_cb = GATHER_CB(self._gather)
+        if comm is not None:  # (ctypes thunks cost ~10 us each: only the sharded loop needs these)
+            self.filter_cb = FILTER_CB(self._filter)
+            self.allreduce_cb = ALLREDUCE_CB(self._allreduce)
+            self.hp_cb = HP_CB(self._hp)
+            self.gather_cb = GATHER_CB(self._gather)
 
     def _view(self, ptr, width):
         for b in self.bufs:
