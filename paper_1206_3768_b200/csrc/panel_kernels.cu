@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(32) panel_post_potrf_kernel(const double2* g, 
 // (288 B) keep the 16-byte DMMA fragment loads bank-conflict free.
 constexpr int XS = 18, FS = 18;
 __host__ __device__ constexpr size_t panel_smem_bytes(int np) {
-  return ((size_t)np * XS + 2 * (size_t)np * FS + 1024 + 16 * XS + 2 * 16 * FS) * sizeof(double2);
+  return ((size_t)np * XS + 2 * ((size_t)np * FS + 64) + 1024 + 16 * XS + 2 * 16 * FS) * sizeof(double2);
 }
 
 // complex 8x8x4 block on DMMA: (cr, ci) += a b (CONJ_B: a conj(b)), four real products
@@ -138,16 +138,17 @@ __global__ void __launch_bounds__(PK_THREADS) panel_right_kernel(double2* y, lon
   const int t16 = (n + 15) >> 4, np = t16 * 16;
   double2* Xs = psm;                        // [np][XS]: column c, row r at c * XS + r
   double2* Fbuf = Xs + (size_t)np * XS;     // 2 x [np][FS]: factor block, k * FS + c
-  double2* Ps = Fbuf + 2 * (size_t)np * FS; // [4][4][32][2]: partial C fragments
+  double2* Ps = Fbuf + 2 * ((size_t)np * FS + 64);  // [4][4][32][2]: partial C fragments
   double2* Ts = Ps + 1024;                  // [16][XS]: T, column kk, row r at kk * XS + r
   double2* Lbuf = Ts + 16 * XS;             // 2 x [16][FS]: k * FS + c = (L_bb^-1)[c][k]
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, gq = lane >> 2, t = lane & 3;
   const int blk = w & 3, kq = w >> 2, rb = blk & 1, cb = blk >> 1;
   const int r0 = blockIdx.x * 16;
+  const int ks = np + 4;  // MODE 1: k-stride of the column-major factor block
   const double2 zero = make_double2(0.0, 0.0);
   // factor block b into buffer `buf` (asynchronous; zero fill outside the matrix)
   auto stage = [&](int b, int buf) {
-    double2* Fs = Fbuf + (size_t)buf * np * FS;
+    double2* Fs = Fbuf + (size_t)buf * (np * FS + 64);
     const int b16 = b * 16;
     if (MODE == 0) {  // Fs[k][c] = L[b16 + c][k], k < b16 (c contiguous in memory)
       for (int idx = tid; idx < b16 * 16; idx += PK_THREADS) {
@@ -157,12 +158,13 @@ __global__ void __launch_bounds__(PK_THREADS) panel_right_kernel(double2* y, lon
       }
       double2* Li = Lbuf + buf * 16 * FS;
       if (tid < 256) cp_async16(&Li[(tid >> 4) * FS + (tid & 15)], &linv[(long long)b * 256 + tid], true);
-    } else {  // Fs[k][c] = G2[k][b16 + c], k < b16 + 16 (k contiguous in memory)
+    } else {  // G2[k][b16 + c], k < b16 + 16, stored column-major (c * ks + k: k contiguous in global
+              // and shared memory, conflict-free copies; ks = 4 mod 8 keeps the fragment loads so)
       const int klen = b16 + 16;
       for (int idx = tid; idx < klen * 16; idx += PK_THREADS) {
         const int c = idx / klen, k = idx - c * klen, j = b16 + c;
         const bool ok = j < n && k < n;
-        cp_async16(&Fs[k * FS + c], &g[(long long)(ok ? j : 0) * ldg + (ok ? k : 0)], ok);
+        cp_async16(&Fs[c * ks + k], &g[(long long)(ok ? j : 0) * ldg + (ok ? k : 0)], ok);
       }
     }
   };
@@ -176,7 +178,7 @@ __global__ void __launch_bounds__(PK_THREADS) panel_right_kernel(double2* y, lon
   cp_async_commit();
   for (int it = 0; it < t16; ++it) {
     const int b = first + it * step, b16 = b * 16, buf = it & 1;
-    const double2* Fs = Fbuf + (size_t)buf * np * FS;
+    const double2* Fs = Fbuf + (size_t)buf * (np * FS + 64);
     if (it + 1 < t16) stage(b + step, buf ^ 1);  // (that buffer's readers finished in step it - 1)
     cp_async_commit();
     cp_async_wait<1>();
@@ -186,28 +188,35 @@ __global__ void __launch_bounds__(PK_THREADS) panel_right_kernel(double2* y, lon
     {
       double cr0[2] = {0.0, 0.0}, ci0[2] = {0.0, 0.0}, cr1[2] = {0.0, 0.0}, ci1[2] = {0.0, 0.0};
       const double2* xa = Xs + t * XS + rb * 8 + gq;
-      const double2* fb = Fs + t * FS + cb * 8 + gq;
+      const double2* fb = MODE == 0 ? Fs + t * FS + cb * 8 + gq : Fs + (cb * 8 + gq) * ks + t;
+      const int fstep = MODE == 0 ? 4 * FS : 4;  // one k4 step in the factor block
       const int nk4 = b16 >> 2;
       int k4 = kq;
       for (; k4 + 4 < nk4; k4 += 8) {  // two steps per trip on independent accumulators
-        const double2 a0 = xa[4 * k4 * XS], f0 = fb[4 * k4 * FS];
-        const double2 a1 = xa[4 * (k4 + 4) * XS], f1 = fb[4 * (k4 + 4) * FS];
+        const double2 a0 = xa[4 * k4 * XS], f0 = fb[k4 * fstep];
+        const double2 a1 = xa[4 * (k4 + 4) * XS], f1 = fb[(k4 + 4) * fstep];
         zmma884<MODE == 0>(cr0, ci0, a0, f0);
         zmma884<MODE == 0>(cr1, ci1, a1, f1);
       }
-      if (k4 < nk4) zmma884<MODE == 0>(cr0, ci0, xa[4 * k4 * XS], fb[4 * k4 * FS]);
+      if (k4 < nk4) zmma884<MODE == 0>(cr0, ci0, xa[4 * k4 * XS], fb[k4 * fstep]);
       double2* pp = Ps + ((kq * 4 + blk) * 32 + lane) * 2;
       pp[0] = make_double2(cr0[0] + cr1[0], ci0[0] + ci1[0]);
       pp[1] = make_double2(cr0[1] + cr1[1], ci0[1] + ci1[1]);
     }
     __syncthreads();
     if (MODE == 0) {
-      if (tid < 256) {  // T = Y_b - (k-quarters 0..3 in fixed order), element (r, c) per thread
-        const int r = tid & 15, c = tid >> 4;
-        const double2* pp = Ps + (((r >> 3) + 2 * (c >> 3)) * 32 + (r & 7) * 4 + ((c & 7) >> 1)) * 2 + (c & 1);
-        const double2 p0 = pp[0], p1 = pp[256], p2 = pp[512], p3 = pp[768];
-        const double2 yv = Xs[(b16 + c) * XS + r];
-        Ts[c * XS + r] = make_double2(yv.x - ((p0.x + p1.x) + (p2.x + p3.x)), yv.y - ((p0.y + p1.y) + (p2.y + p3.y)));
+      if (tid < 128) {  // T = Y_b - (k-quarters 0..3 in fixed order); thread = (block, lane) of the
+                        // C fragments, both of its elements: consecutive lanes read consecutive 32 bytes
+        const int fb = tid >> 5, fl = tid & 31;
+        const double2* pp = Ps + (fb * 32 + fl) * 2;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = (fb & 1) * 8 + (fl >> 2), c = (fb >> 1) * 8 + 2 * (fl & 3) + e;
+          const double2 p0 = pp[e], p1 = pp[256 + e], p2 = pp[512 + e], p3 = pp[768 + e];
+          const double2 yv = Xs[(b16 + c) * XS + r];
+          Ts[c * XS + r] =
+              make_double2(yv.x - ((p0.x + p1.x) + (p2.x + p3.x)), yv.y - ((p0.y + p1.y) + (p2.y + p3.y)));
+        }
       }
       __syncthreads();
       if (w < 4) {  // X_b = T L_bb^-H: X_b[r][c] = sum_k T[r][k] conj((L_bb^-1)[c][k]) (zero for k > c)
@@ -230,7 +239,7 @@ __global__ void __launch_bounds__(PK_THREADS) panel_right_kernel(double2* y, lon
 #pragma unroll
         for (int k4 = 0; k4 < 4; ++k4) {
           const int kk = 4 * k4 + t, cc = cb * 8 + gq;
-          const double2 f = Fs[(b16 + kk) * FS + cc];
+          const double2 f = Fs[cc * ks + b16 + kk];
           zmma884<false>(cr4[k4], ci4[k4], Xs[(b16 + kk) * XS + rb * 8 + gq], kk < cc ? f : zero);
         }
         const double cr[2] = {(cr4[0][0] + cr4[1][0]) + (cr4[2][0] + cr4[3][0]),
@@ -243,7 +252,7 @@ __global__ void __launch_bounds__(PK_THREADS) panel_right_kernel(double2* y, lon
           const double2* pp = Ps + (blk * 32 + lane) * 2 + e;
           const double2 p0 = pp[0], p1 = pp[256], p2 = pp[512], p3 = pp[768];
           const double2 xj = Xs[(b16 + c) * XS + r];
-          const double mjj = 1.0 - 0.5 * (Fs[(b16 + c) * FS + c].x - 1.0);
+          const double mjj = 1.0 - 0.5 * (Fs[c * ks + b16 + c].x - 1.0);
           o[e] = make_double2(xj.x * mjj - (((p0.x + p1.x) + (p2.x + p3.x)) + cr[e]),
                               xj.y * mjj - (((p0.y + p1.y) + (p2.y + p3.y)) + ci[e]));
         }
