@@ -49,6 +49,8 @@ struct chfsi_ctx {
   size_t qr_pinned_bytes = 0;
   bool qr_pending = false;
   int qr_pending_n = 0;
+  double* nd_pinned = nullptr;  // page-locked status of the speculative near-diagonal eigensolver
+  bool nd_pending = false;
   unsigned* red_counter = nullptr;  // ticket word of the single-launch reductions (zero between launches)
   double2* panel_linv = nullptr;  // inverted diagonal blocks of the Cholesky-QR factor (panel_kernels.cu)
 };
@@ -66,6 +68,15 @@ int ensure_pinned(chfsi_ctx* ctx, size_t bytes);
 int qr_orthonormalize_deferred(chfsi_ctx* ctx, int m, int n, void* Y, long long ldy);
 int qr_deferred_verdict(chfsi_ctx* ctx, bool* accept);
 int qr_deferred_restore(chfsi_ctx* ctx, int m, int n, void* Y);
+// Speculative Rayleigh-Ritz eigensolver (native loop): the cooperative
+// near-diagonal solver is queued WITHOUT waiting for its verdict — the
+// caller goes on queuing the rotations and residual norms as if it had
+// succeeded and judges it (`heev_rr_verdict`) after the pass's own
+// synchronisation. On failure A is untouched (the solver's contract) and
+// the caller redoes the step with zheevd. *queued = false when the solver
+// does not apply (width, tolerance, CHFSI_ND_PERSIST=0): nothing was done.
+int heev_rr_speculative(chfsi_ctx* ctx, int n, void* A, long long lda, double* w, double tol, bool* queued);
+int heev_rr_verdict(chfsi_ctx* ctx, bool* done);
 // chfsi_filter_z with an optional known first product hy0 = H y0 (ld ldhy0):
 // the first recurrence step is then elementwise (the native loop passes the
 // previous Rayleigh-Ritz's rotated H P)

@@ -160,6 +160,7 @@ int chfsi_ctx_destroy(chfsi_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->qr_pinned) cudaFreeHost(ctx->qr_pinned);
+  if (ctx->nd_pinned) cudaFreeHost(ctx->nd_pinned);
   delete ctx;
   return CHFSI_OK;
 }
@@ -995,39 +996,57 @@ namespace {
 // per NS iteration). *done = false (A untouched) when G is not in that regime
 // (r > 0.5, CHFSI_RR_BAIL), does not converge within kMaxSteps, or W is not unitary to
 // rounding (defect at the last NS input > 1e-8): the caller uses zheevd.
+double nd_bail() {  // regime bound on max|G_ij| / |d_j - d_i| (tuning)
+  static const double bail = [] {
+    const char* e = getenv("CHFSI_RR_BAIL");
+    return e ? atof(e) : 0.5;  // measured: 0.1 -> 0.5 turns 5 of the cold C2 start's 10 zheevd calls into fast ones
+  }();
+  return bail;
+}
+
+bool nd_persist_enabled() {
+  static const bool persist = [] {
+    const char* e = getenv("CHFSI_ND_PERSIST");
+    return !(e && atoi(e) == 0);
+  }();
+  return persist;
+}
+
+// The cooperative near-diagonal eigensolver (nd_persist.cu) queued on the
+// stream with its 4-double status copied to page-locked `hs` — no host
+// synchronisation here.
+int nd_persist_queue(chfsi_ctx* ctx, int n, double2* a, long long lda, double* w, double tol, double* hs) {
+  cudaStream_t s = ctx->stream;
+  const size_t pneed = chfsi::nd_persist_ws_bytes(n);
+  if (pneed > ctx->eig_ws_bytes) {
+    CK_CUDA(cudaStreamSynchronize(s));
+    if (ctx->eig_ws) CK_CUDA(cudaFree(ctx->eig_ws));
+    ctx->eig_ws = nullptr;
+    ctx->eig_ws_bytes = 0;
+    CK_CUDA(cudaMalloc(&ctx->eig_ws, pneed));
+    ctx->eig_ws_bytes = pneed;
+  }
+  double* st_dev = ctx->scalars + 12;  // 4 doubles of the context's scalar scratch
+  CK_CUDA(chfsi::nd_persist_launch(a, lda, n, w, tol, nd_bail(), ctx->eig_ws, st_dev, s));
+  CK_CUDA(cudaMemcpyAsync(hs, st_dev, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  return CHFSI_OK;
+}
+
 int heev_near_diag(chfsi_ctx* ctx, int n, double2* a, long long lda, double* w, double tol,
                    bool* done) {
   *done = false;
   cudaStream_t s = ctx->stream;
   const size_t mat = (size_t)n * n * sizeof(double2);
   constexpr int kMaxSteps = 6;
-  static const double bail = [] {  // regime bound on max|G_ij| / |d_j - d_i| (tuning)
-    const char* e = getenv("CHFSI_RR_BAIL");
-    return e ? atof(e) : 0.5;  // measured: 0.1 -> 0.5 turns 5 of the cold C2 start's 10 zheevd calls into fast ones
-  }();
+  const double bail = nd_bail();
   constexpr int kSlots = 4 * (kMaxSteps + 1) + kMaxSteps;  // build stats + NS defects
   // Panel widths: the whole iteration as one cooperative kernel (nd_persist.cu;
   // CHFSI_ND_PERSIST=0 keeps the multi-kernel version below) — one host
   // round trip per call instead of one per step, no per-step launches.
-  static const bool persist = [] {
-    const char* e = getenv("CHFSI_ND_PERSIST");
-    return !(e && atoi(e) == 0);
-  }();
-  if (persist && n <= chfsi::kNdPersistMaxN) {
-    const size_t pneed = chfsi::nd_persist_ws_bytes(n);
-    if (pneed > ctx->eig_ws_bytes) {
-      CK_CUDA(cudaStreamSynchronize(s));
-      if (ctx->eig_ws) CK_CUDA(cudaFree(ctx->eig_ws));
-      ctx->eig_ws = nullptr;
-      ctx->eig_ws_bytes = 0;
-      CK_CUDA(cudaMalloc(&ctx->eig_ws, pneed));
-      ctx->eig_ws_bytes = pneed;
-    }
+  if (nd_persist_enabled() && n <= chfsi::kNdPersistMaxN) {
     CK(chfsi::ensure_pinned(ctx, 4 * sizeof(double)));
-    double* st_dev = ctx->scalars + 12;  // 4 doubles of the context's scalar scratch
-    CK_CUDA(chfsi::nd_persist_launch(a, lda, n, w, tol, bail, ctx->eig_ws, st_dev, s));
     double* hs = static_cast<double*>(ctx->pinned);
-    CK_CUDA(cudaMemcpyAsync(hs, st_dev, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(nd_persist_queue(ctx, n, a, lda, w, tol, hs));
     CK_CUDA(cudaStreamSynchronize(s));
     static const bool dbgp = getenv("CHFSI_RR_DEBUG") != nullptr;
     if (dbgp)
@@ -1109,6 +1128,27 @@ int heev_near_diag(chfsi_ctx* ctx, int n, double2* a, long long lda, double* w, 
 }
 
 }  // namespace
+
+namespace chfsi {
+
+int heev_rr_speculative(chfsi_ctx* ctx, int n, void* A, long long lda, double* w, double tol, bool* queued) {
+  *queued = false;
+  if (!(tol > 0.0) || n < 2 || n > kNdPersistMaxN || !nd_persist_enabled()) return CHFSI_OK;
+  if (!ctx->nd_pinned) CK_CUDA(cudaMallocHost(&ctx->nd_pinned, 4 * sizeof(double)));
+  CK(nd_persist_queue(ctx, n, static_cast<double2*>(A), lda, w, tol, ctx->nd_pinned));
+  ctx->nd_pending = true;
+  *queued = true;
+  return CHFSI_OK;
+}
+
+int heev_rr_verdict(chfsi_ctx* ctx, bool* done) {
+  CK_ARG(ctx && done && ctx->nd_pending, "no speculative eigensolver pending");
+  ctx->nd_pending = false;
+  *done = ctx->nd_pinned[0] == 1.0;
+  return CHFSI_OK;
+}
+
+}  // namespace chfsi
 
 namespace {
 

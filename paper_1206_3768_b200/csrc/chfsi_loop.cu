@@ -14,6 +14,7 @@
 // stream synchronisation per pass, plus the near-diagonal eigensolver's
 // regime checks). Device phase times are taken with events on the stream.
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <utility>
 #include <cmath>
@@ -140,15 +141,46 @@ int rotate_pair(chfsi_ctx* ctx, int n, int w, const void* q, const void* hp, con
   return CHFSI_OK;
 }
 
+// CHFSI_RR_DEFER=0: the near-diagonal eigensolver's verdict is awaited inside
+// Rayleigh-Ritz (one host round trip per pass more) instead of at the pass's end
+bool rr_defer_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CHFSI_RR_DEFER");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
+// `speculate`: the near-diagonal eigensolver is queued without waiting for
+// its verdict and the rotations / residual norms follow at once (*pending =
+// true: the caller judges it after the pass's synchronisation and calls
+// rayleigh_ritz_redo when it failed). Measured before: the verdict's round
+// trip left the stream idle 26-41 us per pass until the rotation started.
 int rayleigh_ritz(chfsi_ctx* ctx, chfsi_loop* L, const void* q, void* rot_p, int width, double eig_tol,
-                  int* used_fast) {
+                  int* used_fast, bool speculate = false, bool* pending = nullptr) {
   const int n = L->n;
   const long long ldg = L->blk;
+  if (pending) *pending = false;
   CK(chfsi_cheb_step_z(ctx, n, width, L->H, L->ldh, L->conj_h, q, n, nullptr, 0, L->hp, n, 1.0, 0.0,
                        0.0));
   CK(chfsi_gemm_z(ctx, 'C', 'N', width, width, n, 1.0, 0.0, q, n, L->hp, n, 0.0, 0.0, L->g, ldg));
   CK(chfsi_symmetrize_z(ctx, width, L->g, ldg));
-  CK(chfsi_heev_rr_z(ctx, width, L->g, ldg, L->ritz_d, eig_tol, used_fast));
+  bool queued = false;
+  if (speculate && pending)
+    CK(chfsi::heev_rr_speculative(ctx, width, L->g, ldg, L->ritz_d, eig_tol, &queued));
+  if (queued) *pending = true;
+  else CK(chfsi_heev_rr_z(ctx, width, L->g, ldg, L->ritz_d, eig_tol, used_fast));
+  CK(rotate_pair(ctx, n, width, q, L->hp, L->g, ldg, rot_p, L->hp_rot));
+  CK(chfsi_colnorm_residual_z(ctx, n, width, L->hp_rot, n, rot_p, n, L->ritz_d, L->res_d));
+  return CHFSI_OK;
+}
+
+// The speculative eigensolver failed (G is untouched, H P is still in L->hp):
+// zheevd, then the rotations and residual norms again.
+int rayleigh_ritz_redo(chfsi_ctx* ctx, chfsi_loop* L, const void* q, void* rot_p, int width) {
+  const int n = L->n;
+  const long long ldg = L->blk;
+  CK(chfsi_heevd_z(ctx, width, L->g, ldg, L->ritz_d));
   CK(rotate_pair(ctx, n, width, q, L->hp, L->g, ldg, rot_p, L->hp_rot));
   CK(chfsi_colnorm_residual_z(ctx, n, width, L->hp_rot, n, rot_p, n, L->ritz_d, L->res_d));
   return CHFSI_OK;
@@ -385,10 +417,12 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
     const double eig_tol = L->rr_fast_tol > 0.0 ? L->rr_fast_tol : 0.0;
     int used_fast = 0;
     bool spec_redo = false;  // the speculative QR must be judged (and redone) now
+    bool nd_pending = false; // the near-diagonal eigensolver's verdict is still out
     if (dist) {
       CK(rayleigh_ritz_dist(ctx, L, result, rot_p, width, eig_tol, &used_fast));
     } else {
-      const int rc = rayleigh_ritz(ctx, L, result, rot_p, width, eig_tol, &used_fast);
+      const int rc = rayleigh_ritz(ctx, L, result, rot_p, width, eig_tol, &used_fast,
+                                   rr_defer_enabled(), &nd_pending);
       if (rc != CHFSI_OK) {
         // A failed Cholesky inside the speculative QR leaves non-finite
         // panels; the eigensolver then fails before the pass's readback.
@@ -414,6 +448,11 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
       bool accept = false;
       if (!spec_redo) CK(chfsi::qr_deferred_verdict(ctx, &accept));
       if (!accept) {  // rare: redo the pass's QR and Rayleigh-Ritz on the full path
+        if (nd_pending) {  // (its input came from the rejected QR: the verdict is moot)
+          bool ignored = false;
+          CK(chfsi::heev_rr_verdict(ctx, &ignored));
+          nd_pending = false;
+        }
         CK(orthonormalize(ctx, L, result, width, 2));
         L->rr_fast_eigs -= used_fast;
         used_fast = 0;
@@ -423,6 +462,21 @@ extern "C" int chfsi_solve_loop_z(chfsi_ctx* ctx, chfsi_loop* L) {
         CK(readback(host, width));
         CK_CUDA(cudaStreamSynchronize(s));
         L->qr_redone += 1;
+      }
+    }
+    if (nd_pending) {  // the speculative eigensolver's verdict (its status is on the host now)
+      bool done = false;
+      CK(chfsi::heev_rr_verdict(ctx, &done));
+      if (done) {
+        L->rr_fast_eigs += 1;
+      } else {  // not near-diagonal: zheevd, rotations and residuals again
+        const auto t_redo = std::chrono::steady_clock::now();
+        CK(rayleigh_ritz_redo(ctx, L, result, rot_p, width));
+        host = static_cast<double*>(ctx->pinned);
+        CK(readback(host, width));
+        CK_CUDA(cudaStreamSynchronize(s));
+        // (behind the pass's event set: the stream was idle at the start, so wall time = device time)
+        L->t_rr += std::chrono::duration<double>(std::chrono::steady_clock::now() - t_redo).count();
       }
     }
     pending = ev;
