@@ -558,13 +558,14 @@ def _solve_sequence_on(pencils, cfg, seed, mode, keep_standard, on_problem, over
             if mode == "harness" and blk >= n:
                 raise ValueError(f"chfsi warm starts need blk < n (blk={blk}, n={n})")
             start = 0 if guess is None else 1
-            rng = np.random.default_rng((seed, pencil.label, start))
-            if prefetch is not None:  # (always problem 1: guess is None there)
-                rng, prefetch = prefetch, None
             if guess is None or warm is None:
                 warm = None  # (cold restart: the estimate drawn for a warm start is not used)
+            if prefetch is not None:  # (always problem 1: guess is None there)
+                rng, prefetch = prefetch, None
+            elif warm is not None:
+                rng = warm.rng  # the warm start's generator, already past the q0 draw
             else:
-                rng = warm.rng  # the same generator, already past the q0 draw
+                rng = np.random.default_rng((seed, pencil.label, start))
             _mark("solve start")
             out_bufs = arena.take(n, blk, cfg.nev) if arena is not None else None
             sol, rep = chfsi_solve(sp.h, cfg, guess=guess, rng=rng, label=pencil.label,
