@@ -41,12 +41,6 @@ __device__ __forceinline__ void cmac(double2& acc, const double2 a, const double
   acc.y = fma(a.x, b.y, acc.y);
   acc.y = fma(a.y, b.x, acc.y);
 }
-__device__ __forceinline__ void cmac_conj(double2& acc, const double2 a, const double2 b) {  // acc += a conj(b)
-  acc.x = fma(a.x, b.x, acc.x);
-  acc.x = fma(a.y, b.y, acc.x);
-  acc.y = fma(a.y, b.x, acc.y);
-  acc.y = fma(-a.x, b.y, acc.y);
-}
 
 // One warp per 16x16 diagonal block of the lower Cholesky factor L (g, ld
 // ldg): acc[i] = (first ? 1 : acc[i]) * L_ii, last[i] = L_ii (when given),
