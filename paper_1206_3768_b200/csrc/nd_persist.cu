@@ -67,11 +67,30 @@ __device__ void block_max_publish(double (&v)[4], int nv, int first, double* par
   __syncthreads();
 }
 
-// max over every CTA's partial j (max is exact: every thread gets the same bits)
-__device__ double grid_max(const double* part, int j) {
-  double r = 0.0;
-  for (int b = 0; b < (int)gridDim.x; ++b) r = pmax(r, __ldcg(part + b * 4 + j));
-  return r;
+// max over every CTA's four partials (max is exact: every thread gets the
+// same bits). One 16-byte-pair of loads per thread and a block reduction —
+// the per-thread loop over all CTAs' partials that stood here before cost
+// ~100 dependent-issue L2 loads per statistic and thread (~25 us per call).
+__device__ void grid_max4(const double* part, double (&out)[4], double* sh) {
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  if (threadIdx.x < gridDim.x) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = __ldcg(part + threadIdx.x * 4 + j);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double r = warp_max(v[j]);
+    if (lane == 0) sh[wid * 4 + j] = r;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    double r = 0.0;
+    for (int k = 0; k < ND_WARPS; ++k) r = pmax(r, sh[k * 4 + j]);
+    out[j] = r;
+  }
+  __syncthreads();
 }
 
 // X = I + S, S_ij = G_ij / (d_j - d_i); stats as nd_build_step_kernel
@@ -139,35 +158,52 @@ __device__ void gemm_phase(const double2* A, const double2* B, double2* C, int n
     if (epi == EPI_HERM && ti > tj) continue;  // (uniform over the CTA)
     const int r0 = ti * 16, c0 = tj * 16;
     __syncthreads();  // the previous tile's panel reads are done
-    if (!CONJ_A) {
-      for (int idx = threadIdx.x; idx < 16 * n; idx += blockDim.x) {
-        const int r = idx & 15, k = idx >> 4;
-        As[k * 17 + r] = r0 + r < n ? __ldcg(&A[(long long)k * n + r0 + r]) : make_double2(0.0, 0.0);
+    // Panels by cp.async (16-byte copies from L2, all in flight at once: the
+    // plain load -> store loops serialised ~10 L2 latencies per panel and
+    // were most of a phase's ~7 us); op(A) = A^H is conjugated in the MMA.
+    {
+      const int hi = threadIdx.x >> 4, lo = threadIdx.x & 15;  // 16 x 16 thread grid
+      if (!CONJ_A) {  // As[k][r] = A[r0 + r][k]: r contiguous in memory
+        for (int k = hi; k < n; k += 16)
+          cp_async16(&As[k * 17 + lo], &A[(long long)k * n + (r0 + lo < n ? r0 + lo : 0)], r0 + lo < n);
+      } else {        // As[k][r] = A[k][r0 + r] (conjugated later): k contiguous in memory
+        const bool ok = r0 + hi < n;
+        for (int k = lo; k < n; k += 16)
+          cp_async16(&As[k * 17 + hi], &A[(long long)(ok ? r0 + hi : 0) * n + k], ok);
       }
-    } else {
-      for (int idx = threadIdx.x; idx < 16 * n; idx += blockDim.x) {
-        const int k = idx % n, r = idx / n;
-        double2 v = r0 + r < n ? __ldcg(&A[(long long)(r0 + r) * n + k]) : make_double2(0.0, 0.0);
-        v.y = -v.y;
-        As[k * 17 + r] = v;
-      }
-    }
-    for (int idx = threadIdx.x; idx < 16 * n; idx += blockDim.x) {
-      const int k = idx % n, c = idx / n;
-      Bs[c * ldk + k] = c0 + c < n ? __ldcg(&B[(long long)(c0 + c) * n + k]) : make_double2(0.0, 0.0);
+      const bool okb = c0 + hi < n;
+      for (int k = lo; k < n; k += 16)  // Bs[c][k] = B[k][c0 + c]: k contiguous in memory
+        cp_async16(&Bs[hi * ldk + k], &B[(long long)(okb ? c0 + hi : 0) * n + k], okb);
+      cp_async_commit();
+      cp_async_wait<0>();
     }
     __syncthreads();
-    double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
-    for (int k0 = kb; k0 < ke; k0 += 4) {
-      const int k = k0 + t;
+    // two k4 steps per trip on independent accumulator pairs (the four DMMAs
+    // of a step form two dependent pairs; one pair of chains per step parity)
+    double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0}, cr1[2] = {0.0, 0.0}, ci1[2] = {0.0, 0.0};
+    auto frag = [&](int k, double2& a, double2& b) {
       const bool ok = k < ke;
-      const double2 a = ok ? As[k * 17 + sr + g] : make_double2(0.0, 0.0);
-      const double2 b = ok ? Bs[(sc + g) * ldk + k] : make_double2(0.0, 0.0);
-      dmma884(cr, a.x, b.x);
-      dmma884(cr, -a.y, b.y);
-      dmma884(ci, a.x, b.y);
-      dmma884(ci, a.y, b.x);
+      a = ok ? As[k * 17 + sr + g] : make_double2(0.0, 0.0);
+      b = ok ? Bs[(sc + g) * ldk + k] : make_double2(0.0, 0.0);
+      if (CONJ_A) a.y = -a.y;  // op(A) = A^H: the staged panel holds A
+    };
+    for (int k0 = kb; k0 < ke; k0 += 8) {
+      double2 a0, b0, a1, b1;
+      frag(k0 + t, a0, b0);
+      frag(k0 + 4 + t, a1, b1);  // (past ke: zeros)
+      dmma884(cr, a0.x, b0.x);
+      dmma884(cr1, a1.x, b1.x);
+      dmma884(ci, a0.x, b0.y);
+      dmma884(ci1, a1.x, b1.y);
+      dmma884(cr, -a0.y, b0.y);
+      dmma884(cr1, -a1.y, b1.y);
+      dmma884(ci, a0.y, b0.x);
+      dmma884(ci1, a1.y, b1.x);
     }
+    cr[0] += cr1[0];
+    cr[1] += cr1[1];
+    ci[0] += ci1[0];
+    ci[1] += ci1[1];
     if (kh) {
       red[(sub * 32 + lane) * 2 + 0] = make_double2(cr[0], cr[1]);
       red[(sub * 32 + lane) * 2 + 1] = make_double2(ci[0], ci[1]);
@@ -217,7 +253,10 @@ __global__ void __launch_bounds__(ND_THREADS) nd_persist_kernel(const NdParams p
   double2 *X = p.X, *W = p.W, *W2 = p.W2;
   build_phase(p.G0, n, X, p.part, sh);
   grid.sync();
-  double rmax = grid_max(p.part, 0), emax = grid_max(p.part, 1), dmax = grid_max(p.part, 2);
+  static_assert(kNumSMs <= ND_THREADS, "grid_max4 reads one CTA's partials per thread");
+  double gm[4];
+  grid_max4(p.part, gm, sh);
+  double rmax = gm[0], emax = gm[1], dmax = gm[2];
   double last_defect = 0.0;
   bool done = false;
   int it = 0;
@@ -261,10 +300,11 @@ __global__ void __launch_bounds__(ND_THREADS) nd_persist_kernel(const NdParams p
     grid.sync();
     build_phase(p.G, n, X, p.part, sh);
     grid.sync();
-    rmax = grid_max(p.part, 0);
-    emax = grid_max(p.part, 1);
-    dmax = grid_max(p.part, 2);
-    last_defect = grid_max(p.part, 3);
+    grid_max4(p.part, gm, sh);
+    rmax = gm[0];
+    emax = gm[1];
+    dmax = gm[2];
+    last_defect = gm[3];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     p.status[0] = done ? 1.0 : 0.0;
