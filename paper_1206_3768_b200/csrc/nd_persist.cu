@@ -94,7 +94,10 @@ __device__ void grid_max4(const double* part, double (&out)[4], double* sh) {
 }
 
 // X = I + S, S_ij = G_ij / (d_j - d_i); stats as nd_build_step_kernel
-__device__ void build_phase(const double2* g, int n, double2* x, double* part, double* sh) {
+// (g has leading dimension ldg; copy != nullptr: also copy g into it, ld n —
+// the first step reads the caller's matrix and keeps it as G0 in one pass)
+__device__ void build_phase(const double2* g, long long ldg, int n, double2* x, double* part, double* sh,
+                            double2* copy = nullptr) {
   const long long total = (long long)n * n;
   double st[4] = {0.0, 0.0, 0.0, 0.0};
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -103,10 +106,13 @@ __device__ void build_phase(const double2* g, int n, double2* x, double* part, d
     double2 out;
     if (i == j) {
       out = make_double2(1.0, 0.0);
-      st[2] = pmax(st[2], fabs(__ldcg(&g[(long long)i * n + i].x)));
+      const double2 d = __ldcg(&g[(long long)i * ldg + i]);
+      if (copy) copy[idx] = d;
+      st[2] = pmax(st[2], fabs(d.x));
     } else {
-      const double2 e = __ldcg(&g[(long long)j * n + i]);
-      const double gap = __ldcg(&g[(long long)j * n + j].x) - __ldcg(&g[(long long)i * n + i].x);
+      const double2 e = __ldcg(&g[(long long)j * ldg + i]);
+      if (copy) copy[idx] = e;
+      const double gap = __ldcg(&g[(long long)j * ldg + j].x) - __ldcg(&g[(long long)i * ldg + i].x);
       const double ae = hypot(e.x, e.y);
       st[1] = pmax(st[1], ae);
       if (ae == 0.0) {
@@ -243,15 +249,10 @@ __global__ void __launch_bounds__(ND_THREADS) nd_persist_kernel(const NdParams p
   cg::grid_group grid = cg::this_grid();
   const int n = p.n;
   const long long total = (long long)n * n;
-  // G0 <- A (the input is kept for the exact re-projection G = W^H G0 W)
-  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int j = (int)(idx / n), i = (int)(idx % n);
-    p.G0[idx] = p.ain[(long long)j * p.lda + i];
-  }
-  grid.sync();
+  // first measurement straight from the input, which is copied to G0 in the
+  // same pass (kept for the exact re-projection G = W^H G0 W)
   double2 *X = p.X, *W = p.W, *W2 = p.W2;
-  build_phase(p.G0, n, X, p.part, sh);
+  build_phase(p.ain, p.lda, n, X, p.part, sh, p.G0);
   grid.sync();
   static_assert(kNumSMs <= ND_THREADS, "grid_max4 reads one CTA's partials per thread");
   double gm[4];
@@ -298,7 +299,7 @@ __global__ void __launch_bounds__(ND_THREADS) nd_persist_kernel(const NdParams p
     grid.sync();
     gemm_phase<true>(W, X, p.G, n, EPI_HERM, nullptr, nullptr, dsm);     // G = W^H G0 W
     grid.sync();
-    build_phase(p.G, n, X, p.part, sh);
+    build_phase(p.G, n, n, X, p.part, sh);
     grid.sync();
     grid_max4(p.part, gm, sh);
     rmax = gm[0];
@@ -313,26 +314,28 @@ __global__ void __launch_bounds__(ND_THREADS) nd_persist_kernel(const NdParams p
     p.status[3] = emax;
   }
   if (!done) return;  // grid-uniform
-  // ascending eigenvalues (rank sort of the real diagonal, ties by index),
-  // the diagonal staged in shared memory first
+  // ascending eigenvalues (rank sort of the real diagonal, ties by index):
+  // every CTA ranks the whole diagonal in shared memory (n <= 256: one entry
+  // per thread), so the column gather needs no grid barrier after the sort
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
   double* diag = reinterpret_cast<double*>(dsm);
+  int* perm_s = reinterpret_cast<int*>(diag + kNdPersistMaxN);
   for (int i = threadIdx.x; i < n; i += blockDim.x) diag[i] = __ldcg(&p.G[(long long)i * n + i].x);
   __syncthreads();
-  for (int i = gt; i < n; i += nt) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const double di = diag[i];
     int rank = 0;
     for (int j = 0; j < n; ++j) {
       const double dj = diag[j];
       rank += (dj < di) || (dj == di && j < i);
     }
-    p.w[rank] = di;
-    p.perm[rank] = i;
+    perm_s[rank] = i;
+    if (blockIdx.x == 0) p.w[rank] = di;
   }
-  grid.sync();
+  __syncthreads();
   for (long long idx = gt; idx < total; idx += nt) {
     const int r = (int)(idx / n), i = (int)(idx % n);
-    p.aout[(long long)r * p.lda + i] = __ldcg(&W[(long long)__ldcg(&p.perm[r]) * n + i]);
+    p.aout[(long long)r * p.lda + i] = __ldcg(&W[(long long)perm_s[r] * n + i]);
   }
 }
 
