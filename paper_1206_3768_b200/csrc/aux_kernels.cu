@@ -142,8 +142,19 @@ __global__ void __launch_bounds__(kRedThreads) copy_norm2_kernel(const double2* 
   __shared__ double sh[32];
   __shared__ bool last;
   double acc = 0.0;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {  // four independent loads per trip
+    double2 a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = src[i + u * stride];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      dst[i + u * stride] = a[u];
+      acc = fma(a[u].x, a[u].x, fma(a[u].y, a[u].y, acc));
+    }
+  }
+  for (; i < n; i += stride) {
     const double2 a = src[i];
     dst[i] = a;
     acc = fma(a.x, a.x, fma(a.y, a.y, acc));
@@ -253,7 +264,27 @@ __global__ void colnorm_residual_kernel(const double2* __restrict__ hp, long lon
   const double2* a = hp + (long long)j * ldhp;
   const double2* b = p ? p + (long long)j * ldp : nullptr;
   double acc = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+  // (four rows per trip, their loads issued together: the one-row loop
+  // serialised an L2 latency per trip; same summation order per thread)
+  int i = threadIdx.x;
+  for (; i + 3 * (int)blockDim.x < n; i += 4 * blockDim.x) {
+    double2 x[4], y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = a[i + u * blockDim.x];
+    if (b) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) y[u] = b[i + u * blockDim.x];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (b) {
+        x[u].x = dsub(x[u].x, dmul(lam, y[u].x));
+        x[u].y = dsub(x[u].y, dmul(lam, y[u].y));
+      }
+      acc = fma(x[u].x, x[u].x, fma(x[u].y, x[u].y, acc));
+    }
+  }
+  for (; i < n; i += blockDim.x) {
     double2 x = a[i];
     if (b) {
       const double2 y = b[i];

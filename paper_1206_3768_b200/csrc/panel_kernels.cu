@@ -7,7 +7,7 @@
 // kernel each.
 //
 //   post_potrf  diag(L) bookkeeping of the acceptance test and the inverses
-//               of L's 16x16 diagonal blocks (one warp per block)
+//               of L's 16x16 diagonal blocks (one CTA per block)
 //   right<0>    Y <- Y L^-H   (block forward substitution over 16-column
 //               blocks; the diagonal solves are products with the inverted
 //               blocks, so nothing in the kernel is sequential per column)
@@ -42,35 +42,34 @@ __device__ __forceinline__ void cmac(double2& acc, const double2 a, const double
   acc.y = fma(a.y, b.x, acc.y);
 }
 
-// One warp per 16x16 diagonal block of the lower Cholesky factor L (g, ld
+// One CTA per 16x16 diagonal block of the lower Cholesky factor L (g, ld
 // ldg): acc[i] = (first ? 1 : acc[i]) * L_ii, last[i] = L_ii (when given),
 // linv[b][j*16 + i] = (L_bb^-1)[i][j] (lower; blocks past n padded with the
 // identity), *eps = 0 (the linearised pass accumulates its maximum there).
-__global__ void __launch_bounds__(32) panel_post_potrf_kernel(const double2* g, long long ldg, int n,
-                                                              double* acc, int first, double* last,
-                                                              double2* linv, double* eps) {
+__global__ void __launch_bounds__(256) panel_post_potrf_kernel(const double2* g, long long ldg, int n,
+                                                               double* acc, int first, double* last,
+                                                               double2* linv, double* eps) {
   __shared__ double2 Lb[16][17];
   __shared__ double2 Xb[16][17];
-  const int b = blockIdx.x, lane = threadIdx.x, b16 = b * 16;
-  for (int idx = lane; idx < 256; idx += 32) {
-    const int c = idx >> 4, r = idx & 15;
+  const int b = blockIdx.x, tid = threadIdx.x, b16 = b * 16;
+  {  // one tile element per thread (one L2 latency for the whole tile)
+    const int c = tid >> 4, r = tid & 15;
     const int gi = b16 + r, gj = b16 + c;
     double2 v = make_double2(r == c ? 1.0 : 0.0, 0.0);
     if (r >= c && gi < n) v = g[(long long)gj * ldg + gi];
     Lb[r][c] = v;
-    Xb[r][c] = make_double2(0.0, 0.0);
   }
-  __syncwarp();
-  if (lane < 16) {
-    const int i = b16 + lane;
+  __syncthreads();
+  if (tid < 16) {
+    const int i = b16 + tid;
     if (i < n) {
-      const double d = Lb[lane][lane].x;
+      const double d = Lb[tid][tid].x;
       acc[i] = (first ? 1.0 : acc[i]) * d;
       if (last) last[i] = d;
     }
-    // column j = lane of X = L_bb^-1 by forward substitution (real diagonal);
+    // column j = tid of X = L_bb^-1 by forward substitution (real diagonal);
     // the column stays in registers (fully unrolled: entries above j are zero)
-    const int j = lane;
+    const int j = tid;
     double2 x[16];
 #pragma unroll
     for (int i2 = 0; i2 < 16; ++i2) {
@@ -83,12 +82,9 @@ __global__ void __launch_bounds__(32) panel_post_potrf_kernel(const double2* g, 
 #pragma unroll
     for (int i2 = 0; i2 < 16; ++i2) Xb[i2][j] = x[i2];
   }
-  __syncwarp();
-  for (int idx = lane; idx < 256; idx += 32) {
-    const int j = idx >> 4, i = idx & 15;
-    linv[(long long)b * 256 + idx] = Xb[i][j];
-  }
-  if (b == 0 && lane == 0 && eps) *eps = 0.0;
+  __syncthreads();
+  linv[(long long)b * 256 + tid] = Xb[tid & 15][tid >> 4];
+  if (b == 0 && tid == 0 && eps) *eps = 0.0;
 }
 
 // shared memory (complex elements): the CTA's rows [np][XS], two factor-block
@@ -323,7 +319,7 @@ cudaError_t panel_post_potrf_launch(const double2* g, long long ldg, int n, doub
   if (n <= 0) return cudaSuccess;
   if (n > kPanelMaxW) return cudaErrorInvalidValue;
   note_launch();
-  panel_post_potrf_kernel<<<(n + 15) / 16, 32, 0, s>>>(g, ldg, n, acc, first ? 1 : 0, last, linv, eps);
+  panel_post_potrf_kernel<<<(n + 15) / 16, 256, 0, s>>>(g, ldg, n, acc, first ? 1 : 0, last, linv, eps);
   return cudaGetLastError();
 }
 
