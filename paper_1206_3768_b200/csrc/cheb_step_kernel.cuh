@@ -379,17 +379,50 @@ __global__ void __launch_bounds__(GROUPS* WM* WN * 32, MINB)
       for (int e = 0; e < NACC; ++e) acc[i][j][e] = 0.0;
 
   const int sg = sigma(g);
+  // Per 8-row block of the warp tile: ALL of its Ycur / Yprev reads first,
+  // then the arithmetic and the stores. Ynext may alias Yprev, so the
+  // compiler cannot move a later element's loads above an earlier element's
+  // store: element by element, the epilogue was a chain of 2 * MI * NI
+  // dependent L2 round trips per thread (ncu: 12 % long-scoreboard stalls).
+  // Each thread still reads an element before it overwrites it, and no two
+  // threads share an element. Same operation order as epilogue_store.
   auto epilogue = [&](const Cursor& c) {
 #pragma unroll
-    for (int i = 0; i < MI; ++i)
+    for (int i = 0; i < MI; ++i) {
+      const int row = c.m0 + wm * TM + i * 8 + sg;
+      double2 yc[NI][2], yp[NI][2];
 #pragma unroll
       for (int j = 0; j < NI; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int row = c.m0 + wm * TM + i * 8 + sg;
           const int col = c.n0 + wn * TN + j * 8 + sigma(2 * t + e);
-          if (row < p.m && col < p.w) epilogue_store(p, row, col, acc[i][j][e], acc[i][j][2 + e]);
+          const bool ok = row < p.m && col < p.w;
+          yc[j][e] = (ok && p.read_cur) ? p.ycur[(long long)col * p.ldc + row] : make_double2(0.0, 0.0);
+          yp[j][e] = (ok && p.read_prev) ? p.yprev[(long long)col * p.ldp + row] : make_double2(0.0, 0.0);
         }
+#pragma unroll
+      for (int j = 0; j < NI; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = c.n0 + wn * TN + j * 8 + sigma(2 * t + e);
+          if (!(row < p.m && col < p.w)) continue;
+          double tr = acc[i][j][e], ti = acc[i][j][2 + e];
+          if (p.read_cur) {
+            tr = dsub(tr, dmul(p.c, yc[j][e].x));
+            ti = dsub(ti, dmul(p.c, yc[j][e].y));
+          }
+          tr = dmul(p.alpha, tr);
+          ti = dmul(p.alpha, ti);
+          if (p.read_prev) {
+            tr = dsub(tr, dmul(p.beta, yp[j][e].x));
+            ti = dsub(ti, dmul(p.beta, yp[j][e].y));
+          }
+          const long long idx = (long long)col * p.ldn + row;
+          const double2 v = make_double2(tr, ti);
+          p.ynext[idx] = v;
+          for (int k = 0; k < p.npeer; ++k) p.ynext[idx + p.peer_shift[k]] = v;  // P2P store to peer k
+        }
+    }
   };
 
   // per-thread fragment byte offsets: row (warp base + sigma(g)) * 128, and
