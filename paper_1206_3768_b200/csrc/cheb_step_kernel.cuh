@@ -314,13 +314,18 @@ __global__ void __launch_bounds__(GROUPS* WM* WN * 32, MINB)
     if (c.j == e1 || c.j == e2 || c.j == e3) enter(c);
     else if (c.kk == kiters) set_tile(c, c.tile + ((c.j > e1 && c.j < e2) ? G : 1), 0);
   };
-  // one elected thread: arm the stage's barrier and issue its four TMA boxes
-  auto issue = [&](const Cursor& c, int stage) {
+  // one elected thread: arm the stage's barrier and issue its TMA boxes
+  // (what: 1 = the H panel, 2 = the Y panel, 3 = both; the barrier is armed
+  // with the whole stage's bytes by whichever part comes first)
+  auto issue = [&](const Cursor& c, int stage, int what = 3) {
     const unsigned dst = smem0 + stage * STAGE_BYTES, bar = full0 + 8 * stage;
     const int x = c.kk * (NH * BK);  // in doubles
-    mbar_expect_tx(bar, STAGE_BYTES);
+    if (what & 1) {
+      mbar_expect_tx(bar, STAGE_BYTES);
 #pragma unroll
-    for (int hh = 0; hh < NH; ++hh) tma_load_2d(dst + hh * A_BYTES, &tmA, bar, x + hh * BK, c.m0);
+      for (int hh = 0; hh < NH; ++hh) tma_load_2d(dst + hh * A_BYTES, &tmA, bar, x + hh * BK, c.m0);
+    }
+    if (!(what & 2)) return;
     if (p.kblk_slabs > 0) {  // rank-blocked Y: block q holds rows [q*kblk, (q+1)*kblk)
       const int q = c.kk / p.kblk_slabs, xl = (c.kk - q * p.kblk_slabs) * (NH * BK);
 #pragma unroll
@@ -343,6 +348,23 @@ __global__ void __launch_bounds__(GROUPS* WM* WN * 32, MINB)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  // producer cursor (the group's thread 0): the group's iterations are
+  // j = group, group + GROUPS, ... and stage j % STAGES is always its own
+  Cursor lc;
+  start(lc);
+  for (int k = 0; k < group; ++k) advance(lc);
+  // The H panels of the first ring stages are requested BEFORE the
+  // dependency wait: H does not depend on the previous step (under PDL the
+  // previous grid only writes Y and the stream-K scratch), so their HBM
+  // latency overlaps the previous step's tail instead of opening every
+  // launch with ~1 us of idle warps. The Y panels follow after the wait.
+  if (tid == 0) {
+    Cursor la = lc;
+    for (int s = group; s < STAGES && la.j < total; s += GROUPS) {
+      issue(la, s, 1);
+      for (int k = 0; k < GROUPS; ++k) advance(la);
+    }
+  }
   // Programmatic dependent launch: the launch and the prologue above overlap
   // the previous step's tail; nothing the previous grid writes (Ycur, Yprev,
   // the stream-K partials and flags) is touched before this wait returns
@@ -354,15 +376,9 @@ __global__ void __launch_bounds__(GROUPS* WM* WN * 32, MINB)
     p.trace[cta * 5 + 0] = gtimer();
     p.trace[cta * 5 + 4] = smid() | ((unsigned long long)blockIdx.x << 16);
   }
-
-  // producer cursor (the group's thread 0): the group's iterations are
-  // j = group, group + GROUPS, ... and stage j % STAGES is always its own
-  Cursor lc;
-  start(lc);
-  for (int k = 0; k < group; ++k) advance(lc);
   if (tid == 0) {
     for (int s = group; s < STAGES && lc.j < total; s += GROUPS) {
-      issue(lc, s);
+      issue(lc, s, 2);
       for (int k = 0; k < GROUPS; ++k) advance(lc);
     }
   }
