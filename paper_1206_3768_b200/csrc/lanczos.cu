@@ -165,7 +165,21 @@ __global__ void __launch_bounds__(LZ_THREADS) lanczos_coop_kernel(const LanczosP
     for (int j = tid; j <= it; j += LZ_THREADS) {
       const double2* vj = p.V + (long long)j * n;
       double cr = 0.0, ci = 0.0;
-      for (int i = r0; i < r1; ++i) {
+      int i = r0;
+      for (; i + 3 < r1; i += 4) {  // four rows' loads in flight (same summation order)
+        double2 a[4], rv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a[u] = vj[i + u];
+          rv[u] = p.r[i + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          cr = fma(a[u].x, rv[u].x, fma(a[u].y, rv[u].y, cr));
+          ci = fma(a[u].x, rv[u].y, fma(-a[u].y, rv[u].x, ci));
+        }
+      }
+      for (; i < r1; ++i) {
         const double2 a = vj[i], rv = p.r[i];
         cr = fma(a.x, rv.x, fma(a.y, rv.y, cr));
         ci = fma(a.x, rv.y, fma(-a.y, rv.x, ci));
@@ -177,7 +191,18 @@ __global__ void __launch_bounds__(LZ_THREADS) lanczos_coop_kernel(const LanczosP
     // ---- coef[j] = sum_b cpart[b][j] (block order), j spread over warps
     for (int j = b * LZ_WARPS + warp; j <= it; j += G * LZ_WARPS) {
       double cr = 0.0, ci = 0.0;
-      for (int bb = lane; bb < G; bb += 32) {
+      int bb = lane;
+      for (; bb + 96 < G; bb += 128) {  // four blocks' partials in flight per lane (same order)
+        double2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldcg(p.cpart + (long long)(bb + 32 * u) * p.k + j);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          cr += v[u].x;
+          ci += v[u].y;
+        }
+      }
+      for (; bb < G; bb += 32) {
         const double2 v = __ldcg(p.cpart + (long long)bb * p.k + j);
         cr += v.x;
         ci += v.y;
